@@ -1,0 +1,638 @@
+// extern "C" boundary of libmpmrb_b200.so (include/mpmrb_b200.h).
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "common.cuh"
+#include "contact.cuh"
+#include "internal.h"
+#include "sim.h"
+#include "solver.cuh"
+
+namespace mpmrb {
+
+static thread_local char g_err[1024] = "";
+
+int set_error(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int set_cuda_error(cudaError_t e, const char* expr, const char* file, int line) {
+  return set_error(MPMRB_E_CUDA, "CUDA error %s (%s) in %s at %s:%d", cudaGetErrorName(e),
+                   cudaGetErrorString(e), expr, file, line);
+}
+
+int DevBuf::grow(size_t need) {
+  if (need <= bytes && p) return MPMRB_OK;
+  if (need == 0) need = 16;
+  size_t nb = need + need / 4 + 256;
+  void* q = nullptr;
+  cudaError_t e = cudaMalloc(&q, nb);
+  if (e != cudaSuccess) {
+    set_cuda_error(e, "cudaMalloc", __FILE__, __LINE__);
+    return MPMRB_E_CUDA;
+  }
+  if (p) cudaFree(p);
+  p = q;
+  bytes = nb;
+  return MPMRB_OK;
+}
+
+void DevBuf::release() {
+  if (p) cudaFree(p);
+  p = nullptr;
+  bytes = 0;
+}
+
+static const char* code_name(int code) {
+  switch (code) {
+    case MPMRB_E_ALLOCATION: return "AllocationError";
+    case MPMRB_E_PLAN_EPOCH: return "PlanEpochError";
+    case MPMRB_E_INVALID: return "ValueError";
+    case MPMRB_E_NOT_DESCENT: return "line search needs a descent direction";
+    case MPMRB_E_NONFINITE: return "FloatingPointError";
+    case MPMRB_E_DIVERGED: return "SimulationDiverged";
+    case MPMRB_E_CAPACITY: return "capacity exceeded";
+    default: return "error";
+  }
+}
+
+int Ctx::check_status(const char* where) {
+  cudaError_t e = cudaStreamSynchronize(stream);
+  if (e != cudaSuccess) return set_cuda_error(e, "cudaStreamSynchronize", where, 0);
+  DevStatus h{};
+  e = cudaMemcpy(&h, status, sizeof(DevStatus), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return set_cuda_error(e, "cudaMemcpy(status)", where, 0);
+  if (h.code == 0) return MPMRB_OK;
+  cudaMemset(status, 0, sizeof(DevStatus));
+  return set_error(h.code, "%s: %s (site %d, index %lld)", where, code_name(h.code), h.detail,
+                   h.aux);
+}
+
+}  // namespace mpmrb
+
+using namespace mpmrb;
+
+struct mpmrb_ctx : public Ctx {};
+struct mpmrb_sim : public Sim {};
+
+#define CHECK_CTX(c) \
+  if (!(c)) return set_error(MPMRB_E_INVALID, "null context")
+
+extern "C" {
+
+int mpmrb_abi_version(void) { return MPMRB_ABI_VERSION; }
+
+const char* mpmrb_last_error(void) { return g_err; }
+
+int mpmrb_create(int device, mpmrb_ctx** out) {
+  if (!out) return set_error(MPMRB_E_INVALID, "out is null");
+  MPMRB_CUDA_OK(cudaSetDevice(device));
+  mpmrb_ctx* c = new (std::nothrow) mpmrb_ctx();
+  if (!c) return set_error(MPMRB_E_INVALID, "out of host memory");
+  c->device = device;
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  cudaError_t e = cudaMalloc(&c->status, sizeof(DevStatus));
+  if (e != cudaSuccess) {
+    delete c;
+    return set_cuda_error(e, "cudaMalloc(status)", __FILE__, __LINE__);
+  }
+  cudaMemset(c->status, 0, sizeof(DevStatus));
+  *out = c;
+  return MPMRB_OK;
+}
+
+int mpmrb_destroy(mpmrb_ctx* c) {
+  if (!c) return MPMRB_OK;
+  cudaStreamSynchronize(c->stream);
+  for (auto& b : c->scratch) b.release();
+  if (c->status) cudaFree(c->status);
+  delete c;
+  return MPMRB_OK;
+}
+
+int mpmrb_set_stream(mpmrb_ctx* c, void* s) {
+  CHECK_CTX(c);
+  c->stream = (cudaStream_t)s;
+  return MPMRB_OK;
+}
+
+int mpmrb_sync(mpmrb_ctx* c) {
+  CHECK_CTX(c);
+  return c->check_status("mpmrb_sync");
+}
+
+int64_t mpmrb_launch_count(mpmrb_ctx* c) { return c ? (int64_t)c->launches : 0; }
+
+// ------------------------------------------------------------------ binning
+
+int mpmrb_sort_plan(mpmrb_ctx* c, const double* x, int64_t n, double h, uint16_t* keys,
+                    int64_t* perm, int64_t* inv_perm, uint16_t* bin_keys, int64_t* bin_starts,
+                    int64_t* bin_of, int64_t* n_bins_host) {
+  CHECK_CTX(c);
+  if (n < 0 || !(h > 0)) return set_error(MPMRB_E_INVALID, "bad n or h");
+  if (c->scratch[SS_COUNT].grow(64)) return MPMRB_E_CUDA;
+  int* nb = c->scratch[SS_COUNT].as<int>();
+  int rc = launch_sort_plan(*c, x, n, h, keys, (long long*)perm, (long long*)inv_perm, bin_keys,
+                            (long long*)bin_starts, (long long*)bin_of, nb);
+  if (rc) return rc;
+  int hb = 0;
+  MPMRB_CUDA_OK(cudaMemcpyAsync(&hb, nb, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  rc = c->check_status("build_sort_plan");
+  if (rc) return rc;
+  *n_bins_host = hb;
+  return MPMRB_OK;
+}
+
+int mpmrb_plan_staleness(mpmrb_ctx* c, const uint16_t* plan_keys, const double* x, int64_t n,
+                         double h, double* out_host) {
+  CHECK_CTX(c);
+  if (c->scratch[SS_COUNT].grow(64)) return MPMRB_E_CUDA;
+  unsigned long long* cnt = c->scratch[SS_COUNT].as<unsigned long long>();
+  int rc = launch_staleness(*c, plan_keys, x, n, h, cnt);
+  if (rc) return rc;
+  unsigned long long hc = 0;
+  MPMRB_CUDA_OK(cudaMemcpyAsync(&hc, cnt, 8, cudaMemcpyDeviceToHost, c->stream));
+  rc = c->check_status("plan_staleness");
+  if (rc) return rc;
+  *out_host = n > 0 ? (double)hc / (double)n : 0.0;
+  return MPMRB_OK;
+}
+
+int mpmrb_base_cells(mpmrb_ctx* c, const double* x, int64_t n, double h, int64_t* cells) {
+  CHECK_CTX(c);
+  return launch_base_cells(*c, x, n, h, (long long*)cells);
+}
+
+int mpmrb_grid_allocate(mpmrb_ctx* c, const double* x, int64_t n, double h, int64_t* block_keys,
+                        int64_t block_cap, uint64_t* hash_keys, int32_t* hash_vals,
+                        int64_t hash_cap, int64_t* n_blocks_host) {
+  CHECK_CTX(c);
+  if (!(h > 0)) return set_error(MPMRB_E_INVALID, "grid spacing h must be positive");
+  if (hash_cap < 2 || (hash_cap & (hash_cap - 1)) || hash_cap < 2 * block_cap)
+    return set_error(MPMRB_E_INVALID, "hash_cap must be a power of two >= 2*block_cap");
+  if (c->scratch[SS_KEYS].grow(8 * (block_cap + 1)) || c->scratch[SS_COUNT].grow(64))
+    return MPMRB_E_CUDA;
+  int* nb = c->scratch[SS_COUNT].as<int>();
+  int rc = launch_grid_build(*c, x, n, h, (long long*)block_keys, block_cap,
+                             (unsigned long long*)hash_keys, (int*)hash_vals, hash_cap,
+                             c->scratch[SS_KEYS].as<long long>(), nb);
+  if (rc) return rc;
+  int hb = 0;
+  MPMRB_CUDA_OK(cudaMemcpyAsync(&hb, nb, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  rc = c->check_status("SparseGrid.allocate");
+  *n_blocks_host = hb;
+  return rc;
+}
+
+int mpmrb_node_ids(mpmrb_ctx* c, const mpmrb_grid_view* g, const int64_t* coords, int64_t m,
+                   int64_t* ids) {
+  CHECK_CTX(c);
+  int rc = launch_node_ids(*c, *g, (const long long*)coords, m, (long long*)ids);
+  if (rc) return rc;
+  return c->check_status("SparseGrid.node_ids");
+}
+
+int mpmrb_build_stencil(mpmrb_ctx* c, const mpmrb_grid_view* g, const double* x, int64_t n,
+                        double* weights, int64_t* nodes, double* dpos) {
+  CHECK_CTX(c);
+  int rc = launch_build_stencil(*c, *g, x, n, weights, (long long*)nodes, dpos);
+  if (rc) return rc;
+  return c->check_status("build_stencil");
+}
+
+// ------------------------------------------------------------------ transfer
+
+int mpmrb_scatter_reduce(mpmrb_ctx* c, const int64_t* node_ids, const double* values,
+                         int64_t rows, int64_t k, int64_t nch, int64_t n_out, double* out) {
+  CHECK_CTX(c);
+  int rc = launch_scatter_reduce(*c, (const long long*)node_ids, values, rows, k, nch, n_out, out);
+  if (rc) return rc;
+  return c->check_status("scatter_reduce");
+}
+
+static int upload_mats(Ctx& c, const mpmrb_material* mats_host, int n) {
+  if (c.scratch[SS_MATS].grow(sizeof(mpmrb_material) * (n > 0 ? n : 1))) return MPMRB_E_CUDA;
+  if (n > 0)
+    MPMRB_CUDA_OK(cudaMemcpyAsync(c.scratch[SS_MATS].p, mats_host, sizeof(mpmrb_material) * n,
+                                  cudaMemcpyHostToDevice, c.stream));
+  return MPMRB_OK;
+}
+
+int mpmrb_compute_stresses(mpmrb_ctx* c, const double* f, const int64_t* mid, int64_t n,
+                           const mpmrb_material* mats_host, int32_t n_mats, double* tau) {
+  CHECK_CTX(c);
+  int rc = upload_mats(*c, mats_host, n_mats);
+  if (rc) return rc;
+  rc = launch_stresses(*c, f, (const long long*)mid, n, c->scratch[SS_MATS].as<mpmrb_material>(),
+                       n_mats, tau);
+  if (rc) return rc;
+  return c->check_status("compute_stresses");
+}
+
+static GridDev grid_dev(const mpmrb_grid_view* g) {
+  return GridDev{(const unsigned long long*)g->hash_keys, (const int*)g->hash_vals,
+                 (unsigned)(g->hash_cap - 1), g->h};
+}
+
+static ParticlesDev particles_dev(const mpmrb_particles* p) {
+  return ParticlesDev{p->x, p->v, p->f, p->c, p->mass, p->volume0,
+                      (const long long*)p->material_id, p->plastic, p->n};
+}
+
+int mpmrb_p2g(mpmrb_ctx* c, const mpmrb_grid_view* g, const mpmrb_particles* p,
+              const mpmrb_material* mats_host, int32_t n_mats, double dt, double* mass,
+              double* mom_apic, double* mom_force) {
+  CHECK_CTX(c);
+  long long N = g->n_blocks * kNodesPerBlock;
+  MPMRB_CUDA_OK(cudaMemsetAsync(mass, 0, 8 * N, c->stream));
+  MPMRB_CUDA_OK(cudaMemsetAsync(mom_apic, 0, 24 * N, c->stream));
+  MPMRB_CUDA_OK(cudaMemsetAsync(mom_force, 0, 24 * N, c->stream));
+  int rc = upload_mats(*c, mats_host, n_mats);
+  if (rc) return rc;
+  rc = launch_p2g(*c, grid_dev(g), particles_dev(p), c->scratch[SS_MATS].as<mpmrb_material>(),
+                  n_mats, dt, mass, mom_apic, mom_force);
+  if (rc) return rc;
+  return c->check_status("particle_to_grid");
+}
+
+int mpmrb_grid_update(mpmrb_ctx* c, int64_t n_nodes, const double* mass, const double* mom_apic,
+                      const double* mom_force, const double* g, double dt, uint8_t* active,
+                      double* v_k, double* v_star) {
+  CHECK_CTX(c);
+  int rc = launch_grid_update(*c, n_nodes, nullptr, mass, mom_apic, mom_force, g[0], g[1], g[2],
+                              dt, active, v_k, v_star, nullptr, nullptr);
+  if (rc) return rc;
+  return c->check_status("grid_update");
+}
+
+int mpmrb_g2p(mpmrb_ctx* c, const mpmrb_grid_view* g, const mpmrb_particles* p,
+              const mpmrb_material* mats_host, int32_t n_mats, const double* v_next, double dt,
+              int64_t* n_clamped_host) {
+  CHECK_CTX(c);
+  if (c->scratch[SS_COUNT].grow(64)) return MPMRB_E_CUDA;
+  unsigned long long* cl = c->scratch[SS_COUNT].as<unsigned long long>();
+  MPMRB_CUDA_OK(cudaMemsetAsync(cl, 0, 8, c->stream));
+  int rc = upload_mats(*c, mats_host, n_mats);
+  if (rc) return rc;
+  rc = launch_g2p(*c, grid_dev(g), particles_dev(p), c->scratch[SS_MATS].as<mpmrb_material>(),
+                  n_mats, v_next, dt, cl, nullptr);
+  if (rc) return rc;
+  unsigned long long h = 0;
+  MPMRB_CUDA_OK(cudaMemcpyAsync(&h, cl, 8, cudaMemcpyDeviceToHost, c->stream));
+  rc = c->check_status("grid_to_particle");
+  if (n_clamped_host) *n_clamped_host = (int64_t)h;
+  return rc;
+}
+
+int mpmrb_clamp_degenerate(mpmrb_ctx* c, const double* f, int64_t n, double* f_out,
+                           int64_t* n_bad_host) {
+  CHECK_CTX(c);
+  if (c->scratch[SS_COUNT].grow(64)) return MPMRB_E_CUDA;
+  unsigned long long* nb = c->scratch[SS_COUNT].as<unsigned long long>();
+  int rc = launch_clamp(*c, f, n, f_out, nb);
+  if (rc) return rc;
+  unsigned long long h = 0;
+  MPMRB_CUDA_OK(cudaMemcpyAsync(&h, nb, 8, cudaMemcpyDeviceToHost, c->stream));
+  rc = c->check_status("clamp_degenerate");
+  *n_bad_host = (int64_t)h;
+  return rc;
+}
+
+// ------------------------------------------------------------------ contacts
+
+int mpmrb_contact_model(mpmrb_ctx* c, const double* vc, const double* phi, const double* gl,
+                        const double* mu, int64_t n, double k, double tau_d, double eps_v,
+                        double dt, double* energy, double* grad, double* hess) {
+  CHECK_CTX(c);
+  int rc = launch_contact_model(*c, vc, phi, gl, mu, n, dt * (dt + tau_d) * k, dt + tau_d, eps_v,
+                                energy, grad, hess);
+  if (rc) return rc;
+  return c->check_status("contact_model");
+}
+
+int mpmrb_sdf_query(mpmrb_ctx* c, const mpmrb_geom* geom_host, const double* pts, int64_t n,
+                    double* phi, double* normal, double* witness) {
+  CHECK_CTX(c);
+  if (c->scratch[SS_GEOMS].grow(sizeof(mpmrb_geom))) return MPMRB_E_CUDA;
+  MPMRB_CUDA_OK(cudaMemcpyAsync(c->scratch[SS_GEOMS].p, geom_host, sizeof(mpmrb_geom),
+                                cudaMemcpyHostToDevice, c->stream));
+  int rc = launch_sdf_query(*c, c->scratch[SS_GEOMS].as<mpmrb_geom>(), pts, n, phi, normal,
+                            witness);
+  if (rc) return rc;
+  return c->check_status("query_signed_distance");
+}
+
+int mpmrb_contact_frames(mpmrb_ctx* c, const double* normals, int64_t n, double* frames) {
+  CHECK_CTX(c);
+  int rc = launch_frames(*c, normals, n, frames);
+  if (rc) return rc;
+  return c->check_status("contact_frames");
+}
+
+int mpmrb_detect_contacts(mpmrb_ctx* c, const double* x, int64_t n, const mpmrb_geom* geoms_host,
+                          int32_t n_geoms, double margin, int32_t* bias_stamp,
+                          double* bias_store, int32_t epoch_stamp, int64_t cap,
+                          int64_t* particle, int64_t* body, int64_t* geom, double* phi,
+                          double* normal, double* witness, double* frames, double* bias,
+                          double* mu, int64_t* n_contacts_host) {
+  CHECK_CTX(c);
+  if (c->scratch[SS_GEOMS].grow(sizeof(mpmrb_geom) * (n_geoms > 0 ? n_geoms : 1)) ||
+      c->scratch[SS_TMP0].grow(4 * (n + 1)) || c->scratch[SS_TMP1].grow(4 * (n + 1)) ||
+      c->scratch[SS_TMP2].grow(4 * (cap + 1)) || c->scratch[SS_COUNT].grow(64))
+    return MPMRB_E_CUDA;
+  if (n_geoms > 0)
+    MPMRB_CUDA_OK(cudaMemcpyAsync(c->scratch[SS_GEOMS].p, geoms_host,
+                                  sizeof(mpmrb_geom) * n_geoms, cudaMemcpyHostToDevice,
+                                  c->stream));
+  int* cnt_total = c->scratch[SS_COUNT].as<int>();
+  int* epoch_dev = cnt_total + 4;
+  MPMRB_CUDA_OK(cudaMemcpyAsync(epoch_dev, &epoch_stamp, 4, cudaMemcpyHostToDevice, c->stream));
+  ContactArrays ca{};
+  ca.particle = c->scratch[SS_TMP2].as<int>();
+  ca.particle64 = (long long*)particle;
+  ca.body64 = (long long*)body;
+  ca.geom64 = (long long*)geom;
+  ca.phi = phi;
+  ca.normal = normal;
+  ca.witness = witness;
+  ca.frames = frames;
+  ca.bias = bias;
+  ca.mu = mu;
+  int rc = launch_detect(*c, x, n, c->scratch[SS_GEOMS].as<mpmrb_geom>(), n_geoms, margin,
+                         c->scratch[SS_TMP0].as<int>(), c->scratch[SS_TMP1].as<int>(), cnt_total,
+                         c->scratch[SS_TILE], cap, bias_stamp, bias_store, epoch_dev, ca);
+  if (rc) return rc;
+  int tot = 0;
+  MPMRB_CUDA_OK(cudaMemcpyAsync(&tot, cnt_total, 4, cudaMemcpyDeviceToHost, c->stream));
+  rc = c->check_status("detect_contacts");
+  *n_contacts_host = tot;
+  return rc;
+}
+
+int mpmrb_contact_velocities(mpmrb_ctx* c, const int64_t* nodes, const double* w,
+                             const double* frames, const double* bias, int64_t nc,
+                             const double* v_grid, double* vc) {
+  CHECK_CTX(c);
+  int rc = launch_contact_velocities(*c, (const long long*)nodes, w, frames, bias, nc, v_grid, vc);
+  if (rc) return rc;
+  return c->check_status("contact_velocities");
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ solver
+
+namespace mpmrb {
+namespace {
+__global__ void k_problem_layout(const long long* __restrict__ nodes, const double* __restrict__ w,
+                                 long long nc, int* __restrict__ cnodes, double* __restrict__ cw) {
+  long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= nc * 27) return;
+  long long c = e / 27, k = e % 27;
+  cnodes[k * nc + c] = (int)nodes[e];
+  cw[k * nc + c] = w[e];
+}
+}  // namespace
+}  // namespace mpmrb
+
+extern "C" int mpmrb_qn_solve(mpmrb_ctx* c, const mpmrb_problem* pr,
+                              const mpmrb_solver_params* sp, const double* v0, double* v,
+                              double* gamma, double* objective, double* residual,
+                              double* threshold, double* alpha, mpmrb_solve_report* rep) {
+  CHECK_CTX(c);
+  long long nd = pr->n_nodes, nc = pr->n_contacts;
+  long long ncc = nc > 0 ? nc : 1, ndd = nd > 0 ? nd : 1;
+  int rc = 0;
+  rc |= c->scratch[SS_SOLVER0].grow(4 * 27 * ncc);           // cnodes
+  rc |= c->scratch[SS_SOLVER1].grow(8 * 27 * ncc);           // cw
+  rc |= c->scratch[SS_SOLVER2].grow(8 * 3 * ndd * 3);        // g, jt, dv
+  rc |= c->scratch[SS_SOLVER3].grow(8 * 6 * ndd);            // H6
+  rc |= c->scratch[SS_SOLVER4].grow(8 * 3 * ncc * 2);        // vc, dvc
+  rc |= c->scratch[SS_SOLVER5].grow(8 * 2 * 8 * kMaxSolverCtas);  // partials
+  rc |= c->scratch[SS_SOLVER6].grow(256);                    // bar, sizes, SolveOut
+  if (rc) return MPMRB_E_CUDA;
+  char* misc = c->scratch[SS_SOLVER6].as<char>();
+  unsigned* bar = (unsigned*)misc;
+  int* sizes = (int*)(misc + 16);
+  SolveOut* so = (SolveOut*)(misc + 64);
+  MPMRB_CUDA_OK(cudaMemsetAsync(misc, 0, 256, c->stream));
+  int hs[2] = {(int)nd, (int)nc};
+  MPMRB_CUDA_OK(cudaMemcpyAsync(sizes, hs, sizeof(hs), cudaMemcpyHostToDevice, c->stream));
+  if (nc > 0) {
+    k_problem_layout<<<grid_for(nc * 27, 256), 256, 0, c->stream>>>(
+        (const long long*)pr->nodes, pr->w, nc, c->scratch[SS_SOLVER0].as<int>(),
+        c->scratch[SS_SOLVER1].as<double>());
+    c->launches++;
+  }
+  SolverArgs a{};
+  a.nd_dev = sizes;
+  a.nc_dev = sizes + 1;
+  a.nc_cap = nc;
+  a.m = pr->m;
+  a.v_star = pr->v_star;
+  a.v0 = v0 ? v0 : pr->v_init;
+  a.cnodes = c->scratch[SS_SOLVER0].as<int>();
+  a.cw = c->scratch[SS_SOLVER1].as<double>();
+  a.frames = pr->frames;
+  a.bias = pr->bias;
+  a.phi = pr->phi;
+  a.mu = pr->mu;
+  a.gamma_lag = pr->gamma_lag;
+  a.K = pr->dt * (pr->dt + pr->tau_d) * pr->stiffness;  // contact_model.py:42-43
+  a.den = pr->dt + pr->tau_d;
+  a.eps_v = pr->eps_v;
+  a.eps_a = sp->eps_a;
+  a.eps_r = sp->eps_r;
+  a.ls_tol = sp->ls_tol;
+  a.max_iters = sp->max_iters;
+  a.ls_max = sp->ls_max_iters;
+  a.skip_if_no_contacts = 0;
+  a.force_ctas = 0;
+  double* sv2 = c->scratch[SS_SOLVER2].as<double>();
+  a.v = v;
+  a.g = sv2;
+  a.jt = sv2 + 3 * ndd;
+  a.dv = sv2 + 6 * ndd;
+  a.H6 = c->scratch[SS_SOLVER3].as<double>();
+  a.vc = c->scratch[SS_SOLVER4].as<double>();
+  a.dvc = a.vc + 3 * ncc;
+  a.partials = c->scratch[SS_SOLVER5].as<double>();
+  a.bar = bar;
+  a.gamma = gamma;
+  a.tr_obj = objective;
+  a.tr_res = residual;
+  a.tr_thr = threshold;
+  a.tr_alpha = alpha;
+  a.out = so;
+  a.act = nullptr;
+  a.v_next_full = nullptr;
+  const char* force = getenv("MPMRB_SOLVER_CTAS");
+  if (force) a.force_ctas = atoi(force);
+  rc = launch_qn_solve(*c, a, 0);
+  if (rc) return rc;
+  SolveOut h{};
+  MPMRB_CUDA_OK(cudaMemcpyAsync(&h, so, sizeof(SolveOut), cudaMemcpyDeviceToHost, c->stream));
+  rc = c->check_status("quasi_newton_solve");
+  if (rc) return rc;
+  rep->converged = h.converged;
+  rep->iterations = h.iterations;
+  rep->ls_evals = h.ls_evals;
+  rep->regularized = h.regularized;
+  rep->status = h.status;
+  if (h.status == MPMRB_E_NOT_DESCENT)
+    return set_error(MPMRB_E_NOT_DESCENT, "line search needs a descent direction");
+  if (h.status == MPMRB_E_NONFINITE)
+    return set_error(MPMRB_E_NONFINITE, "Hessian block not SPD after regularization");
+  if (h.status_flags & 1)
+    return set_error(MPMRB_E_NONFINITE, "contact solve produced non-finite velocities");
+  return MPMRB_OK;
+}
+
+// ------------------------------------------------------------------ sim
+
+extern "C" {
+
+int mpmrb_sim_create(mpmrb_ctx* c, mpmrb_sim** out) {
+  CHECK_CTX(c);
+  mpmrb_sim* s = new (std::nothrow) mpmrb_sim();
+  if (!s) return set_error(MPMRB_E_INVALID, "out of host memory");
+  s->ctx = c;
+  if (getenv("MPMRB_NO_GRAPH")) s->use_graph = false;
+  const char* force = getenv("MPMRB_SOLVER_CTAS");
+  if (force) s->force_ctas = atoi(force);
+  *out = s;
+  return MPMRB_OK;
+}
+
+int mpmrb_sim_destroy(mpmrb_sim* s) {
+  if (!s) return MPMRB_OK;
+  cudaStreamSynchronize(s->ctx->stream);
+  DevBuf* bufs[] = {&s->b_mats, &s->b_geoms, &s->b_counters, &s->b_misc, &s->b_solveout,
+                    &s->b_bar, &s->b_partials, &s->b_dyn, &s->b_accum, &s->b_probe_hk,
+                    &s->b_probe_hv, &s->b_probe_uk, &s->b_probe_bk, &s->b_plankeys, &s->b_stats,
+                    &s->b_hkeys, &s->b_hvals, &s->b_ukeys, &s->b_bkeys, &s->b_mass, &s->b_mom,
+                    &s->b_vk, &s->b_vstar, &s->b_vnext, &s->b_active, &s->b_wcount, &s->b_woff,
+                    &s->b_act, &s->b_remap, &s->b_mc, &s->b_vstarc, &s->b_vkc, &s->b_cnt,
+                    &s->b_offs, &s->b_cpart, &s->b_cbody, &s->b_cphi, &s->b_cmu, &s->b_cgl,
+                    &s->b_cnormal, &s->b_cwit, &s->b_cbias, &s->b_cframes, &s->b_cnodes,
+                    &s->b_cw, &s->b_sv, &s->b_sg, &s->b_sjt, &s->b_sH, &s->b_sdv, &s->b_svc,
+                    &s->b_sdvc, &s->b_gamma, &s->b_gworld, &s->b_tiles, &s->b_bias_stamp,
+                    &s->b_bias_store};
+  for (DevBuf* b : bufs) b->release();
+  delete s;
+  return MPMRB_OK;
+}
+
+int mpmrb_sim_set_particles(mpmrb_sim* s, const mpmrb_particles* p) {
+  if (!s || !p) return set_error(MPMRB_E_INVALID, "null argument");
+  ParticlesDev np = particles_dev(p);
+  if (std::memcmp(&np, &s->p, sizeof(np)) != 0) s->invalidate();
+  s->p = np;
+  s->have_particles = true;
+  return MPMRB_OK;
+}
+
+int mpmrb_sim_set_materials(mpmrb_sim* s, const mpmrb_material* mats, int32_t n) {
+  if (!s) return set_error(MPMRB_E_INVALID, "null sim");
+  if (s->b_mats.grow(sizeof(mpmrb_material) * (n > 0 ? n : 1))) return MPMRB_E_CUDA;
+  if (n > 0)
+    MPMRB_CUDA_OK(cudaMemcpyAsync(s->b_mats.p, mats, sizeof(mpmrb_material) * n,
+                                  cudaMemcpyHostToDevice, s->ctx->stream));
+  if (n != s->nmat) s->invalidate();
+  s->nmat = n;
+  return MPMRB_OK;
+}
+
+int mpmrb_sim_set_geoms(mpmrb_sim* s, const mpmrb_geom* geoms, int32_t n, int32_t nbody) {
+  if (!s) return set_error(MPMRB_E_INVALID, "null sim");
+  if (nbody > 32) return set_error(MPMRB_E_INVALID, "at most 32 bodies in the fused path");
+  void* old = s->b_geoms.p;
+  if (s->b_geoms.grow(sizeof(mpmrb_geom) * (n > 0 ? n : 1))) return MPMRB_E_CUDA;
+  if (old != s->b_geoms.p || n != s->ngeom || nbody != s->nbody) s->invalidate();
+  if (n > 0)
+    MPMRB_CUDA_OK(cudaMemcpyAsync(s->b_geoms.p, geoms, sizeof(mpmrb_geom) * n,
+                                  cudaMemcpyHostToDevice, s->ctx->stream));
+  s->ngeom = n;
+  s->nbody = nbody;
+  return MPMRB_OK;
+}
+
+int mpmrb_sim_set_params(mpmrb_sim* s, double h, double dt_s, const double* g, double k,
+                         double tau_d, double eps_v, double margin,
+                         const mpmrb_solver_params* sp) {
+  if (!s) return set_error(MPMRB_E_INVALID, "null sim");
+  double K = dt_s * (dt_s + tau_d) * k;
+  bool same = s->have_params && s->h == h && s->dt_s == dt_s && s->gravity[0] == g[0] &&
+              s->gravity[1] == g[1] && s->gravity[2] == g[2] && s->K == K &&
+              s->den == dt_s + tau_d && s->eps_v == eps_v && s->margin == margin &&
+              std::memcmp(&s->sp, sp, sizeof(*sp)) == 0;
+  if (!same) s->invalidate();
+  s->h = h;
+  s->dt_s = dt_s;
+  s->gravity[0] = g[0];
+  s->gravity[1] = g[1];
+  s->gravity[2] = g[2];
+  s->K = K;
+  s->den = dt_s + tau_d;
+  s->eps_v = eps_v;
+  s->margin = margin;
+  s->sp = *sp;
+  s->have_params = true;
+  return MPMRB_OK;
+}
+
+int mpmrb_sim_begin_step(mpmrb_sim* s, int64_t epoch, int32_t n_substeps) {
+  if (!s) return set_error(MPMRB_E_INVALID, "null sim");
+  return s->begin_step(epoch, n_substeps);
+}
+
+int mpmrb_sim_substep(mpmrb_sim* s) {
+  if (!s) return set_error(MPMRB_E_INVALID, "null sim");
+  return s->substep();
+}
+
+int mpmrb_sim_end_step(mpmrb_sim* s, mpmrb_step_stats* st, double* impulses) {
+  if (!s) return set_error(MPMRB_E_INVALID, "null sim");
+  int rc = s->end_step(st, impulses);
+  if (rc) return rc;
+  if (st->status)
+    return set_error(st->status, "advance_step: %s (site %d, index %lld)",
+                     st->status == MPMRB_E_DIVERGED ? "SimulationDiverged" : "device error",
+                     st->status_detail, (long long)st->status_aux);
+  return MPMRB_OK;
+}
+
+double mpmrb_sim_staleness(mpmrb_sim* s) { return s ? s->staleness : 0.0; }
+
+int mpmrb_sim_last_grid(mpmrb_sim* s, int64_t* nb, const int64_t** block_keys,
+                        const double** mass, const double** v_star, const double** v_next) {
+  if (!s) return set_error(MPMRB_E_INVALID, "null sim");
+  int hb = 0;
+  MPMRB_CUDA_OK(cudaStreamSynchronize(s->ctx->stream));
+  MPMRB_CUDA_OK(cudaMemcpy(&hb, s->b_counters.p, 4, cudaMemcpyDeviceToHost));
+  *nb = hb;
+  *block_keys = (const int64_t*)s->b_bkeys.p;
+  *mass = (const double*)s->b_mass.p;
+  *v_star = (const double*)s->b_vstar.p;
+  *v_next = (const double*)s->b_vnext.p;
+  return MPMRB_OK;
+}
+
+int mpmrb_sim_last_contacts(mpmrb_sim* s, int64_t* n, const int32_t** particle,
+                            const double** gamma_world) {
+  if (!s) return set_error(MPMRB_E_INVALID, "null sim");
+  int hc[3] = {0, 0, 0};
+  MPMRB_CUDA_OK(cudaStreamSynchronize(s->ctx->stream));
+  MPMRB_CUDA_OK(cudaMemcpy(hc, s->b_counters.p, sizeof(hc), cudaMemcpyDeviceToHost));
+  *n = hc[2];
+  *particle = (const int32_t*)s->b_cpart.p;
+  *gamma_world = (const double*)s->b_gworld.p;
+  return MPMRB_OK;
+}
+
+}  // extern "C"

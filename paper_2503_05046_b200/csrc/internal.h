@@ -1,0 +1,125 @@
+// Host-side internals shared by the .cu translation units (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstddef>
+#include <cstdint>
+
+#include "../../include/mpmrb_b200.h"
+
+namespace mpmrb {
+
+struct DevStatus;
+
+int set_error(int code, const char* fmt, ...);
+int set_cuda_error(cudaError_t e, const char* expr, const char* file, int line);
+
+// A grow-only device buffer.  Growth frees the old allocation, so it must not
+// happen while a captured graph still references it (sim code re-captures).
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  int grow(size_t need);  // returns MPMRB_OK or MPMRB_E_CUDA
+  void release();
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+struct Ctx {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  DevStatus* status = nullptr;   // device
+  DevStatus* status_host = nullptr;  // pinned mirror
+  long long launches = 0;
+  DevBuf scratch[24];
+  int check_status(const char* where);  // sync + read + clear device status
+};
+
+// Scratch slot ids for API-level (non-fused) calls.
+enum ScratchSlot {
+  SS_TILE = 0, SS_TILE2, SS_HIST, SS_KEYS, SS_TMP0, SS_TMP1, SS_TMP2, SS_TMP3, SS_COUNT,
+  SS_SOLVER0, SS_SOLVER1, SS_SOLVER2, SS_SOLVER3, SS_SOLVER4, SS_SOLVER5, SS_SOLVER6,
+  SS_SOLVER7, SS_SOLVER8, SS_MATS, SS_GEOMS, SS_PROBLEM, SS_HOSTINFO
+};
+
+inline unsigned grid_for(long long n, int threads) {
+  long long b = (n + threads - 1) / threads;
+  if (b < 1) b = 1;
+  return (unsigned)b;
+}
+
+// ---- launchers (each returns MPMRB_OK or an error code) --------------------
+// scan.cu
+int scan_exclusive_i32(Ctx& c, const int* in, int* out, long long n_cap, const int* n_dev,
+                       int* total_dev, DevBuf& tiles);
+int scan_exclusive_i64(Ctx& c, const long long* in, long long* out, long long n, long long* total_dev,
+                       DevBuf& tiles);
+
+// binning.cu
+int launch_base_cells(Ctx& c, const double* x, long long n, double h, long long* cells);
+int launch_sort_plan(Ctx& c, const double* x, long long n, double h, uint16_t* keys,
+                     long long* perm, long long* inv_perm, uint16_t* bin_keys,
+                     long long* bin_starts, long long* bin_of, int* n_bins_dev);
+int launch_staleness(Ctx& c, const uint16_t* plan_keys, const double* x, long long n,
+                     double h, unsigned long long* changed_dev);
+// Block discovery into a hash table; writes sorted keys and hash values.
+// counters_dev[0] receives nb.  Capacity overflow raises MPMRB_E_CAPACITY in
+// the device status (aux = needed count), range errors MPMRB_E_ALLOCATION.
+int launch_grid_build(Ctx& c, const double* x, long long n, double h, long long* block_keys,
+                      long long block_cap, unsigned long long* hkeys, int* hvals,
+                      long long hash_cap, long long* ukeys_scratch, int* nb_dev);
+int launch_node_ids(Ctx& c, const mpmrb_grid_view& g, const long long* coords, long long m,
+                    long long* ids);
+int launch_build_stencil(Ctx& c, const mpmrb_grid_view& g, const double* x, long long n,
+                         double* weights, long long* nodes, double* dpos);
+
+// mpm.cu
+int launch_scatter_reduce(Ctx& c, const long long* ids, const double* vals, long long rows,
+                          long long k, long long nch, long long n_out, double* out);
+int launch_stresses(Ctx& c, const double* f, const long long* mid, long long n,
+                    const mpmrb_material* mats_dev, int nmat, double* tau);
+struct ParticlesDev {
+  double* x;
+  double* v;
+  double* f;
+  double* c;
+  const double* mass;
+  const double* vol0;
+  const long long* mid;
+  double* plastic;
+  long long n;
+};
+struct GridDev {
+  const unsigned long long* hkeys;
+  const int* hvals;
+  unsigned mask;
+  double h;
+};
+int launch_p2g(Ctx& c, const GridDev& g, const ParticlesDev& p, const mpmrb_material* mats_dev,
+               int nmat, double dt, double* mass, double* mom_apic, double* mom_force);
+int launch_grid_update(Ctx& c, long long n_nodes_cap, const int* nb_dev, const double* mass,
+                       const double* mom_apic, const double* mom_force, double gx, double gy,
+                       double gz, double dt, unsigned char* active, double* v_k, double* v_star,
+                       double* v_next_or_null, int* block_active_count_or_null);
+int launch_g2p(Ctx& c, const GridDev& g, const ParticlesDev& p, const mpmrb_material* mats_dev,
+               int nmat, const double* v_next, double dt, unsigned long long* clamped_dev,
+               int* health_dev);
+
+int launch_clamp(Ctx& c, const double* f, long long n, double* out, unsigned long long* nbad);
+int launch_health(Ctx& c, const double* x, const double* v, long long n, double h, int* bad);
+
+// contact.cu
+int launch_contact_model(Ctx& c, const double* vc, const double* phi, const double* gl,
+                         const double* mu, long long n, double K, double den, double eps_v,
+                         double* energy, double* grad, double* hess);
+int launch_sdf_query(Ctx& c, const mpmrb_geom* g_dev, const double* pts, long long n, double* phi,
+                     double* normal, double* witness);
+int launch_frames(Ctx& c, const double* normals, long long n, double* frames);
+int launch_contact_velocities(Ctx& c, const long long* nodes, const double* w,
+                              const double* frames, const double* bias, long long nc,
+                              const double* v_grid, double* vc);
+
+}  // namespace mpmrb

@@ -1,0 +1,334 @@
+// Particle <-> grid transfers on sm_100a (float64).
+//
+//  * k_p2g   : stress (polar / Hencky) + 27-node x 7-channel APIC/MLS scatter
+//              (mpm.py:66-99, materials.py:113-122).  One thread per particle,
+//              stencil kept in registers (never materialised, unlike the
+//              reference's (n,27,3) arrays), float64 REDG atomics into the
+//              node channels.
+//  * k_grid_update : v_k, v*, active mask (mpm.py:102-115) + per-warp active
+//              counts for the ordered active-node compaction (solver.py:203).
+//  * k_g2p   : gather, APIC C, advection, F update, singular-value clamp
+//              (mpm.py:118-138, materials.py:86-110), Drucker-Prager return map
+//              for sand, divergence check (coupling.py:153-165).
+#include "common.cuh"
+#include "internal.h"
+#include "svd3.cuh"
+
+namespace mpmrb {
+
+namespace {
+
+__device__ __forceinline__ M3 particle_stress(const M3& f, const mpmrb_material& m) {
+  return (m.kind == MPMRB_MAT_SAND) ? kirchhoff_hencky(f, m.mu, m.lam)
+                                    : kirchhoff_fixed_corotated(f, m.mu, m.lam);
+}
+
+__global__ void k_scatter_reduce(const long long* __restrict__ ids, const double* __restrict__ vals,
+                                 long long rows, long long k, long long nch, long long n_out,
+                                 double* __restrict__ out, DevStatus* st) {
+  long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= rows * k) return;
+  long long node = ids[e];
+  if (node < 0 || node >= n_out) {
+    raise_status(st, MPMRB_E_INVALID, 10, e);
+    return;
+  }
+  for (long long ch = 0; ch < nch; ++ch) atomicAdd(&out[node * nch + ch], vals[e * nch + ch]);
+}
+
+__global__ void k_stresses(const double* __restrict__ f, const long long* __restrict__ mid,
+                           long long n, const mpmrb_material* __restrict__ mats, int nmat,
+                           double* __restrict__ tau, DevStatus* st) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  long long m = mid[i];
+  if (m < 0 || m >= nmat) {
+    raise_status(st, MPMRB_E_INVALID, 11, i);
+    return;
+  }
+  M3 t = particle_stress(m3_load(f + 9 * i), mats[m]);
+  m3_store(tau + 9 * i, t);
+}
+
+__global__ void __launch_bounds__(128) k_p2g(GridDev g, ParticlesDev p,
+                                             const mpmrb_material* __restrict__ mats, int nmat,
+                                             double dt, double* __restrict__ gmass,
+                                             double* __restrict__ mom_apic,
+                                             double* __restrict__ mom_force, DevStatus* st) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= p.n) return;
+  const double h = g.h;
+  double xp[3] = {p.x[3 * i], p.x[3 * i + 1], p.x[3 * i + 2]};
+  Stencil1 s;
+  make_stencil1(xp, h, s);
+  StencilBlocks sb;
+  if (!resolve_blocks(s, g.hkeys, g.hvals, g.mask, sb)) {
+    raise_status(st, MPMRB_E_ALLOCATION, 20, i);
+    return;
+  }
+  long long mid = p.mid[i];
+  if (mid < 0 || mid >= nmat) {
+    raise_status(st, MPMRB_E_INVALID, 21, i);
+    return;
+  }
+  const double m = p.mass[i];
+  M3 tau = particle_stress(m3_load(p.f + 9 * i), mats[mid]);
+  const double dinv = 4.0 / (h * h);
+  const double coef = (-dt * dinv) * p.vol0[i];
+  M3 S, mC;
+  M3 C = m3_load(p.c + 9 * i);
+#pragma unroll
+  for (int k = 0; k < 9; ++k) {
+    S.a[k] = coef * tau.a[k];
+    mC.a[k] = m * C.a[k];
+  }
+  double mv[3] = {m * p.v[3 * i], m * p.v[3 * i + 1], m * p.v[3 * i + 2]};
+#pragma unroll 1
+  for (int ox = 0; ox < 3; ++ox) {
+    const double dx = (ox - s.fx[0]) * h;
+#pragma unroll 1
+    for (int oy = 0; oy < 3; ++oy) {
+      const double dy = (oy - s.fx[1]) * h;
+      const double wxy = s.w[0][ox] * s.w[1][oy];
+#pragma unroll
+      for (int oz = 0; oz < 3; ++oz) {
+        const double dz = (oz - s.fx[2]) * h;
+        const double w = wxy * s.w[2][oz];
+        const int node = stencil_node(s, sb, ox, oy, oz);
+        atomicAdd(&gmass[node], w * m);
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          double a = mv[d] + (mC(d, 0) * dx + mC(d, 1) * dy + mC(d, 2) * dz);
+          double b = S(d, 0) * dx + S(d, 1) * dy + S(d, 2) * dz;
+          atomicAdd(&mom_apic[3 * node + d], w * a);
+          atomicAdd(&mom_force[3 * node + d], w * b);
+        }
+      }
+    }
+  }
+}
+
+// One thread per allocated node (mpm.py:102-115).  n_nodes = 64*nb from the
+// device (nb_dev) when given.
+__global__ void k_grid_update(long long n_cap, const int* __restrict__ nb_dev,
+                              const double* __restrict__ mass, const double* __restrict__ mom_apic,
+                              const double* __restrict__ mom_force, double gx, double gy,
+                              double gz, double dt, unsigned char* __restrict__ active,
+                              double* __restrict__ v_k, double* __restrict__ v_star,
+                              double* __restrict__ v_next, int* __restrict__ warp_count) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  long long n = nb_dev ? (long long)(*nb_dev) * kNodesPerBlock : n_cap;
+  if (n > n_cap) n = n_cap;
+  bool act = false;
+  if (i < n) {
+    double m = mass[i];
+    act = m > kMassEps;
+    double vk[3] = {0.0, 0.0, 0.0}, vs[3] = {0.0, 0.0, 0.0};
+    if (act) {
+      double inv_m = 1.0 / m;
+      double g[3] = {gx, gy, gz};
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        vk[d] = mom_apic[3 * i + d] * inv_m;
+        vs[d] = (mom_apic[3 * i + d] + mom_force[3 * i + d]) * inv_m + dt * g[d];
+      }
+    }
+    active[i] = act ? 1 : 0;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      v_k[3 * i + d] = vk[d];
+      v_star[3 * i + d] = vs[d];
+      if (v_next) v_next[3 * i + d] = vs[d];  // zero-contact passthrough (coupling.py:125-129)
+    }
+  }
+  if (warp_count) {
+    unsigned b = __ballot_sync(0xffffffffu, act);
+    if ((threadIdx.x & 31) == 0 && (i - (threadIdx.x & 31)) < n_cap)
+      warp_count[i >> 5] = __popc(b);
+  }
+}
+
+__global__ void __launch_bounds__(128) k_g2p(GridDev g, ParticlesDev p,
+                                             const mpmrb_material* __restrict__ mats, int nmat,
+                                             const double* __restrict__ v_next, double dt,
+                                             unsigned long long* __restrict__ clamped,
+                                             int* __restrict__ health, DevStatus* st) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  bool was_clamped = false;
+  if (i < p.n) {
+    const double h = g.h;
+    double xp[3] = {p.x[3 * i], p.x[3 * i + 1], p.x[3 * i + 2]};
+    Stencil1 s;
+    make_stencil1(xp, h, s);
+    StencilBlocks sb;
+    if (!resolve_blocks(s, g.hkeys, g.hvals, g.mask, sb)) {
+      raise_status(st, MPMRB_E_ALLOCATION, 30, i);
+    } else {
+      double vn[3] = {0.0, 0.0, 0.0};
+      M3 B;
+#pragma unroll
+      for (int k = 0; k < 9; ++k) B.a[k] = 0.0;
+#pragma unroll 1
+      for (int ox = 0; ox < 3; ++ox) {
+        const double dx = (ox - s.fx[0]) * h;
+#pragma unroll 1
+        for (int oy = 0; oy < 3; ++oy) {
+          const double dy = (oy - s.fx[1]) * h;
+          const double wxy = s.w[0][ox] * s.w[1][oy];
+#pragma unroll
+          for (int oz = 0; oz < 3; ++oz) {
+            const double dz = (oz - s.fx[2]) * h;
+            const double w = wxy * s.w[2][oz];
+            const int node = stencil_node(s, sb, ox, oy, oz);
+            double wv[3];
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+              wv[d] = w * v_next[3 * node + d];
+              vn[d] += wv[d];
+              B(d, 0) += wv[d] * dx;
+              B(d, 1) += wv[d] * dy;
+              B(d, 2) += wv[d] * dz;
+            }
+          }
+        }
+      }
+      const double dinv = 4.0 / (h * h);
+      M3 C;
+#pragma unroll
+      for (int k = 0; k < 9; ++k) C.a[k] = dinv * B.a[k];
+      M3 A = m3_identity();
+#pragma unroll
+      for (int k = 0; k < 9; ++k) A.a[k] += dt * C.a[k];
+      M3 F = m3_mul(A, m3_load(p.f + 9 * i));
+      if (!(m3_det(F) > 0.0) || !m3_finite(F)) {
+        F = clamp_singular_values(F);
+        was_clamped = true;
+      }
+      long long mid = p.mid[i];
+      if (mid >= 0 && mid < nmat && mats[mid].kind == MPMRB_MAT_SAND) {
+        double dq = 0.0;
+        F = dp_return_map(F, mats[mid].mu, mats[mid].lam, mats[mid].dp_alpha, &dq);
+        if (p.plastic) p.plastic[i] += dq;
+      }
+      double xn[3];
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        xn[d] = xp[d] + dt * vn[d];
+        p.x[3 * i + d] = xn[d];
+        p.v[3 * i + d] = vn[d];
+      }
+      m3_store(p.c + 9 * i, C);
+      m3_store(p.f + 9 * i, F);
+      if (health) {
+        const double lim = h * (double)((1 << 20) - 2);
+        bool ok = true;
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+          ok &= isfinite(xn[d]) && isfinite(vn[d]) && fabs(xn[d]) < lim;
+        if (!ok) atomicOr(health, 1);
+      }
+    }
+  }
+  if (clamped) {
+    unsigned b = __ballot_sync(0xffffffffu, was_clamped);
+    if ((threadIdx.x & 31) == 0 && b) atomicAdd(clamped, (unsigned long long)__popc(b));
+  }
+}
+
+__global__ void k_clamp(const double* __restrict__ f, long long n, double* __restrict__ out,
+                        unsigned long long* __restrict__ nbad) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  bool bad = false;
+  if (i < n) {
+    M3 F = m3_load(f + 9 * i);
+    bad = !(m3_det(F) > 0.0) || !m3_finite(F);
+    if (bad) F = clamp_singular_values(F);
+    m3_store(out + 9 * i, F);
+  }
+  unsigned b = __ballot_sync(0xffffffffu, bad);
+  if ((threadIdx.x & 31) == 0 && b) atomicAdd(nbad, (unsigned long long)__popc(b));
+}
+
+// coupling.py:153-165: finite x, v and |x| < h (2^20 - 2)
+__global__ void k_health(const double* __restrict__ x, const double* __restrict__ v, long long n,
+                         double lim, int* __restrict__ bad) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= 3 * n) return;
+  double xi = x[i], vi = v[i];
+  if (!(isfinite(xi) && isfinite(vi) && fabs(xi) < lim)) atomicOr(bad, 1);
+}
+
+}  // namespace
+
+int launch_health(Ctx& c, const double* x, const double* v, long long n, double h, int* bad) {
+  if (n == 0) return MPMRB_OK;
+  k_health<<<grid_for(3 * n, 256), 256, 0, c.stream>>>(x, v, n, h * (double)((1 << 20) - 2), bad);
+  c.launches++;
+  MPMRB_CUDA_OK(cudaGetLastError());
+  return MPMRB_OK;
+}
+
+int launch_clamp(Ctx& c, const double* f, long long n, double* out, unsigned long long* nbad) {
+  MPMRB_CUDA_OK(cudaMemsetAsync(nbad, 0, 8, c.stream));
+  if (n == 0) return MPMRB_OK;
+  k_clamp<<<grid_for(n, 128), 128, 0, c.stream>>>(f, n, out, nbad);
+  c.launches++;
+  MPMRB_CUDA_OK(cudaGetLastError());
+  return MPMRB_OK;
+}
+
+int launch_scatter_reduce(Ctx& c, const long long* ids, const double* vals, long long rows,
+                          long long k, long long nch, long long n_out, double* out) {
+  MPMRB_CUDA_OK(cudaMemsetAsync(out, 0, sizeof(double) * n_out * nch, c.stream));
+  if (rows * k == 0) return MPMRB_OK;
+  k_scatter_reduce<<<grid_for(rows * k, 256), 256, 0, c.stream>>>(ids, vals, rows, k, nch, n_out,
+                                                                  out, c.status);
+  c.launches++;
+  MPMRB_CUDA_OK(cudaGetLastError());
+  return MPMRB_OK;
+}
+
+int launch_stresses(Ctx& c, const double* f, const long long* mid, long long n,
+                    const mpmrb_material* mats_dev, int nmat, double* tau) {
+  if (n == 0) return MPMRB_OK;
+  k_stresses<<<grid_for(n, 128), 128, 0, c.stream>>>(f, mid, n, mats_dev, nmat, tau, c.status);
+  c.launches++;
+  MPMRB_CUDA_OK(cudaGetLastError());
+  return MPMRB_OK;
+}
+
+int launch_p2g(Ctx& c, const GridDev& g, const ParticlesDev& p, const mpmrb_material* mats_dev,
+               int nmat, double dt, double* mass, double* mom_apic, double* mom_force) {
+  if (p.n == 0) return MPMRB_OK;
+  k_p2g<<<grid_for(p.n, 128), 128, 0, c.stream>>>(g, p, mats_dev, nmat, dt, mass, mom_apic,
+                                                  mom_force, c.status);
+  c.launches++;
+  MPMRB_CUDA_OK(cudaGetLastError());
+  return MPMRB_OK;
+}
+
+int launch_grid_update(Ctx& c, long long n_cap, const int* nb_dev, const double* mass,
+                       const double* mom_apic, const double* mom_force, double gx, double gy,
+                       double gz, double dt, unsigned char* active, double* v_k, double* v_star,
+                       double* v_next, int* warp_count) {
+  if (n_cap == 0) return MPMRB_OK;
+  k_grid_update<<<grid_for(n_cap, 256), 256, 0, c.stream>>>(n_cap, nb_dev, mass, mom_apic,
+                                                            mom_force, gx, gy, gz, dt, active,
+                                                            v_k, v_star, v_next, warp_count);
+  c.launches++;
+  MPMRB_CUDA_OK(cudaGetLastError());
+  return MPMRB_OK;
+}
+
+int launch_g2p(Ctx& c, const GridDev& g, const ParticlesDev& p, const mpmrb_material* mats_dev,
+               int nmat, const double* v_next, double dt, unsigned long long* clamped_dev,
+               int* health_dev) {
+  if (p.n == 0) return MPMRB_OK;
+  k_g2p<<<grid_for(p.n, 128), 128, 0, c.stream>>>(g, p, mats_dev, nmat, v_next, dt, clamped_dev,
+                                                  health_dev, c.status);
+  c.launches++;
+  MPMRB_CUDA_OK(cudaGetLastError());
+  return MPMRB_OK;
+}
+
+}  // namespace mpmrb

@@ -1,0 +1,119 @@
+"""Constitutive models.
+
+* elastic: fixed-corotated hyperelasticity, tau = 2 mu (F - R) F^T +
+  lam (J - 1) J I (reference materials.py:1-122) — the stress is evaluated
+  inside the fused P2G kernel (csrc/svd3.cuh: kirchhoff_fixed_corotated).
+* sand (NEW, parity unpinned — the reference declares plasticity out of scope,
+  SPEC.md:8,98,111): Hencky St.Venant–Kirchhoff stress plus a Drucker–Prager
+  return map applied in the G2P kernel (Klár et al. 2016; oracle/plasticity.py
+  restates it in NumPy).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+
+SIGMA_MIN = 0.05  # materials.py:21
+
+
+@dataclass(frozen=True)
+class Material:
+    youngs_modulus: float
+    poisson_ratio: float
+    density: float
+    model: str = "elastic"          # "elastic" | "sand"
+    friction_angle: float = 30.0    # degrees, sand only
+
+    def __post_init__(self):
+        if not (self.youngs_modulus > 0.0):
+            raise ValueError(f"youngs_modulus must be > 0, got {self.youngs_modulus}")
+        if not (0.0 <= self.poisson_ratio < 0.5):
+            raise ValueError(f"poisson_ratio must be in [0, 0.5), got {self.poisson_ratio}")
+        if not (self.density > 0.0):
+            raise ValueError(f"density must be > 0, got {self.density}")
+        if self.model not in ("elastic", "sand"):
+            raise ValueError(f"unknown material model {self.model!r}")
+        if self.model == "sand" and not (0.0 < self.friction_angle < 90.0):
+            raise ValueError("friction_angle must be in (0, 90) degrees")
+
+    @property
+    def lame(self) -> tuple[float, float]:
+        """(mu, lambda) from (E, nu) (materials.py:40-46)."""
+        e, nu = self.youngs_modulus, self.poisson_ratio
+        return e / (2.0 * (1.0 + nu)), e * nu / ((1.0 + nu) * (1.0 - 2.0 * nu))
+
+    @property
+    def dp_alpha(self) -> float:
+        s = np.sin(np.deg2rad(self.friction_angle))
+        return float(np.sqrt(2.0 / 3.0) * 2.0 * s / (3.0 - s))
+
+    def to_struct(self) -> _lib.Material:
+        m = _lib.Material()
+        m.kind = _lib.MAT_SAND if self.model == "sand" else _lib.MAT_ELASTIC
+        m.mu, m.lam = self.lame
+        m.dp_alpha = self.dp_alpha if self.model == "sand" else 0.0
+        return m
+
+
+def material_table(materials) -> tuple:
+    arr = (_lib.Material * max(1, len(materials)))()
+    for i, m in enumerate(materials):
+        arr[i] = m.to_struct()
+    return arr, len(materials)
+
+
+def det3(m) -> torch.Tensor:
+    """Column triple-product determinant of (...,3,3) (materials.py:49-54)."""
+    m = _lib.as_dev(m)
+    return torch.einsum("...i,...i->...", m[..., :, 0],
+                        torch.linalg.cross(m[..., :, 1], m[..., :, 2], dim=-1))
+
+
+def kirchhoff_stress_batch(f, mu: float, lam: float) -> torch.Tensor:
+    """tau(F) for a (n,3,3) stack of one elastic material (materials.py:113-122)."""
+    f = _lib.as_dev(f)
+    shape = f.shape
+    f = f.reshape(-1, 3, 3).contiguous()
+    mat = _lib.Material()
+    mat.kind, mat.mu, mat.lam = _lib.MAT_ELASTIC, float(mu), float(lam)
+    tab = (_lib.Material * 1)(mat)
+    mid = torch.zeros(f.shape[0], dtype=torch.int64, device=f.device)
+    tau = torch.empty_like(f)
+    _lib.check(_lib.lib().mpmrb_compute_stresses(_lib.ctx(), _lib.ptr(f), _lib.ptr(mid),
+                                                 f.shape[0], tab, 1, _lib.ptr(tau)))
+    return tau.reshape(shape)
+
+
+def compute_stress(f, material: Material) -> torch.Tensor:
+    """Kirchhoff stress of one deformation gradient (materials.py:125-136)."""
+    fn = np.asarray(_lib.to_numpy(f), dtype=np.float64)
+    if fn.shape != (3, 3):
+        raise ValueError(f"expected a (3, 3) deformation gradient, got {fn.shape}")
+    if not np.isfinite(fn).all():
+        raise ValueError("deformation gradient has non-finite entries")
+    if not np.linalg.det(fn) > 0.0:
+        raise ValueError("deformation gradient must have positive determinant")
+    tab, n = material_table([material])
+    fd = _lib.as_dev(fn).reshape(1, 3, 3).contiguous()
+    mid = torch.zeros(1, dtype=torch.int64, device=fd.device)
+    tau = torch.empty_like(fd)
+    _lib.check(_lib.lib().mpmrb_compute_stresses(_lib.ctx(), _lib.ptr(fd), _lib.ptr(mid), 1, tab,
+                                                 n, _lib.ptr(tau)))
+    return tau[0]
+
+
+def clamp_degenerate(f) -> tuple[torch.Tensor, int]:
+    """Clamp singular values at SIGMA_MIN where det(F) <= 0 or non-finite
+    (materials.py:86-110).  Returns (repaired stack, number repaired)."""
+    fd = _lib.as_dev(f).reshape(-1, 3, 3).contiguous()
+    out = torch.empty_like(fd)
+    nbad = C.c_int64()
+    _lib.check(_lib.lib().mpmrb_clamp_degenerate(_lib.ctx(), _lib.ptr(fd), fd.shape[0],
+                                                 _lib.ptr(out), C.byref(nbad)))
+    return out, int(nbad.value)

@@ -1,0 +1,156 @@
+"""Synthetic scenes of the benchmark configurations as plain
+JSON-able dicts, and the builder that turns one into a ``SimState``.
+
+This is NOT the reference's YAML front-end (scene.py is out of scope); it is
+the minimal scene vocabulary the tests, smoke() and bench.py share.  The dict
+format is the one tests/golden/make_golden.py records.
+"""
+
+from __future__ import annotations
+
+import copy
+
+import numpy as np
+
+from .bodies import GeomAttachment, RigidBody, Trajectory
+from .contact_model import ContactParams
+from .coupling import SimState, StepConfig
+from .geometry import Box, Capsule, HalfSpace, Sphere
+from .materials import Material
+from .particles import concatenate, seed_box
+from .solver import SolverParams
+
+
+def _shape(g):
+    if g["shape"] == "halfspace":
+        n = np.asarray(g["normal"], dtype=np.float64)
+        return HalfSpace(normal=tuple(n / np.linalg.norm(n)), offset=float(g["offset"]))
+    if g["shape"] == "sphere":
+        return Sphere(radius=float(g["radius"]))
+    if g["shape"] == "box":
+        return Box(half_extents=tuple(float(a) for a in g["half_extents"]))
+    return Capsule(radius=float(g["radius"]), half_length=float(g["half_length"]))
+
+
+def build_bodies(scene) -> list:
+    out = []
+    for b in scene["bodies"]:
+        geoms = [GeomAttachment(shape=_shape(g), position=np.asarray(g["position"], float),
+                                quat=np.asarray(g["quat"], float), mu=float(g["mu"]))
+                 for g in b["geoms"]]
+        traj = None
+        if b.get("trajectory"):
+            t = b["trajectory"]
+            quats = t.get("quats") or [[1.0, 0.0, 0.0, 0.0]] * len(t["times"])
+            traj = Trajectory(times=np.asarray(t["times"]), positions=np.asarray(t["positions"]),
+                              quats=np.asarray(quats))
+        kw = {}
+        if not b["kinematic"]:
+            kw = dict(mass=float(b["mass"]), inertia_body=np.asarray(b["inertia"], float))
+        body = RigidBody(name=b["name"], kinematic=bool(b["kinematic"]), geoms=geoms,
+                         position=np.asarray(b["position"], float),
+                         quat=np.asarray(b["quat"], float),
+                         v=np.asarray(b.get("v", [0, 0, 0]), float),
+                         omega=np.asarray(b.get("omega", [0, 0, 0]), float),
+                         trajectory=traj, **kw)
+        if body.kinematic and traj is not None:
+            body.position, body.quat, body.v, body.omega = traj.sample(0.0)
+        out.append(body)
+    return out
+
+
+def build_materials(scene) -> list:
+    return [Material(m["E"], m["nu"], m["rho"], model=m.get("model", "elastic"),
+                     friction_angle=m.get("friction_angle", 30.0)) for m in scene["materials"]]
+
+
+def build_particles(scene):
+    mats = build_materials(scene)
+    sets = [seed_box(np.asarray(v["center"]), np.asarray(v["half"]), scene["h"],
+                     mats[v["material"]], material_id=v["material"], particles_per_cell=v["ppc"],
+                     jitter=v["jitter"], velocity=tuple(v["velocity"]), seed=v["seed"])
+            for v in scene["volumes"]]
+    return concatenate(sets)
+
+
+def build_state(scene, particles=None) -> SimState:
+    c = scene["contact"]
+    s = scene["solver"]
+    sp = SolverParams(eps_r=s.get("eps_r", 5e-2), max_iters=s.get("max_iters", 500))
+    return SimState(particles=particles if particles is not None else build_particles(scene),
+                    materials=build_materials(scene), bodies=build_bodies(scene), h=scene["h"],
+                    step=StepConfig(dt=scene["dt"], substeps=scene["substeps"],
+                                    gravity=tuple(scene["gravity"])),
+                    contact_params=ContactParams(stiffness=c["stiffness"], tau_d=c["tau_d"],
+                                                 eps_v=c["eps_v"], margin=c.get("margin")),
+                    solver_params=sp)
+
+
+# ------------------------------------------------------------------ configs
+
+def _floor(mu=0.5):
+    return dict(name="floor", kinematic=True, position=[0, 0, 0], quat=[1, 0, 0, 0],
+                geoms=[dict(shape="halfspace", normal=[0, 0, 1], offset=0.0, position=[0, 0, 0],
+                            quat=[1, 0, 0, 0], mu=mu)])
+
+
+def smoke_scene() -> dict:
+    """~500 particles on a floor, pressed by a descending kinematic sphere."""
+    return dict(h=0.01, dt=1e-3, substeps=2, gravity=[0, 0, -9.81],
+                contact=dict(stiffness=1e5, tau_d=1e-3, eps_v=1e-4, margin=None),
+                solver=dict(eps_r=5e-2),
+                materials=[dict(E=5e4, nu=0.3, rho=1000.0)],
+                volumes=[dict(center=[0, 0, 0.0205], half=[0.02, 0.02, 0.02], material=0, ppc=8,
+                              jitter=1.0, seed=0, velocity=[0, 0, -0.1])],
+                bodies=[_floor(0.8),
+                        dict(name="ball", kinematic=True, position=[0, 0, 0.07], quat=[1, 0, 0, 0],
+                             trajectory=dict(times=[0.0, 1.0], positions=[[0, 0, 0.065],
+                                                                          [0, 0, -0.235]]),
+                             geoms=[dict(shape="sphere", radius=0.025, position=[0, 0, 0],
+                                         quat=[1, 0, 0, 0], mu=0.5)])])
+
+
+def elastic_cube_scene() -> dict:
+    """C1: 8,000-particle elastic cube dropped on a kinematic ground box
+    (the reference CPU scene, 100 rigid steps)."""
+    dt = 1e-3
+    return dict(h=0.01, dt=dt, substeps=10, gravity=[0, 0, -9.81], steps=100,
+                contact=dict(stiffness=1e5, tau_d=dt, eps_v=1e-4, margin=None),
+                solver=dict(eps_r=5e-2),
+                materials=[dict(E=1e5, nu=0.3, rho=1000.0)],
+                volumes=[dict(center=[0, 0, 0.06], half=[0.05, 0.05, 0.05], material=0, ppc=8,
+                              jitter=1.0, seed=0, velocity=[0, 0, 0])],
+                bodies=[dict(name="ground", kinematic=True, position=[0, 0, -0.05],
+                             quat=[1, 0, 0, 0],
+                             geoms=[dict(shape="box", half_extents=[0.3, 0.3, 0.05],
+                                         position=[0, 0, 0], quat=[1, 0, 0, 0], mu=0.5)])])
+
+
+def sand_pile_scene(half=(0.2, 0.2, 0.1), h=0.01, model="sand") -> dict:
+    """C2: Drucker–Prager sand block (256k particles at the default size) on a
+    floor, pushed by a kinematic box starting 5 mm clear at +0.2 m/s
+    (DP parameters proposed there: 30 deg, c = 0, E = 3.5e5)."""
+    dt = 2e-3
+    hx, hy, hz = half
+    push_half = (0.05, hy, 0.05)
+    x0 = -hx - 0.005 - push_half[0]
+    z0 = push_half[2] + 0.005
+    return dict(h=h, dt=dt, substeps=10, gravity=[0, 0, -9.81],
+                contact=dict(stiffness=1e5, tau_d=dt, eps_v=1e-4, margin=None),
+                solver=dict(eps_r=5e-2),
+                materials=[dict(E=3.5e5, nu=0.3, rho=1500.0, model=model, friction_angle=30.0)],
+                volumes=[dict(center=[0, 0, hz + 0.002], half=list(half), material=0, ppc=8,
+                              jitter=1.0, seed=0, velocity=[0, 0, 0])],
+                bodies=[_floor(0.5),
+                        dict(name="pusher", kinematic=True, position=[x0, 0, z0],
+                             quat=[1, 0, 0, 0],
+                             trajectory=dict(times=[0.0, 10.0],
+                                             positions=[[x0, 0, z0], [x0 + 2.0, 0, z0]]),
+                             geoms=[dict(shape="box", half_extents=list(push_half),
+                                         position=[0, 0, 0], quat=[1, 0, 0, 0], mu=0.5)])])
+
+
+def scaled(scene: dict, **kw) -> dict:
+    s = copy.deepcopy(scene)
+    s.update(kw)
+    return s

@@ -44,7 +44,8 @@ def oracle_bodies(scene) -> list:
             t = b["trajectory"]
             traj = SimpleNamespace(times=np.asarray(t["times"], float),
                                    positions=np.asarray(t["positions"], float),
-                                   quats=np.stack([_qnorm(q) for q in t["quats"]]))
+                                   quats=np.stack([_qnorm(q) for q in (
+                                       t.get("quats") or [[1.0, 0, 0, 0]] * len(t["times"]))]))
         ns = SimpleNamespace(name=b["name"], kinematic=bool(b["kinematic"]), geoms=geoms,
                              position=np.asarray(b["position"], float), quat=_qnorm(b["quat"]),
                              v=np.asarray(b.get("v", [0, 0, 0]), float),

@@ -1,0 +1,130 @@
+"""CPU-only checks of the C ABI library and the host-side logic (no GPU)."""
+
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+HEADER = ROOT / "include" / "mpmrb_b200.h"
+
+
+def _declared():
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|double|const char\*)\s+(mpmrb_\w+)\(",
+                                 text, flags=re.M)))
+
+
+def test_library_loads_and_exports_every_header_symbol():
+    from paper_2503_05046_b200 import _lib
+    L = _lib.load_library()
+    names = _declared()
+    assert len(names) >= 30
+    missing = [n for n in names if not hasattr(L, n)]
+    assert not missing, missing
+    # the ctypes table covers every declared entry point
+    assert set(names) <= set(_lib.EXPORTED), set(names) - set(_lib.EXPORTED)
+    assert L.mpmrb_abi_version() == 1
+
+
+def test_library_is_sm100a():
+    import subprocess
+    lib = ROOT / "paper_2503_05046_b200" / "_native" / "libmpmrb_b200.so"
+    out = subprocess.run(["cuobjdump", "--list-elf", str(lib)], capture_output=True, text=True)
+    assert "sm_100a" in out.stdout
+
+
+def test_no_gpu_raises_native_unavailable():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    import paper_2503_05046_b200 as mp
+    with pytest.raises(mp.NativeUnavailable):
+        mp.build_sort_plan(np.zeros((4, 3)), 0.1, 0)
+
+
+def test_line_search_known_answers():
+    # reference test_solver.py:59-82 (host-side scalar logic, same as the kernel)
+    from paper_2503_05046_b200.solver import line_search
+    r = line_search(lambda a: (2 * (a - 3.0), 2.0))
+    assert r.alpha == pytest.approx(3.0, rel=1e-8) and r.evals <= 3
+    r = line_search(lambda a: (a - 1.0 if a < 1.0 else 5.0 * (a - 1.0), 1.0 if a < 1.0 else 5.0))
+    assert r.alpha == pytest.approx(1.0, abs=1e-7)
+    assert line_search(lambda a: (0.5 * (a - 40.0), 0.5)).alpha == pytest.approx(40.0, rel=1e-8)
+    with pytest.raises(ValueError):
+        line_search(lambda a: (1.0, 2.0))
+
+
+def test_param_validation():
+    from paper_2503_05046_b200 import ContactParams, Material, SolverParams, StepConfig
+    with pytest.raises(ValueError):
+        SolverParams(eps_r=-1.0)
+    with pytest.raises(ValueError):
+        SolverParams(max_iters=0)
+    with pytest.raises(ValueError):
+        ContactParams(stiffness=0.0)
+    with pytest.raises(ValueError):
+        Material(youngs_modulus=1.0, poisson_ratio=0.5, density=1.0)
+    with pytest.raises(ValueError):
+        Material(1e5, 0.3, 1000.0, model="sand", friction_angle=95.0)
+    with pytest.raises(ValueError):
+        StepConfig(dt=0.0)
+    mu, lam = Material(1e5, 0.4, 1000.0).lame
+    assert mu == pytest.approx(1e5 / 2.8) and lam == pytest.approx(1e5 * 0.4 / (1.4 * 0.2))
+
+
+def test_rotations_and_trajectory_match_golden(golden):
+    from paper_2503_05046_b200 import scenes
+    from paper_2503_05046_b200.bodies import integrate_free_body, advance_kinematic_body
+    from scenes import load_scene_json
+    from oracle.step import rigid_update
+    g = golden("steps")
+    scene = load_scene_json(g["press_scene_json"])
+    bodies = scenes.build_bodies(scene)
+    from scenes import oracle_bodies
+    obodies = oracle_bodies(scene)
+    # drive both with the same impulses; they must agree bitwise-close
+    for k in range(5):
+        t = (k + 1) * scene["dt"]
+        for b, ob in zip(bodies, obodies):
+            lin = np.array([0.001 * k, -0.002, 0.003])
+            ang = np.array([1e-5, 2e-5 * k, -1e-5])
+            if b.kinematic:
+                advance_kinematic_body(b, t)
+            else:
+                integrate_free_body(b, lin, ang, scene["gravity"], scene["dt"])
+            rigid_update(ob, lin, ang, scene["gravity"], scene["dt"], t)
+            np.testing.assert_allclose(b.position, ob.position, rtol=0, atol=1e-14)
+            np.testing.assert_allclose(b.quat, ob.quat, rtol=0, atol=1e-14)
+            np.testing.assert_allclose(b.omega, ob.omega, rtol=1e-12, atol=1e-14)
+
+
+def test_shape_mass_properties():
+    from paper_2503_05046_b200 import Box, Capsule, Sphere
+    assert Sphere(radius=0.1).volume == pytest.approx(4.0 / 3.0 * np.pi * 1e-3)
+    assert Box(half_extents=(0.1, 0.2, 0.3)).volume == pytest.approx(8 * 0.006)
+    c = Capsule(radius=0.1, half_length=0.2)
+    assert c.volume == pytest.approx(np.pi * 0.01 * 0.4 + 4.0 / 3.0 * np.pi * 1e-3)
+    for shape in (Sphere(radius=0.1), Box(half_extents=(0.1, 0.2, 0.3)), c):
+        inertia = shape.unit_inertia()
+        assert np.allclose(inertia, inertia.T) and np.all(np.linalg.eigvalsh(inertia) > 0)
+
+
+def test_seeding_matches_golden(golden):
+    """seed_box reproduces the reference's jittered lattice exactly (host setup)."""
+    import torch
+    if not torch.cuda.is_available():
+        # ParticleSet uploads to the GPU; check the host generator directly
+        from paper_2503_05046_b200.particles import _jittered_lattice
+        g = golden("steps")
+        from scenes import load_scene_json
+        scene = load_scene_json(g["rest_scene_json"])
+        v = scene["volumes"][0]
+        c, half, h = np.asarray(v["center"]), np.asarray(v["half"]), scene["h"]
+        rng = np.random.default_rng(v["seed"])
+        lo = np.floor((c - half) / h).astype(np.int64)
+        hi = np.ceil((c + half) / h).astype(np.int64)
+        pts = _jittered_lattice(lo, hi, h, 2, v["jitter"], rng)
+        pts = pts[np.all(np.abs(pts - c) <= half, axis=1)]
+        assert np.array_equal(pts, g["rest_x0"])

@@ -1,0 +1,411 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's golden
+vectors and the CPU oracle.  Bit-exact for integer/index work; float64
+tolerances (stated per test) for reassociated sums."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from types import SimpleNamespace  # noqa: E402
+
+from oracle import contact as ocm  # noqa: E402
+from oracle import grid as og  # noqa: E402
+from oracle import mpm as om  # noqa: E402
+from oracle import solver as osv  # noqa: E402
+from oracle import step as ostep  # noqa: E402
+from scenes import load_scene_json, oracle_bodies, oracle_state  # noqa: E402
+
+
+def np_(t):
+    return t.detach().cpu().numpy() if isinstance(t, torch.Tensor) else np.asarray(t)
+
+
+@pytest.fixture(scope="module")
+def mp():
+    import paper_2503_05046_b200 as m
+    return m
+
+
+# ------------------------------------------------------------------ binning (bit-exact)
+
+@pytest.mark.parametrize("tag", ["uniform", "negative", "dense"])
+def test_sort_plan_and_grid_bit_exact(mp, golden, tag):
+    g = golden("binning")
+    x, h = g[f"{tag}_x"], float(g[f"{tag}_h"])
+    plan = mp.build_sort_plan(x, h, 5)
+    assert np.array_equal(np_(plan.keys), g[f"{tag}_keys"])
+    for k in ("perm", "inv_perm", "bin_keys", "bin_starts", "bin_of"):
+        assert np.array_equal(np_(getattr(plan, k)), g[f"{tag}_{k}"]), k
+    assert np.array_equal(np_(mp.grid.base_cells(x, h)), g[f"{tag}_cells"])
+    grid = mp.SparseGrid.allocate(x, h)
+    assert np.array_equal(np_(grid.block_keys), g[f"{tag}_block_keys"])
+    assert np.array_equal(np_(grid.block_coords), g[f"{tag}_block_coords"])
+    st = mp.build_stencil(x, grid)
+    assert np.array_equal(np_(st.nodes), g[f"{tag}_nodes"])
+    assert np.array_equal(np_(st.weights), g[f"{tag}_weights"])  # no FMA contraction: exact
+    assert np.array_equal(np_(st.dpos), g[f"{tag}_dpos"])
+    assert mp.plan_staleness(plan, g[f"{tag}_moved"], h) == float(g[f"{tag}_staleness"])
+
+
+def test_sort_plan_edge_cases(mp):
+    plan = mp.build_sort_plan(np.zeros((0, 3)), 0.1, 0)
+    assert plan.n_particles == 0 and plan.n_bins == 0 and np_(plan.bin_starts).tolist() == [0]
+    # one key only, large n (stability over many warp tiles)
+    x = np.full((5000, 3), 0.01)
+    plan = mp.build_sort_plan(x, 0.1, 0)
+    assert np.array_equal(np_(plan.perm), np.arange(5000))
+    # out of Morton range -> ValueError (transfer.py:58-59)
+    with pytest.raises(ValueError):
+        mp.build_sort_plan(np.array([[1e9, 0.0, 0.0]]), 0.1, 0)
+
+
+def test_sort_plan_large_matches_oracle(mp):
+    rng = np.random.default_rng(3)
+    x = rng.uniform(-2.0, 2.0, size=(300_000, 3))
+    plan = mp.build_sort_plan(x, 0.013, 1)
+    ref = og.sort_plan(x, 0.013, 1)
+    for k in ("keys", "perm", "inv_perm", "bin_keys", "bin_starts", "bin_of"):
+        assert np.array_equal(np_(getattr(plan, k)), getattr(ref, k)), k
+
+
+def test_grid_allocation_errors(mp):
+    grid = mp.SparseGrid.allocate(np.array([[0.5, 0.5, 0.5]]), 0.1)
+    with pytest.raises(mp.AllocationError):
+        grid.node_ids(np.array([[900, 900, 900]]))
+    with pytest.raises(mp.AllocationError):
+        mp.SparseGrid.allocate(np.array([[np.nan, 0.0, 0.0]]), 0.1)
+    with pytest.raises(ValueError):
+        mp.SparseGrid.allocate(np.zeros((3, 3)), 0.0)
+    empty = mp.SparseGrid.allocate(np.zeros((0, 3)), 0.1)
+    assert empty.n_blocks == 0
+
+
+def test_scatter_reduce_contract(mp, golden):
+    rng = np.random.default_rng(0)
+    ids = rng.integers(0, 400, size=(300, 27))
+    vals = rng.normal(size=(300, 27, 4))
+    plan = mp.build_sort_plan(rng.uniform(size=(300, 3)), 0.05, 0)
+    out = np_(mp.scatter_reduce(ids, vals, 400, plan, 0))
+    ref = og.scatter_in_order(ids, vals, 400)
+    assert np.abs(out - ref).max() <= 1e-12 * np.abs(ref).max()
+    with pytest.raises(mp.PlanEpochError):
+        mp.scatter_reduce(ids, vals, 400, plan, 1)
+    with pytest.raises(ValueError):
+        mp.scatter_reduce(ids, vals, 400, plan, 0, mode="turbo")
+
+
+# ------------------------------------------------------------------ P2G / grid / G2P
+
+def _mats(mp, g):
+    return [mp.Material(E, nu, r) for E, nu, r in zip(g["mat_E"], g["mat_nu"], g["mat_rho"])]
+
+
+@pytest.mark.parametrize("tag", ["a", "b"])
+def test_p2g_grid_update_g2p(mp, golden, tag):
+    g = golden("p2g_g2p")
+    mats = _mats(mp, g)
+    h, dt = float(g[f"{tag}_h"]), float(g[f"{tag}_dt"])
+    p = mp.ParticleSet(g[f"{tag}_x"], g[f"{tag}_v"], g[f"{tag}_f"], g[f"{tag}_c"],
+                       g[f"{tag}_mass"], g[f"{tag}_vol"], g[f"{tag}_mid"])
+    tau = np_(mp.mpm.compute_stresses(p, mats))
+    np.testing.assert_allclose(tau, g[f"{tag}_tau"], rtol=1e-11, atol=1e-8)
+    grid = mp.SparseGrid.allocate(p.x, h)
+    assert np.array_equal(np_(grid.block_keys), g[f"{tag}_block_keys"])
+    plan = mp.build_sort_plan(p.x, h, 0)
+    mp.particle_to_grid(p, grid, None, mats, dt, plan, 0)
+    # tolerance: reference's own reassociation bound (test_mpm.py:107-112)
+    assert np.abs(np_(grid.mass) - g[f"{tag}_gmass"]).max() <= 1e-13 * g[f"{tag}_mass"].max()
+    for k, ref in (("mom_apic", g[f"{tag}_mom_apic"]), ("mom_force", g[f"{tag}_mom_force"])):
+        assert np.abs(np_(getattr(grid, k)) - ref).max() <= 1e-12 * np.abs(ref).max(), k
+    mp.grid_update(grid, np.array([0.0, 0.0, -9.81]), dt)
+    assert np.array_equal(np_(grid.active), g[f"{tag}_active"])
+    np.testing.assert_allclose(np_(grid.v_k), g[f"{tag}_v_k"], rtol=1e-10, atol=1e-12)
+    np.testing.assert_allclose(np_(grid.v_star), g[f"{tag}_v_star"], rtol=1e-10, atol=1e-11)
+    grid.v_next = mp._lib.as_dev(g[f"{tag}_v_next"])
+    ncl = mp.grid_to_particle(p, grid, None, dt)
+    assert ncl == int(g[f"{tag}_nclamp"])
+    np.testing.assert_allclose(np_(p.x), g[f"{tag}_x1"], rtol=0, atol=1e-15)
+    np.testing.assert_allclose(np_(p.v), g[f"{tag}_v1"], rtol=1e-12, atol=1e-14)
+    np.testing.assert_allclose(np_(p.c), g[f"{tag}_c1"], rtol=1e-10, atol=1e-11)
+    np.testing.assert_allclose(np_(p.f), g[f"{tag}_f1"], rtol=1e-12, atol=1e-13)
+
+
+def test_p2g_conservation(mp):
+    rng = np.random.default_rng(1)
+    n = 2000
+    x = rng.uniform(0, 0.4, size=(n, 3))
+    v = rng.normal(size=(n, 3))
+    f = np.eye(3)[None] + 0.05 * rng.normal(size=(n, 3, 3))
+    c = 0.1 * rng.normal(size=(n, 3, 3))
+    vol = np.full(n, 1.5e-5)
+    p = mp.ParticleSet(x, v, f, c, 1000.0 * vol, vol)
+    grid = mp.SparseGrid.allocate(p.x, 0.05)
+    plan = mp.build_sort_plan(p.x, 0.05, 0)
+    mp.particle_to_grid(p, grid, None, [mp.Material(1e5, 0.4, 1000.0)], 1e-4, plan, 0)
+    assert float(grid.mass.sum()) == pytest.approx(float(p.mass.sum()), rel=1e-13)
+    ptot = np_((p.mass[:, None] * p.v).sum(0))
+    np.testing.assert_allclose(np_(grid.mom_apic.sum(0)), ptot, rtol=1e-12, atol=1e-15)
+    mf = np_(grid.mom_force)
+    assert np.abs(mf.sum(0)).max() < 1e-12 * (np.abs(mf).max() + 1e-30)
+
+
+def test_clamp_degenerate(mp, golden):
+    g = golden("p2g_g2p")
+    out, k = mp.materials.clamp_degenerate(g["clamp_in"])
+    assert k == int(g["clamp_n"])
+    np.testing.assert_allclose(np_(out), g["clamp_out"], rtol=1e-11, atol=1e-12)
+
+
+def test_g2p_affine_reconstruction(mp):
+    # reference test_mpm.py:143-165
+    rng = np.random.default_rng(4)
+    n = 60
+    x = rng.uniform(0, 0.4, size=(n, 3))
+    f = np.eye(3)[None] + 0.05 * rng.normal(size=(n, 3, 3))
+    p = mp.ParticleSet(x, np.zeros((n, 3)), f, np.zeros((n, 3, 3)), np.ones(n), np.ones(n))
+    grid = mp.SparseGrid.allocate(p.x, 0.05)
+    v0 = np.array([0.3, -0.1, 0.2])
+    a = np.array([[0.1, 0.4, 0.0], [-0.2, 0.3, 0.1], [0.05, 0.0, -0.4]])
+    pos = np_(grid.node_positions(torch.arange(grid.n_nodes, device="cuda")))
+    grid.v_next = mp._lib.as_dev(v0 + pos @ a.T)
+    dt = 1e-4
+    mp.grid_to_particle(p, grid, None, dt)
+    v_exact = v0 + x @ a.T
+    assert np.abs(np_(p.v) - v_exact).max() < 1e-12
+    assert np.abs(np_(p.c) - a[None]).max() < 1e-10
+    f_exact = np.einsum("ij,pjk->pik", np.eye(3) + dt * a, f)
+    assert np.abs(np_(p.f) - f_exact).max() < 1e-12
+
+
+# ------------------------------------------------------------------ SDF / contacts
+
+@pytest.mark.parametrize("name", ["halfspace", "sphere", "box", "capsule"])
+def test_sdf(mp, golden, name):
+    g = golden("sdf_contacts")
+    shapes = {"halfspace": mp.HalfSpace(normal=(0.0, 0.6, 0.8), offset=0.05),
+              "sphere": mp.Sphere(radius=0.3), "box": mp.Box(half_extents=(0.15, 0.1, 0.25)),
+              "capsule": mp.Capsule(radius=0.05, half_length=0.2)}
+    phi, nrm, wit = mp.query_signed_distance(shapes[name], g[f"{name}_pts"])
+    np.testing.assert_allclose(np_(phi), g[f"{name}_phi"], rtol=0, atol=1e-15)
+    np.testing.assert_allclose(np_(nrm), g[f"{name}_normal"], rtol=0, atol=1e-15)
+    np.testing.assert_allclose(np_(wit), g[f"{name}_witness"], rtol=0, atol=1e-15)
+
+
+def test_frames(mp, golden):
+    g = golden("sdf_contacts")
+    np.testing.assert_allclose(np_(mp.contact_frames(g["frames_normals"])), g["frames"], rtol=0,
+                               atol=1e-15)
+
+
+def test_detect_contacts_with_bias_cache(mp, golden):
+    from paper_2503_05046_b200 import scenes
+    g = golden("sdf_contacts")
+    scene = load_scene_json(g["scene_json"])
+    bodies = scenes.build_bodies(scene)
+    n = g["det_x"].shape[0]
+    p = mp.ParticleSet(g["det_x"], np.zeros((n, 3)), np.tile(np.eye(3), (n, 1, 1)),
+                       np.zeros((n, 3, 3)), np.ones(n), np.ones(n))
+    cache = mp.BiasCache()
+    c1 = mp.detect_contacts(p, bodies, 0.01, cache)
+    bodies[1].v = g["det_body1_v2"]
+    p.x.copy_(torch.as_tensor(g["det_x2"], device="cuda"))
+    c2 = mp.detect_contacts(p, bodies, 0.01, cache)
+    for tag, c in (("c1", c1), ("c2", c2)):
+        for k in ("particle", "body", "geom"):
+            assert np.array_equal(np_(getattr(c, k)), g[f"{tag}_{k}"]), (tag, k)
+        for k in ("phi", "normal", "witness", "frames", "bias", "mu"):
+            np.testing.assert_allclose(np_(getattr(c, k)), g[f"{tag}_{k}"], rtol=0, atol=1e-14,
+                                       err_msg=f"{tag} {k}")
+    cache.clear()
+    c3 = mp.detect_contacts(p, bodies, 0.01, cache)
+    assert c3.n == c2.n
+
+
+def test_contact_model_matches_oracle(mp):
+    rng = np.random.default_rng(8)
+    n = 500
+    vc = rng.normal(0, 0.5, size=(n, 3))
+    vc[:50, :2] *= 1e-5  # stiction branch
+    phi = rng.uniform(-0.005, 0.005, size=n)
+    gl = rng.uniform(0, 2, size=n)
+    mu = rng.uniform(0.2, 1.1, size=n)
+    P = mp.ContactParams(stiffness=1e5, tau_d=2e-3, eps_v=1e-4)
+    dt = 1e-3
+    e = np_(mp.contact_model.contact_energy(vc, phi, gl, mu, P, dt))
+    gr = np_(mp.contact_model.contact_gradient(vc, phi, gl, mu, P, dt))
+    H = np_(mp.contact_model.contact_hessian(vc, phi, gl, mu, P, dt))
+    args = (phi, gl, mu, 1e5, 2e-3, 1e-4, dt)
+    np.testing.assert_allclose(e, ocm.energy(vc, *args), rtol=1e-13, atol=1e-16)
+    np.testing.assert_allclose(gr, ocm.gradient(vc, *args), rtol=1e-13, atol=1e-16)
+    np.testing.assert_allclose(H, ocm.hessian(vc, *args), rtol=1e-13, atol=1e-12)
+
+
+# ------------------------------------------------------------------ solver
+
+def _problem(mp, g, s):
+    pre = f"s{s}_"
+    k, tau_d, eps_v, dt = g[pre + "cparams"]
+    return mp.ContactProblem(m=g[pre + "m"], v_star=g[pre + "v_star"], v_init=g[pre + "v_init"],
+                             nodes=g[pre + "nodes"], w=g[pre + "w"], frames=g[pre + "frames"],
+                             bias=g[pre + "bias"], phi=g[pre + "phi"], mu=g[pre + "mu"],
+                             gamma_lag=g[pre + "gamma_lag"],
+                             contact_params=mp.ContactParams(stiffness=k, tau_d=tau_d,
+                                                             eps_v=eps_v),
+                             dt=dt)
+
+
+def _mnorm(v, m):
+    return float(np.sqrt(np.sum(m[:, None] * v * v)))
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2, 3])
+@pytest.mark.parametrize("ctas", [0, 3])
+def test_qn_solve_matches_reference(mp, golden, seed, ctas, monkeypatch):
+    """Tight solves agree with the reference to 1e-9 in the mass norm (the
+    reference's own QN-vs-dense bound is 1e-6, test_solver.py:150-160);
+    iteration counts within 2%; ctas=3 forces the multi-CTA grid barrier."""
+    if ctas:
+        monkeypatch.setenv("MPMRB_SOLVER_CTAS", str(ctas))
+    g = golden("solver")
+    prob = _problem(mp, g, seed)
+    m = g[f"s{seed}_m"]
+    for tag, par in (("tight", mp.SolverParams(eps_r=1e-10, max_iters=3000)),
+                     ("loose", mp.SolverParams(eps_r=5e-2))):
+        v, gam, rep = mp.quasi_newton_solve(prob, par)
+        pre = f"s{seed}_{tag}_"
+        ref_v = g[pre + "v"]
+        assert rep.converged == bool(g[pre + "conv"])
+        ref_it = int(g[pre + "iters"])
+        assert abs(rep.iterations - ref_it) <= max(1, ref_it // 50), (rep.iterations, ref_it)
+        assert _mnorm(np_(v) - ref_v, m) <= 1e-9 * max(1.0, _mnorm(ref_v, m))
+        gscale = np.abs(g[pre + "gamma"]).max()
+        assert np.abs(np_(gam) - g[pre + "gamma"]).max() <= 1e-7 * gscale
+        np.testing.assert_allclose(rep.residual_trace[0], g[pre + "residual"][0], rtol=1e-11)
+        np.testing.assert_allclose(rep.objective_trace[0], g[pre + "objective"][0], rtol=1e-11)
+        # converged state satisfies the reference's criterion
+        assert rep.residual_trace[-1] < rep.threshold_trace[-1] or not rep.converged
+
+
+def test_zero_contact_solve_returns_v_star(mp):
+    rng = np.random.default_rng(2)
+    m = rng.uniform(0.5, 2.0, size=6)
+    vs = rng.normal(size=(6, 3))
+    prob = mp.ContactProblem(m=m, v_star=vs, v_init=vs.copy(), nodes=np.zeros((0, 27), np.int64),
+                             w=np.zeros((0, 27)), frames=np.zeros((0, 3, 3)), bias=np.zeros((0, 3)),
+                             phi=np.zeros(0), mu=np.zeros(0), gamma_lag=np.zeros(0),
+                             contact_params=mp.ContactParams(), dt=1e-3)
+    v, gam, rep = mp.quasi_newton_solve(prob, mp.SolverParams())
+    assert rep.converged and rep.iterations == 0
+    assert np.array_equal(np_(v), vs)
+    assert tuple(gam.shape) == (0, 3)
+
+
+# ------------------------------------------------------------------ fused coupling step
+
+def _gpu_state(mp, g, tag):
+    from paper_2503_05046_b200 import scenes
+    scene = load_scene_json(g[f"{tag}_scene_json"])
+    p = mp.ParticleSet(g[f"{tag}_x0"], g[f"{tag}_v0"], g[f"{tag}_f0"], g[f"{tag}_c0"],
+                       g[f"{tag}_mass"], g[f"{tag}_vol"], g[f"{tag}_mid"])
+    return scenes.build_state(scene, particles=p), scene
+
+
+@pytest.mark.parametrize("tag", ["rest", "press"])
+@pytest.mark.parametrize("fused", [True, False])
+def test_steps_match_reference(mp, golden, tag, fused):
+    """Full coupling steps vs the reference's recorded trajectory: positions to
+    1e-10 m, wrench to 1e-6 relative (solver reassociation + eps_r=5e-2 stop)."""
+    g = golden("steps")
+    state, scene = _gpu_state(mp, g, tag)
+    step = mp.advance_step if fused else mp.advance_step_ops
+    nsteps = g[f"{tag}_wrench"].shape[0]
+    for i in range(nsteps):
+        s = step(state)
+        assert s.n_contacts_mean == g[f"{tag}_contacts_mean"][i]
+        assert s.staleness == g[f"{tag}_staleness"][i]
+        assert s.n_active_nodes == g[f"{tag}_active_mean"][i]
+        ws = np.abs(g[f"{tag}_wrench"][i]).max()
+        assert np.abs(s.wrench - g[f"{tag}_wrench"][i]).max() <= 1e-6 * ws + 1e-9, i
+        np.testing.assert_allclose(np_(state.particles.x), g[f"{tag}_xs"][i], rtol=0, atol=1e-10)
+    np.testing.assert_allclose(np_(state.particles.v), g[f"{tag}_v1"], rtol=0, atol=1e-7)
+    np.testing.assert_allclose(np_(state.particles.f), g[f"{tag}_f1"], rtol=0, atol=1e-8)
+    np.testing.assert_allclose(np.array([b.position for b in state.bodies]),
+                               g[f"{tag}_bodies_pos"], rtol=0, atol=1e-10)
+
+
+def test_fused_substep_equivalence(mp):
+    """One step with N substeps == N steps of one substep (coupling.py:44-55
+    invariant; tolerance instead of bitwise because of atomics)."""
+    from paper_2503_05046_b200 import scenes
+    base = dict(h=0.02, dt=2e-3, substeps=4, gravity=[0, 0, -9.81],
+                contact=dict(stiffness=1e5, tau_d=1e-3, eps_v=1e-4, margin=None),
+                solver=dict(eps_r=5e-2), materials=[dict(E=1e5, nu=0.4, rho=1000.0)],
+                volumes=[dict(center=[0, 0, 0.2], half=[0.03] * 3, material=0, ppc=8,
+                              jitter=1.0, seed=3, velocity=[0.1, -0.05, 0.0])], bodies=[])
+    a = scenes.build_state(base)
+    b = scenes.build_state(dict(base, dt=5e-4, substeps=1))
+    mp.advance_step(a)
+    for _ in range(4):
+        mp.advance_step(b)
+    for k in ("x", "v", "f", "c"):
+        np.testing.assert_allclose(np_(getattr(a.particles, k)), np_(getattr(b.particles, k)),
+                                   rtol=0, atol=1e-12)
+
+
+def test_divergence_detection(mp):
+    from paper_2503_05046_b200 import scenes
+    st = scenes.build_state(scenes.smoke_scene())
+    st.particles.v[0, 0] = float("nan")
+    with pytest.raises(mp.SimulationDiverged):
+        mp.advance_step(st)
+
+
+def test_third_law_op_path(mp):
+    """Grid momentum from contact equals the impulse charged to bodies
+    (test_coupling.py:96-114), on the op-by-op GPU path."""
+    from paper_2503_05046_b200 import scenes
+    from paper_2503_05046_b200.coupling import _advance_substep
+    sc = scenes.smoke_scene()
+    st = scenes.build_state(sc)
+    plan = mp.build_sort_plan(st.particles.x, st.h, 0)
+    info = _advance_substep(st, 5e-4, plan, 0)
+    assert info["n_contacts"] > 0
+    total = np_(info["gamma_world"]).sum(0)
+    np.testing.assert_allclose(st._accum.linear.sum(0), -total, atol=1e-15)
+    p_change = np_((st.particles.mass[:, None] * st.particles.v).sum(0))
+    st2 = scenes.build_state(sc)
+    st2.bodies = []
+    st2.__post_init__()
+    _advance_substep(st2, 5e-4, mp.build_sort_plan(st2.particles.x, st2.h, 0), 0)
+    p_free = np_((st2.particles.mass[:, None] * st2.particles.v).sum(0))
+    np.testing.assert_allclose(p_change - p_free, total, rtol=1e-9, atol=1e-13)
+
+
+def test_fused_matches_oracle_with_free_body_and_sand(mp):
+    """Multi-material scene with a free body and a Drucker–Prager material,
+    fused GPU path vs the oracle (sand parity is oracle-pinned only)."""
+    from paper_2503_05046_b200 import scenes
+    sc = scenes.sand_pile_scene(half=(0.03, 0.03, 0.02))
+    sc["bodies"].append(dict(name="ball", kinematic=False, mass=0.05,
+                             inertia=(np.eye(3) * 2e-6).tolist(), position=[0.0, 0.0, 0.06],
+                             quat=[1, 0, 0, 0], v=[0, 0, -0.5], omega=[0, 1.0, 0],
+                             geoms=[dict(shape="sphere", radius=0.015, position=[0, 0, 0],
+                                         quat=[1, 0, 0, 0], mu=0.5)]))
+    sc["substeps"] = 4
+    st = scenes.build_state(sc)
+    p0 = st.particles.numpy()
+    ref = oracle_state(sc, p0["x"], p0["v"], p0["f"], p0["c"], p0["mass"], p0["volume0"],
+                       p0["material_id"])
+    for i in range(6):
+        s = mp.advance_step(st)
+        r = ostep.step(ref)
+        assert s.n_contacts_mean == r["n_contacts_mean"], i
+        ws = np.abs(r["wrench"]).max()
+        assert np.abs(s.wrench - r["wrench"]).max() <= 1e-6 * ws + 1e-9
+    np.testing.assert_allclose(np_(st.particles.x), ref.x, rtol=0, atol=1e-10)
+    np.testing.assert_allclose(np_(st.particles.f), ref.f, rtol=0, atol=1e-8)
+    np.testing.assert_allclose(np_(st.particles.plastic), ref.plastic, rtol=0, atol=1e-8)
+    np.testing.assert_allclose(np.array([b.position for b in st.bodies]),
+                               np.array([b.position for b in ref.bodies]), rtol=0, atol=1e-10)
