@@ -1,0 +1,391 @@
+#!/usr/bin/env python
+"""Benchmark of the fused MPM + convex-contact coupling step on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload sand|sand1m|cube]
+
+A "step" is one rigid coupling step (N substeps of P2G -> grid update ->
+contact detection -> device quasi-Newton solve -> G2P) of the configuration
+BASELINE.json's metric is quoted on, configs[1]: a Drucker–Prager sand block of
+~256k particles on a floor, pushed by a kinematic box.
+Inputs are synthetic (seeded jittered lattice), float64 throughout.
+
+Metric: MPM particle-substeps/s including the convex contact solve (whole job,
+all ranks), with ms per rigid step.  Multi-GPU runs (torchrun) are batched
+independent environments, one per GPU (weak scaling, no data-path collective);
+timing is device time (CUDA events) reduced as the MAX over ranks.
+
+The cpu_baseline leg and ``--impl reference`` time the CPU oracle port
+(oracle/, a float64 NumPy restatement of the reference, which is itself pure
+NumPy) on this host's cores on a bounded sample (one substep) of the same
+workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "MPM particle-substeps/sec incl. convex contact solve; ms per rigid step"
+UNIT = "particle-substeps/s"
+PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
+FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=["sand", "sand1m", "cube"], default="sand")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def workload_scene(name: str, rank: int = 0) -> dict:
+    from paper_2503_05046_b200 import scenes
+    if name == "sand":
+        sc = scenes.sand_pile_scene()
+    elif name == "sand1m":
+        sc = scenes.sand_pile_scene(half=(0.4, 0.4, 0.1))
+    else:
+        sc = scenes.elastic_cube_scene()
+    for v in sc["volumes"]:
+        v["seed"] = v["seed"] + 1000 * rank  # independent environment per rank
+    return sc
+
+
+def host_particles(scene: dict):
+    """Seed the scene's particles on the host (same lattice as seed_box)."""
+    from paper_2503_05046_b200.particles import _jittered_lattice
+    out = {k: [] for k in ("x", "v", "mass", "vol", "mid")}
+    h = scene["h"]
+    for v in scene["volumes"]:
+        m = scene["materials"][v["material"]]
+        c, half = np.asarray(v["center"], float), np.asarray(v["half"], float)
+        rng = np.random.default_rng(v["seed"])
+        lo = np.floor((c - half) / h).astype(np.int64)
+        hi = np.ceil((c + half) / h).astype(np.int64)
+        per_axis = max(1, round(v["ppc"] ** (1.0 / 3.0)))
+        pts = _jittered_lattice(lo, hi, h, per_axis, v["jitter"], rng)
+        pts = pts[np.all(np.abs(pts - c) <= half, axis=1)]
+        n = pts.shape[0]
+        vol = 8.0 * half.prod() / n
+        out["x"].append(pts)
+        out["v"].append(np.tile(np.asarray(v["velocity"], float), (n, 1)))
+        out["mass"].append(np.full(n, m["rho"] * vol))
+        out["vol"].append(np.full(n, vol))
+        out["mid"].append(np.full(n, v["material"], dtype=np.int64))
+    arr = {k: np.concatenate(val) for k, val in out.items()}
+    n = arr["x"].shape[0]
+    arr["f"] = np.tile(np.eye(3), (n, 1, 1))
+    arr["c"] = np.zeros((n, 3, 3))
+    return arr
+
+
+def peaks():
+    try:
+        d = json.loads(PEAKS_FILE.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+
+
+# ------------------------------------------------------------------ CPU oracle
+
+def cpu_oracle_sample(scene: dict, budget_s: float = 30.0) -> dict:
+    """Time the oracle port on one substep of the workload (1 thread)."""
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    sys.path.insert(0, str(ROOT / "tests"))
+    from scenes import oracle_state
+    from oracle import step as ostep
+    sc = dict(scene)
+    sc["dt"] = scene["dt"] / scene["substeps"]
+    sc["substeps"] = 1
+    arr = host_particles(sc)
+    s = oracle_state(sc, arr["x"], arr["v"], arr["f"], arr["c"], arr["mass"], arr["vol"],
+                     arr["mid"])
+    n = arr["x"].shape[0]
+    t0 = time.perf_counter()
+    out = ostep.step(s)
+    dt = time.perf_counter() - t0
+    return dict(value=n / dt, unit=UNIT, cores=1, kind="port",
+                sample=(f"1 substep of the full workload ({n} particles, "
+                        f"{out['n_contacts_mean']:.0f} contacts, "
+                        f"{out['iterations_mean']:.0f} solver iters) from t=0, "
+                        f"{dt:.2f} s, numpy single-thread"),
+                seconds=dt)
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    scene = workload_scene(args.workload)
+    os.environ["OMP_NUM_THREADS"] = "1"
+    # one warm-up sample on a 1/64 subset keeps imports/allocators warm
+    small = json.loads(json.dumps(scene))
+    small["volumes"][0]["half"] = [a / 4 for a in small["volumes"][0]["half"]]
+    cpu_oracle_sample(small)
+    vals, secs = [], []
+    budget = 150.0
+    t_start = time.perf_counter()
+    for i in range(max(1, args.steps)):
+        r = cpu_oracle_sample(scene)
+        vals.append(r["value"])
+        secs.append(r["seconds"])
+        if time.perf_counter() - t_start + r["seconds"] > budget:
+            break
+    value = float(np.mean(vals))
+    n = host_particles(scene)["x"].shape[0]
+    line = dict(metric=METRIC, value=value, unit=UNIT, impl="reference", n_gpus=args.gpus,
+                steps=args.steps, warmup=args.warmup,
+                ms_per_step=float(np.mean(secs)) * 1e3 * scene["substeps"],
+                higher_is_better=True, scaling="weak", vs_baseline=None, dtype="f64",
+                data="synthetic",
+                config=dict(workload=f"sand pile (configs[1]), {n} particles, DP sand, "
+                                     "kinematic pusher, dt=2e-3, N=10",
+                            substeps=scene["substeps"], samples_timed=len(vals)),
+                cpu_baseline=dict(value=value, unit=UNIT, cores=1, kind="port",
+                                  sample=(f"{len(vals)} x one substep of the full workload "
+                                          "from t=0 (oracle/ NumPy port of the pure-NumPy "
+                                          "reference; single-threaded by design)")),
+                e2e=dict(value=value, unit=UNIT, h2d_bytes_per_step=0, d2h_bytes_per_step=0))
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.path = Path(f"/tmp/bench_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-i", str(self.idx), "-lms", "100"], stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return dict(sm_mhz=None, sm_max_mhz=None, reasons=["nvidia-smi unavailable"])
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.fh.close()
+        rows = []
+        for ln in self.path.read_text().splitlines():
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        if not rows:
+            return dict(sm_mhz=None, sm_max_mhz=None, reasons=["no samples"])
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        smax = max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[j] for r in rows for j in range(4) if r[5 + j] == "Active"})
+        loaded = [s for s in sm if s > 0.5 * smax] or sm
+        return dict(sm_mhz=float(statistics.median(loaded)), sm_max_mhz=smax, reasons=reasons,
+                    samples=len(rows))
+
+
+# ------------------------------------------------------------------ ours
+
+def algorithmic_bytes(stage: str, n: int, n_act: int, sand: bool) -> float:
+    """Algorithmic HBM bytes per launch (float64):
+    P2G reads x,v (24+24), C,F (72+72), m, V0, material id (8 each) = 216 B
+    per particle and writes 7 channels x 8 B = 56 B per active node; G2P reads
+    x, F (96) and writes x, v, C, F (192) = 288 B per particle (+16 B plastic
+    read+write for sand) and reads v_next (24 B) per active node."""
+    if stage == "p2g":
+        return 216.0 * n + 56.0 * n_act
+    if stage == "g2p":
+        return (288.0 + (16.0 if sand else 0.0)) * n + 24.0 * n_act
+    raise ValueError(stage)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2503_05046_b200 as mp
+    from paper_2503_05046_b200 import _lib, scenes
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    scene = workload_scene(args.workload, rank)
+    state = scenes.build_state(scene)
+    n = state.particles.n
+    N = scene["substeps"]
+    sand = any(m.get("model") == "sand" for m in scene["materials"])
+
+    for _ in range(max(3, args.warmup)):
+        mp.advance_step(state)
+    torch.cuda.synchronize()
+    stream = state._stream
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- timed region: K steps, L2 flushed between steps (outside timing)
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = _lib.launch_count()
+    total_ms = 0.0
+    iters, ncont = [], []
+    barrier()
+    for _ in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev0.record(stream)
+        s = mp.advance_step(state)
+        with torch.cuda.stream(stream):
+            ev1.record(stream)
+        ev1.synchronize()
+        total_ms += ev0.elapsed_time(ev1)
+        iters.append(s.iterations_mean)
+        ncont.append(s.n_contacts_mean)
+    barrier()
+    clk = clocks.stop()
+    launches = _lib.launch_count() - launches0
+    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = world * n * N * args.steps / (total_ms * 1e-3)
+
+    # ---- live per-stage timing (one profiled substep, direct launches)
+    prof = {}
+    mp.advance_step(state, profile=prof)
+    st = prof["stage_ms"]
+    substep_ms = sum(st.values())
+    hbm, peak_src = peaks()
+    cand = {k: st[k] for k in ("p2g", "g2p")}
+    dom = max(cand, key=cand.get)
+    abytes = algorithmic_bytes(dom, n, prof["n_active"], sand)
+    achieved = abytes / (st[dom] * 1e-3) / 1e9
+    traffic = None
+    tf = ROOT / "profiles" / "ncu_traffic.json"
+    if tf.exists():
+        try:
+            traffic = json.loads(tf.read_text()).get(args.workload, {}).get(dom)
+        except Exception:
+            traffic = None
+    roofline = dict(bound="hbm", kernel=dom, achieved=achieved, peak=hbm, unit="GB/s",
+                    frac=achieved / hbm, traffic=traffic, peak_source=peak_src,
+                    algorithmic_bytes=abytes, launch_ms=st[dom],
+                    share_of_substep=st[dom] / substep_ms,
+                    stages_ms=st, solver=dict(iterations=prof["iterations"],
+                                              ls_evals=prof["ls_evals"],
+                                              contacts=prof["n_contacts"],
+                                              ms=st["solve"],
+                                              us_per_iter=(1e3 * st["solve"] / prof["iterations"]
+                                                           if prof["iterations"] else None)))
+
+    # ---- end to end through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        p = state.particles
+        keys = ("x", "v", "f", "c", "plastic", "mass", "volume0", "material_id")
+        host = {k: torch.empty(getattr(p, k).shape, dtype=getattr(p, k).dtype,
+                               pin_memory=True) for k in keys}
+        for k in keys:
+            host[k].copy_(getattr(p, k))
+        outs = ("x", "v", "f", "c", "plastic")
+        h2d = sum(host[k].numel() * host[k].element_size() for k in keys)
+        d2h = sum(host[k].numel() * host[k].element_size() for k in outs) + 48 * len(state.bodies)
+        ke = max(3, min(args.steps, 10))
+        cur = torch.cuda.current_stream()
+        e_ms = 0.0
+        barrier()
+        for _ in range(ke):
+            flush.zero_()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(cur)
+            for k in keys:
+                getattr(p, k).copy_(host[k], non_blocking=True)
+            mp.advance_step(state)   # waits on `cur`, syncs its own stream at the end
+            for k in outs:
+                host[k].copy_(getattr(p, k), non_blocking=True)
+            b.record(cur)
+            b.synchronize()
+            e_ms += a.elapsed_time(b)
+        te = torch.tensor([e_ms], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e_ms = float(te.item())
+        e2e = dict(value=world * n * N * ke / (e_ms * 1e-3), unit=UNIT, h2d_bytes_per_step=h2d,
+                   d2h_bytes_per_step=d2h, steps=ke, ms_per_step=e_ms / ke)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_oracle_sample(scene)
+        cpu.pop("seconds", None)
+
+    if rank == 0:
+        line = dict(
+            metric=METRIC, value=value, unit=UNIT, n_gpus=world, steps=args.steps,
+            warmup=args.warmup, ms_per_step=ms_per_step, higher_is_better=True, scaling="weak",
+            vs_baseline=None, dtype="f64", data="synthetic (seeded jittered lattice)",
+            config=dict(workload=(f"sand pile (configs[1]): {n} particles/GPU, Drucker-Prager "
+                                  "sand, floor + kinematic pusher box, dt=2e-3, N=10 substeps"
+                                  if args.workload.startswith("sand") else
+                                  f"elastic cube (configs[0]): {n} particles, dt=1e-3, N=10"),
+                        particles_per_gpu=n, substeps=N, envs=world,
+                        parallelism=f"{world} independent envs (1/GPU)",
+                        l2="flushed (256 MiB write) between timed steps",
+                        contacts_mean=float(np.mean(ncont)),
+                        solver_iters_mean=float(np.mean(iters))),
+            roofline=roofline, cpu_baseline=cpu, e2e=e2e, gpu_launches=int(launches),
+            clocks=clk)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

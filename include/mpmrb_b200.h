@@ -255,6 +255,12 @@ int mpmrb_qn_solve(mpmrb_ctx* ctx, const mpmrb_problem* prob_host,
                    double* gamma, double* objective, double* residual, double* threshold,
                    double* alpha, mpmrb_solve_report* report_host);
 
+/* Solver phase timers (globaltimer ns, accumulated over solves since the last
+ * reset) when the context was created with MPMRB_SOLVER_PROF=1, else zeros:
+ * [0] init [1] node phase [2] dvc phase [3] line search [4] update
+ * [5] epilogue [6] iterations [7] line-search evals [8] sum of CTAs [9] solves. */
+int mpmrb_solver_profile(mpmrb_ctx* ctx, uint64_t* out_host /*12*/, int32_t reset);
+
 /* ------------------------------------------------------------------ fused substep */
 /* coupling.py:115-219 as a device pipeline: one CUDA graph per substep. */
 typedef struct mpmrb_sim mpmrb_sim;
@@ -278,6 +284,12 @@ int mpmrb_sim_substep(mpmrb_sim* sim);
  * (n_bodies*6: linear then angular, NOT divided by dt).  Synchronises. */
 int mpmrb_sim_end_step(mpmrb_sim* sim, mpmrb_step_stats* stats_host,
                        double* impulses_host);
+/* Run ONE substep with direct launches and CUDA events between the 7
+ * pipeline stages (grid build, P2G, grid update+compaction, contacts, solve,
+ * reactions, G2P): stage_ms_host[7]; sizes_host[5] = nb, n_active, n_contacts,
+ * solver iterations, line-search evaluations.  Must be called between
+ * begin_step and end_step (it is one of that step's substeps). */
+int mpmrb_sim_profile_substep(mpmrb_sim* sim, float* stage_ms_host, int32_t* sizes_host);
 /* transfer.py:105-113 plan staleness measured at the last end_step. */
 double mpmrb_sim_staleness(mpmrb_sim* sim);
 /* Device pointers of the most recent substep's grid (for parity tests). */

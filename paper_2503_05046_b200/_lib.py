@@ -132,7 +132,8 @@ _SIGS = {
     "mpmrb_contact_velocities": ([_P, _P, _P, _P, _P, _I64, _P, _P], C.c_int),
     "mpmrb_qn_solve": ([_P, C.POINTER(Problem), C.POINTER(SolverParamsC), _P, _P, _P, _P, _P, _P,
                         _P, C.POINTER(SolveReportC)], C.c_int),
-    "mpmrb_sim_create": ([_P, C.POINTER(C.c_void_p)], C.c_int),
+    "mpmrb_solver_profile": ([_P, C.POINTER(C.c_uint64), C.c_int32], C.c_int),
+    "mpmrb_sim_create":([_P, C.POINTER(C.c_void_p)], C.c_int),
     "mpmrb_sim_destroy": ([_P], C.c_int),
     "mpmrb_sim_set_particles": ([_P, C.POINTER(Particles)], C.c_int),
     "mpmrb_sim_set_materials": ([_P, C.POINTER(Material), C.c_int32], C.c_int),
@@ -143,6 +144,7 @@ _SIGS = {
     "mpmrb_sim_substep": ([_P], C.c_int),
     "mpmrb_sim_end_step": ([_P, C.POINTER(StepStats), C.POINTER(_D)], C.c_int),
     "mpmrb_sim_staleness": ([_P], C.c_double),
+    "mpmrb_sim_profile_substep": ([_P, C.POINTER(C.c_float), C.POINTER(C.c_int32)], C.c_int),
     "mpmrb_sim_last_grid":([_P, C.POINTER(_I64), C.POINTER(_P), C.POINTER(_P), C.POINTER(_P),
                              C.POINTER(_P)], C.c_int),
     "mpmrb_sim_last_contacts": ([_P, C.POINTER(_I64), C.POINTER(_P), C.POINTER(_P)], C.c_int),

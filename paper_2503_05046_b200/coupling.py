@@ -147,8 +147,15 @@ def _stream_of(state: SimState) -> torch.cuda.Stream:
     return state._stream
 
 
-def advance_step(state: SimState) -> StepSummary:
-    """Advance one coupling step of size dt (N fused substeps + rigid update)."""
+STAGES = ("grid_build", "p2g", "grid_update", "contacts", "solve", "reactions", "g2p")
+
+
+def advance_step(state: SimState, profile: dict | None = None) -> StepSummary:
+    """Advance one coupling step of size dt (N fused substeps + rigid update).
+
+    ``profile``: if a dict is given, the step's first substep runs with direct
+    launches and CUDA events between its stages; the dict receives the stage
+    times (ms) and sizes (used by bench.py's live roofline)."""
     L = _lib.lib()
     p = state.particles
     sim = _ensure_sim(state)
@@ -182,7 +189,15 @@ def advance_step(state: SimState) -> StepSummary:
                 f"non-finite or out-of-range particle state after step {state.step_index}")
         _lib.check(rc)
         state.plan_builds += 1
-        for _ in range(n):
+        for k in range(n):
+            if profile is not None and k == 0:
+                ms = (C.c_float * 7)()
+                sz = (C.c_int32 * 5)()
+                _lib.check(L.mpmrb_sim_profile_substep(sim, ms, sz))
+                profile["stage_ms"] = dict(zip(STAGES, [float(a) for a in ms]))
+                profile.update(n_blocks=int(sz[0]), n_active=int(sz[1]), n_contacts=int(sz[2]),
+                               iterations=int(sz[3]), ls_evals=int(sz[4]))
+                continue
             _lib.check(L.mpmrb_sim_substep(sim))
         rc = L.mpmrb_sim_end_step(sim, C.byref(stats), imp)
     if rc == _lib.E_DIVERGED:

@@ -102,7 +102,26 @@ int mpmrb_create(int device, mpmrb_ctx** out) {
     return set_cuda_error(e, "cudaMalloc(status)", __FILE__, __LINE__);
   }
   cudaMemset(c->status, 0, sizeof(DevStatus));
+  const char* prof = getenv("MPMRB_SOLVER_PROF");
+  if (prof && atoi(prof) > 0) {
+    if (cudaMalloc(&c->solver_prof, 8 * kSolverProf) == cudaSuccess)
+      cudaMemset(c->solver_prof, 0, 8 * kSolverProf);
+    else
+      c->solver_prof = nullptr;
+  }
   *out = c;
+  return MPMRB_OK;
+}
+
+int mpmrb_solver_profile(mpmrb_ctx* c, uint64_t* out_host, int32_t reset) {
+  CHECK_CTX(c);
+  if (!c->solver_prof) {
+    std::memset(out_host, 0, 8 * kSolverProf);
+    return MPMRB_OK;
+  }
+  MPMRB_CUDA_OK(cudaStreamSynchronize(c->stream));
+  MPMRB_CUDA_OK(cudaMemcpy(out_host, c->solver_prof, 8 * kSolverProf, cudaMemcpyDeviceToHost));
+  if (reset) MPMRB_CUDA_OK(cudaMemset(c->solver_prof, 0, 8 * kSolverProf));
   return MPMRB_OK;
 }
 
@@ -410,17 +429,19 @@ extern "C" int mpmrb_qn_solve(mpmrb_ctx* c, const mpmrb_problem* pr,
   int rc = 0;
   rc |= c->scratch[SS_SOLVER0].grow(4 * 27 * ncc);           // cnodes
   rc |= c->scratch[SS_SOLVER1].grow(8 * 27 * ncc);           // cw
-  rc |= c->scratch[SS_SOLVER2].grow(8 * 3 * ndd * 3);        // g, jt, dv
-  rc |= c->scratch[SS_SOLVER3].grow(8 * 6 * ndd);            // H6
-  rc |= c->scratch[SS_SOLVER4].grow(8 * 3 * ncc * 2);        // vc, dvc
+  rc |= c->scratch[SS_SOLVER2].grow(8 * 3 * ndd);            // dv
+  rc |= c->scratch[SS_SOLVER3].grow(8 * 9 * ncc);            // gw (3), rgr (6)
+  rc |= c->scratch[SS_SOLVER4].grow(8 * 8 * ncc);            // vc, dvc, vhat, mug
   rc |= c->scratch[SS_SOLVER5].grow(8 * 2 * 8 * kMaxSolverCtas);  // partials
-  rc |= c->scratch[SS_SOLVER6].grow(256);                    // bar, sizes, SolveOut
+  rc |= c->scratch[SS_SOLVER6].grow(4096);                   // flags, sizes, SolveOut
+  rc |= c->scratch[SS_SOLVER7].grow(4 * 7 * (ndd + 2) + 64);  // adjacency int arrays
+  rc |= c->scratch[SS_SOLVER8].grow(2 * 4 * 27 * ncc);       // adjacency entries (+tmp)
+  rc |= c->scratch[SS_PROBLEM].grow(8 * 27 * ncc);           // adjacency weights
   if (rc) return MPMRB_E_CUDA;
   char* misc = c->scratch[SS_SOLVER6].as<char>();
-  unsigned* bar = (unsigned*)misc;
-  int* sizes = (int*)(misc + 16);
-  SolveOut* so = (SolveOut*)(misc + 64);
-  MPMRB_CUDA_OK(cudaMemsetAsync(misc, 0, 256, c->stream));
+  int* sizes = (int*)(misc + 2048);
+  SolveOut* so = (SolveOut*)(misc + 2304);
+  MPMRB_CUDA_OK(cudaMemsetAsync(misc, 0, 4096, c->stream));
   int hs[2] = {(int)nd, (int)nc};
   MPMRB_CUDA_OK(cudaMemcpyAsync(sizes, hs, sizeof(hs), cudaMemcpyHostToDevice, c->stream));
   if (nc > 0) {
@@ -429,10 +450,29 @@ extern "C" int mpmrb_qn_solve(mpmrb_ctx* c, const mpmrb_problem* pr,
         c->scratch[SS_SOLVER1].as<double>());
     c->launches++;
   }
+  int* ai = c->scratch[SS_SOLVER7].as<int>();
+  SolverAdjacency adj{};
+  adj.cnt = ai;
+  adj.fill = ai + (ndd + 2);
+  adj.off = ai + 2 * (ndd + 2);
+  adj.flag = ai + 3 * (ndd + 2);
+  adj.flag_off = ai + 4 * (ndd + 2);
+  adj.cn = ai + 5 * (ndd + 2);
+  adj.fn = ai + 6 * (ndd + 2);
+  adj.n_cn = ai + 7 * (ndd + 2);
+  adj.ent = c->scratch[SS_SOLVER8].as<int>();
+  adj.ent_tmp = adj.ent + 27 * ncc;
+  adj.w = c->scratch[SS_PROBLEM].as<double>();
+  rc = launch_solver_adjacency(*c, sizes, sizes + 1, nd, nc, c->scratch[SS_SOLVER0].as<int>(),
+                               c->scratch[SS_SOLVER1].as<double>(), adj, c->scratch[SS_TILE]);
+  if (rc) return rc;
   SolverArgs a{};
   a.nd_dev = sizes;
   a.nc_dev = sizes + 1;
   a.nc_cap = nc;
+  a.nd_cap = nd;
+  a.adj = adj;
+  a.prof = c->solver_prof;
   a.m = pr->m;
   a.v_star = pr->v_star;
   a.v0 = v0 ? v0 : pr->v_init;
@@ -453,16 +493,15 @@ extern "C" int mpmrb_qn_solve(mpmrb_ctx* c, const mpmrb_problem* pr,
   a.ls_max = sp->ls_max_iters;
   a.skip_if_no_contacts = 0;
   a.force_ctas = 0;
-  double* sv2 = c->scratch[SS_SOLVER2].as<double>();
   a.v = v;
-  a.g = sv2;
-  a.jt = sv2 + 3 * ndd;
-  a.dv = sv2 + 6 * ndd;
-  a.H6 = c->scratch[SS_SOLVER3].as<double>();
+  a.dv = c->scratch[SS_SOLVER2].as<double>();
+  a.gw = c->scratch[SS_SOLVER3].as<double>();
+  a.rgr = a.gw + 3 * ncc;
   a.vc = c->scratch[SS_SOLVER4].as<double>();
   a.dvc = a.vc + 3 * ncc;
+  a.cvhat = a.vc + 6 * ncc;
+  a.cmug = a.vc + 7 * ncc;
   a.partials = c->scratch[SS_SOLVER5].as<double>();
-  a.bar = bar;
   a.gamma = gamma;
   a.tr_obj = objective;
   a.tr_res = residual;
@@ -520,7 +559,9 @@ int mpmrb_sim_destroy(mpmrb_sim* s) {
                     &s->b_act, &s->b_remap, &s->b_mc, &s->b_vstarc, &s->b_vkc, &s->b_cnt,
                     &s->b_offs, &s->b_cpart, &s->b_cbody, &s->b_cphi, &s->b_cmu, &s->b_cgl,
                     &s->b_cnormal, &s->b_cwit, &s->b_cbias, &s->b_cframes, &s->b_cnodes,
-                    &s->b_cw, &s->b_sv, &s->b_sg, &s->b_sjt, &s->b_sH, &s->b_sdv, &s->b_svc,
+                    &s->b_cw, &s->b_sv, &s->b_sgw, &s->b_srgr, &s->b_adjcnt, &s->b_adjfill,
+                    &s->b_adjoff, &s->b_adjent, &s->b_adjw, &s->b_adjflag,
+                    &s->b_adjflagoff, &s->b_adjcn, &s->b_adjfn, &s->b_sdv, &s->b_svc,
                     &s->b_sdvc, &s->b_gamma, &s->b_gworld, &s->b_tiles, &s->b_bias_stamp,
                     &s->b_bias_store};
   for (DevBuf* b : bufs) b->release();
@@ -608,6 +649,11 @@ int mpmrb_sim_end_step(mpmrb_sim* s, mpmrb_step_stats* st, double* impulses) {
 }
 
 double mpmrb_sim_staleness(mpmrb_sim* s) { return s ? s->staleness : 0.0; }
+
+int mpmrb_sim_profile_substep(mpmrb_sim* s, float* stage_ms_host, int32_t* sizes_host) {
+  if (!s) return set_error(MPMRB_E_INVALID, "null sim");
+  return s->profile_substep(stage_ms_host, sizes_host);
+}
 
 int mpmrb_sim_last_grid(mpmrb_sim* s, int64_t* nb, const int64_t** block_keys,
                         const double** mass, const double** v_star, const double** v_next) {

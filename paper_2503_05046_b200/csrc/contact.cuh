@@ -176,6 +176,28 @@ __device__ __forceinline__ void cm_hessian(const ContactModel& cm, const double*
   G[3] = -b * vc[0] * vc[1];
 }
 
+// Fused gradient + Hessian (+ energy) with the per-solve constants
+// vhat = -phi/(dt+tau_d) and mug = mu*gamma_lag precomputed: one sqrt and two
+// divisions per evaluation (contact_model.py:114-138).  Same operation order
+// as the separate functions above, so results are bitwise identical.
+__device__ __forceinline__ double cm_eval(const ContactModel& cm, const double* vc, double vhat,
+                                          double mug, double* g, double* G) {
+  const double gap = vhat - vc[2];
+  g[2] = -(cm.K * fmax(0.0, gap));
+  G[2] = (gap >= 0.0) ? cm.K : 0.0;
+  const double s = sqrt(vc[0] * vc[0] + vc[1] * vc[1]);
+  const double a = mug / fmax(s, cm.eps_v);
+  g[0] = a * vc[0];
+  g[1] = a * vc[1];
+  const double b = (s > cm.eps_v) ? a / fmax(s * s, cm.eps_v * cm.eps_v) : 0.0;
+  G[0] = a - b * vc[0] * vc[0];
+  G[1] = a - b * vc[1] * vc[1];
+  G[3] = -b * vc[0] * vc[1];
+  const double gp = fmax(0.0, gap);
+  const double hub = (s <= cm.eps_v) ? s * s / (2.0 * cm.eps_v) : s - 0.5 * cm.eps_v;
+  return 0.5 * cm.K * gp * gp + mug * hub;  // energy (contact_model.py:62-72)
+}
+
 int launch_detect(Ctx& c, const double* x, long long n, const mpmrb_geom* geoms_dev, int ngeom,
                   double margin, int* cnt, int* offs, int* total_dev, DevBuf& tiles,
                   long long cap, int* bias_stamp, double* bias_store,

@@ -35,6 +35,8 @@ struct Ctx {
   DevStatus* status_host = nullptr;  // pinned mirror
   long long launches = 0;
   DevBuf scratch[24];
+  // phase timers of the solver kernel (enabled by MPMRB_SOLVER_PROF=1)
+  unsigned long long* solver_prof = nullptr;
   int check_status(const char* where);  // sync + read + clear device status
 };
 

@@ -237,15 +237,23 @@ int Sim::reserve(long long n, long long nb_needed) {
   rc |= b_cnodes.grow(4 * 27 * nc_cap);
   rc |= b_cw.grow(8 * 27 * nc_cap);
   rc |= b_sv.grow(8 * 3 * N);
-  rc |= b_sg.grow(8 * 3 * N);
-  rc |= b_sjt.grow(8 * 3 * N);
-  rc |= b_sH.grow(8 * 6 * N);
   rc |= b_sdv.grow(8 * 3 * N);
-  rc |= b_svc.grow(8 * 3 * nc_cap);
+  rc |= b_svc.grow(8 * 5 * nc_cap);  // vc (3), vhat, mu*gamma_lag
   rc |= b_sdvc.grow(8 * 3 * nc_cap);
+  rc |= b_sgw.grow(8 * 3 * nc_cap);
+  rc |= b_srgr.grow(8 * 6 * nc_cap);
+  rc |= b_adjcnt.grow(4 * (N + 1));
+  rc |= b_adjfill.grow(4 * (N + 1));
+  rc |= b_adjoff.grow(4 * (N + 1));
+  rc |= b_adjent.grow(2 * 4 * 27 * nc_cap);
+  rc |= b_adjw.grow(8 * 27 * nc_cap);
+  rc |= b_adjflag.grow(4 * (N + 1));
+  rc |= b_adjflagoff.grow(4 * (N + 1));
+  rc |= b_adjcn.grow(4 * (N + 1));
+  rc |= b_adjfn.grow(4 * (N + 1));
   rc |= b_gamma.grow(8 * 3 * nc_cap);
   rc |= b_gworld.grow(8 * 3 * nc_cap);
-  long long scan_n = (N / 32 + 1) > (n + 1) ? (N / 32 + 1) : (n + 1);
+  long long scan_n = (N + 1) > (n + 1) ? (N + 1) : (n + 1);
   rc |= b_tiles.grow(8 * (scan_n / 2048 + 2));
   if (rc) return MPMRB_E_CUDA;
   return MPMRB_OK;
@@ -257,11 +265,13 @@ int Sim::capture_or_launch() {
   int* counters = b_counters.as<int>();  // [0] nb, [1] n_act, [2] nc, [3] substep idx
   GridDev g{b_hkeys.as<unsigned long long>(), b_hvals.as<int>(), (unsigned)(hash_cap - 1), h};
   int rc;
+  mark(0);
   // 1. grid (grid.py:71-103)
   rc = launch_grid_build(c, p.x, n_particles, h, b_bkeys.as<long long>(), nb_cap,
                          b_hkeys.as<unsigned long long>(), b_hvals.as<int>(), hash_cap,
                          b_ukeys.as<long long>(), counters + 0);
   if (rc) return rc;
+  mark(1);
   // 2. P2G (mpm.py:66-99)
   MPMRB_CUDA_OK(cudaMemsetAsync(b_mass.p, 0, 8 * N, c.stream));
   MPMRB_CUDA_OK(cudaMemsetAsync(b_mom.p, 0, 8 * 6 * N, c.stream));
@@ -270,6 +280,7 @@ int Sim::capture_or_launch() {
   rc = launch_p2g(c, g, p, b_mats.as<mpmrb_material>(), nmat, dt_s, b_mass.as<double>(), mom_apic,
                   mom_force);
   if (rc) return rc;
+  mark(2);
   // 3. grid update + ordered active compaction (mpm.py:102-115, solver.py:203-205)
   rc = launch_grid_update(c, N, counters + 0, b_mass.as<double>(), mom_apic, mom_force, gravity[0],
                           gravity[1], gravity[2], dt_s, b_active.as<unsigned char>(),
@@ -284,6 +295,7 @@ int Sim::capture_or_launch() {
       b_vk.as<double>(), b_act.as<int>(), b_remap.as<int>(), b_mc.as<double>(),
       b_vstarc.as<double>(), b_vkc.as<double>());
   c.launches++;
+  mark(3);
   // 4. contacts (collision.py:88-132)
   ContactArrays ca{};
   ca.particle = b_cpart.as<int>();
@@ -303,13 +315,32 @@ int Sim::capture_or_launch() {
       b_remap.as<int>(), K, den, b_cnodes.as<int>(), b_cw.as<double>(), b_cgl.as<double>(),
       c.status);
   c.launches++;
+  mark(4);
   // 5. quasi-Newton solve on the device (solver.py:328-382)
   k_reset_solveout<<<1, 32, 0, c.stream>>>(b_solveout.as<SolveOut>());
   c.launches++;
+  SolverAdjacency adj{};
+  adj.cnt = b_adjcnt.as<int>();
+  adj.fill = b_adjfill.as<int>();
+  adj.off = b_adjoff.as<int>();
+  adj.ent = b_adjent.as<int>();
+  adj.ent_tmp = b_adjent.as<int>() + 27 * nc_cap;
+  adj.w = b_adjw.as<double>();
+  adj.flag = b_adjflag.as<int>();
+  adj.flag_off = b_adjflagoff.as<int>();
+  adj.cn = b_adjcn.as<int>();
+  adj.fn = b_adjfn.as<int>();
+  adj.n_cn = counters + 5;
+  rc = launch_solver_adjacency(c, counters + 1, counters + 2, N, nc_cap, b_cnodes.as<int>(),
+                               b_cw.as<double>(), adj, b_tiles);
+  if (rc) return rc;
   SolverArgs a{};
   a.nd_dev = counters + 1;
   a.nc_dev = counters + 2;
   a.nc_cap = nc_cap;
+  a.nd_cap = N;
+  a.adj = adj;
+  a.prof = c.solver_prof;
   a.m = b_mc.as<double>();
   a.v_star = b_vstarc.as<double>();
   a.v0 = b_vkc.as<double>();
@@ -331,30 +362,62 @@ int Sim::capture_or_launch() {
   a.skip_if_no_contacts = 1;
   a.force_ctas = force_ctas;
   a.v = b_sv.as<double>();
-  a.g = b_sg.as<double>();
-  a.jt = b_sjt.as<double>();
-  a.H6 = b_sH.as<double>();
   a.dv = b_sdv.as<double>();
   a.vc = b_svc.as<double>();
+  a.cvhat = b_svc.as<double>() + 3 * nc_cap;
+  a.cmug = b_svc.as<double>() + 4 * nc_cap;
   a.dvc = b_sdvc.as<double>();
+  a.gw = b_sgw.as<double>();
+  a.rgr = b_srgr.as<double>();
   a.partials = b_partials.as<double>();
-  a.bar = b_bar.as<unsigned>();
   a.gamma = b_gamma.as<double>();
   a.out = b_solveout.as<SolveOut>();
   a.act = b_act.as<int>();
   a.v_next_full = b_vnext.as<double>();
   rc = launch_qn_solve(c, a, 0);
   if (rc) return rc;
+  mark(5);
   k_substep_end<<<1, 512, 0, c.stream>>>(
       counters, b_solveout.as<SolveOut>(), b_gamma.as<double>(), ca.frames, ca.witness,
       ca.body, b_geoms.as<mpmrb_geom>(), ngeom, nbody, nc_cap, b_accum.as<double>(),
       b_gworld.as<double>(), counters + 3, b_stats.as<SubstepStat>(), max_substeps, c.status);
   c.launches++;
+  mark(6);
   // 6. G2P (mpm.py:118-138)
   rc = launch_g2p(c, g, p, b_mats.as<mpmrb_material>(), nmat, b_vnext.as<double>(), dt_s,
                   b_misc.as<unsigned long long>(), b_misc.as<int>() + 2);
   if (rc) return rc;
+  mark(7);
   MPMRB_CUDA_OK(cudaGetLastError());
+  return MPMRB_OK;
+}
+
+void Sim::mark(int k) {
+  if (prof_on) cudaEventRecord(prof_ev[k], ctx->stream);
+}
+
+// One substep with direct launches and events between the pipeline stages
+// (bench.py's live per-kernel timing; graph replays cannot be bracketed).
+int Sim::profile_substep(float* stage_ms, int* sizes) {
+  Ctx& c = *ctx;
+  if (!prof_ev[0])
+    for (int k = 0; k < kProfEvents; ++k) MPMRB_CUDA_OK(cudaEventCreate(&prof_ev[k]));
+  prof_on = true;
+  int rc = capture_or_launch();
+  prof_on = false;
+  if (rc) return rc;
+  MPMRB_CUDA_OK(cudaStreamSynchronize(c.stream));
+  for (int k = 0; k + 1 < kProfEvents; ++k)
+    MPMRB_CUDA_OK(cudaEventElapsedTime(&stage_ms[k], prof_ev[k], prof_ev[k + 1]));
+  int hc[4] = {0, 0, 0, 0};
+  MPMRB_CUDA_OK(cudaMemcpy(hc, b_counters.p, sizeof(hc), cudaMemcpyDeviceToHost));
+  sizes[0] = hc[0];
+  sizes[1] = hc[1];
+  sizes[2] = hc[2];
+  SolveOut so{};
+  MPMRB_CUDA_OK(cudaMemcpy(&so, b_solveout.p, sizeof(so), cudaMemcpyDeviceToHost));
+  sizes[3] = so.iterations;
+  sizes[4] = so.ls_evals;
   return MPMRB_OK;
 }
 
@@ -364,7 +427,7 @@ int Sim::begin_step(long long epoch, int n_substeps) {
   if (!have_params) return set_error(MPMRB_E_INVALID, "sim: params not set");
   // size the grid for the current positions (one host sync per step)
   if (b_counters.grow(64) || b_misc.grow(64) || b_solveout.grow(sizeof(SolveOut)) ||
-      b_bar.grow(64) || b_partials.grow(sizeof(double) * 2 * 8 * kMaxSolverCtas) ||
+      b_bar.grow(4096) || b_partials.grow(sizeof(double) * 2 * 8 * kMaxSolverCtas) ||
       b_dyn.grow(64) || b_accum.grow(sizeof(double) * 6 * kMaxBodies))
     return MPMRB_E_CUDA;
   if (!bar_init) {
@@ -527,6 +590,8 @@ int Sim::end_step(mpmrb_step_stats* out, double* impulses_host) {
 
 Sim::~Sim() {
   if (graph_exec) cudaGraphExecDestroy(graph_exec);
+  for (int k = 0; k < kProfEvents; ++k)
+    if (prof_ev[k]) cudaEventDestroy(prof_ev[k]);
 }
 
 }  // namespace mpmrb

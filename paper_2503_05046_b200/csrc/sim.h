@@ -39,9 +39,16 @@ struct Sim {
   DevBuf b_mc, b_vstarc, b_vkc;
   DevBuf b_cnt, b_offs, b_cpart, b_cbody, b_cphi, b_cmu, b_cgl, b_cnormal, b_cwit, b_cbias,
       b_cframes, b_cnodes, b_cw;
-  DevBuf b_sv, b_sg, b_sjt, b_sH, b_sdv, b_svc, b_sdvc, b_gamma, b_gworld, b_tiles;
+  DevBuf b_sv, b_sdv, b_svc, b_sdvc, b_sgw, b_srgr, b_gamma, b_gworld, b_tiles;
+  DevBuf b_adjcnt, b_adjfill, b_adjoff, b_adjent, b_adjw, b_adjflag, b_adjflagoff, b_adjcn,
+      b_adjfn;
   DevBuf b_bias_stamp, b_bias_store;
 
+  static constexpr int kProfEvents = 8;
+  cudaEvent_t prof_ev[kProfEvents] = {};
+  bool prof_on = false;
+  void mark(int k);
+  int profile_substep(float* stage_ms, int* sizes);
   int reserve(long long n, long long nb_needed);
   int capture_or_launch();
   int begin_step(long long epoch, int n_substeps);

@@ -7,6 +7,7 @@ namespace mpmrb {
 
 constexpr int kSolverThreads = 512;
 constexpr int kMaxSolverCtas = 160;
+constexpr int kSolverProf = 12;  // phase timers (ns), see solver.cu
 
 struct SolveOut {
   int converged;
@@ -19,11 +20,28 @@ struct SolveOut {
   int n_dofs;
 };
 
+// Node -> (contact, slot) adjacency of one solve (built by
+// launch_solver_adjacency from the contact stencils).
+struct SolverAdjacency {
+  int* cnt;      // (nd_cap+1) scratch
+  int* fill;     // (nd_cap+1) scratch
+  int* off;      // (nd_cap+1) CSR offsets
+  int* ent;      // (27 nc_cap) packed (c << 5) | k, ascending within a node
+  int* ent_tmp;  // (27 nc_cap) scratch: entries in atomic fill order
+  double* w;     // (27 nc_cap) stencil weight of each entry
+  int* flag;     // (nd_cap+1) scratch: node has entries
+  int* flag_off; // (nd_cap+1) scan of flag
+  int* cn;       // (nd_cap) nodes with entries ("contact nodes")
+  int* fn;       // (nd_cap) nodes without entries
+  int* n_cn;     // device count of contact nodes
+};
+
 struct SolverArgs {
   // sizes (device)
   const int* nd_dev;
   const int* nc_dev;
   long long nc_cap;
+  long long nd_cap;
   // problem on active nodes (solver.py:75-110)
   const double* m;
   const double* v_star;
@@ -36,6 +54,7 @@ struct SolverArgs {
   const double* mu;
   const double* gamma_lag;
   double K, den, eps_v;
+  SolverAdjacency adj;
   // solver parameters (solver.py:35-49)
   double eps_a, eps_r, ls_tol;
   int max_iters, ls_max;
@@ -43,14 +62,14 @@ struct SolverArgs {
   int force_ctas;  // 0 = automatic
   // work (device)
   double* v;
-  double* g;
-  double* jt;
-  double* H6;
   double* dv;
   double* vc;
   double* dvc;
-  double* partials;  // [kMaxRed][kMaxSolverCtas]
-  unsigned* bar;     // 2 words, zero-initialised once
+  double* gw;        // (nc,3) R^T g_c
+  double* rgr;       // (nc,6) R^T G R (00,11,22,10,20,21)
+  double* cvhat;     // (nc,) -phi/(dt+tau_d), per solve
+  double* cmug;      // (nc,) mu*gamma_lag, per solve
+  double* partials;  // 2 x [kMaxRed][kMaxSolverCtas]
   // outputs
   double* gamma;
   double* tr_obj;
@@ -58,11 +77,16 @@ struct SolverArgs {
   double* tr_thr;
   double* tr_alpha;
   SolveOut* out;
+  unsigned long long* prof;  // optional [kSolverProf] phase times (ns)
   // fused epilogue: scatter v into the full grid
   const int* act;
   double* v_next_full;
 };
 
+// Build the adjacency from cnodes/cw (w != 0 slots only).
+int launch_solver_adjacency(Ctx& c, const int* nd_dev, const int* nc_dev, long long nd_cap,
+                            long long nc_cap, const int* cnodes, const double* cw,
+                            const SolverAdjacency& adj, DevBuf& tiles);
 int launch_qn_solve(Ctx& c, const SolverArgs& a, int grid_ctas);
 
 }  // namespace mpmrb
