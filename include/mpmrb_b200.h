@@ -259,7 +259,7 @@ int mpmrb_qn_solve(mpmrb_ctx* ctx, const mpmrb_problem* prob_host,
  * reset) when the context was created with MPMRB_SOLVER_PROF=1, else zeros:
  * [0] init [1] node phase [2] dvc phase [3] line search [4] update
  * [5] epilogue [6] iterations [7] line-search evals [8] sum of CTAs [9] solves. */
-int mpmrb_solver_profile(mpmrb_ctx* ctx, uint64_t* out_host /*12*/, int32_t reset);
+int mpmrb_solver_profile(mpmrb_ctx* ctx, uint64_t* out_host /*16*/, int32_t reset);
 
 /* ------------------------------------------------------------------ fused substep */
 /* coupling.py:115-219 as a device pipeline: one CUDA graph per substep. */

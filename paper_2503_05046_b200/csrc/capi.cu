@@ -432,9 +432,9 @@ extern "C" int mpmrb_qn_solve(mpmrb_ctx* c, const mpmrb_problem* pr,
   rc |= c->scratch[SS_SOLVER2].grow(8 * 3 * ndd);            // dv
   rc |= c->scratch[SS_SOLVER3].grow(8 * 9 * ncc);            // gw (3), rgr (6)
   rc |= c->scratch[SS_SOLVER4].grow(8 * 8 * ncc);            // vc, dvc, vhat, mug
-  rc |= c->scratch[SS_SOLVER5].grow(8 * 2 * 8 * kMaxSolverCtas);  // partials
+  rc |= c->scratch[SS_SOLVER5].grow(8 * (2 * 8 * kMaxSolverCtas + 8));  // partials, ls_out
   rc |= c->scratch[SS_SOLVER6].grow(4096);                   // flags, sizes, SolveOut
-  rc |= c->scratch[SS_SOLVER7].grow(4 * 7 * (ndd + 2) + 64);  // adjacency int arrays
+  rc |= c->scratch[SS_SOLVER7].grow(4 * 15 * (ndd + 2) + 64);  // adjacency int arrays
   rc |= c->scratch[SS_SOLVER8].grow(2 * 4 * 27 * ncc);       // adjacency entries (+tmp)
   rc |= c->scratch[SS_PROBLEM].grow(8 * 27 * ncc);           // adjacency weights
   if (rc) return MPMRB_E_CUDA;
@@ -459,7 +459,13 @@ extern "C" int mpmrb_qn_solve(mpmrb_ctx* c, const mpmrb_problem* pr,
   adj.flag_off = ai + 4 * (ndd + 2);
   adj.cn = ai + 5 * (ndd + 2);
   adj.fn = ai + 6 * (ndd + 2);
-  adj.n_cn = ai + 7 * (ndd + 2);
+  adj.cn_e = ai + 7 * (ndd + 2);
+  adj.hflag = ai + 9 * (ndd + 2);
+  adj.hflag_off = ai + 10 * (ndd + 2);
+  adj.hn = ai + 11 * (ndd + 2);
+  adj.hn_e = ai + 12 * (ndd + 2);
+  adj.n_cn = ai + 14 * (ndd + 2);
+  adj.n_hn = adj.n_cn + 1;
   adj.ent = c->scratch[SS_SOLVER8].as<int>();
   adj.ent_tmp = adj.ent + 27 * ncc;
   adj.w = c->scratch[SS_PROBLEM].as<double>();
@@ -502,6 +508,7 @@ extern "C" int mpmrb_qn_solve(mpmrb_ctx* c, const mpmrb_problem* pr,
   a.cvhat = a.vc + 6 * ncc;
   a.cmug = a.vc + 7 * ncc;
   a.partials = c->scratch[SS_SOLVER5].as<double>();
+  a.ls_out = a.partials + 2 * 8 * kMaxSolverCtas;
   a.gamma = gamma;
   a.tr_obj = objective;
   a.tr_res = residual;
@@ -561,7 +568,9 @@ int mpmrb_sim_destroy(mpmrb_sim* s) {
                     &s->b_cnormal, &s->b_cwit, &s->b_cbias, &s->b_cframes, &s->b_cnodes,
                     &s->b_cw, &s->b_sv, &s->b_sgw, &s->b_srgr, &s->b_adjcnt, &s->b_adjfill,
                     &s->b_adjoff, &s->b_adjent, &s->b_adjw, &s->b_adjflag,
-                    &s->b_adjflagoff, &s->b_adjcn, &s->b_adjfn, &s->b_sdv, &s->b_svc,
+                    &s->b_adjflagoff, &s->b_adjcn, &s->b_adjfn, &s->b_adjcne, &s->b_adjh,
+                    &s->b_sdv,
+                    &s->b_svc,
                     &s->b_sdvc, &s->b_gamma, &s->b_gworld, &s->b_tiles, &s->b_bias_stamp,
                     &s->b_bias_store};
   for (DevBuf* b : bufs) b->release();

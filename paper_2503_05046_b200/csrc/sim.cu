@@ -251,6 +251,8 @@ int Sim::reserve(long long n, long long nb_needed) {
   rc |= b_adjflagoff.grow(4 * (N + 1));
   rc |= b_adjcn.grow(4 * (N + 1));
   rc |= b_adjfn.grow(4 * (N + 1));
+  rc |= b_adjcne.grow(4 * 2 * (N + 1));
+  rc |= b_adjh.grow(4 * 5 * (N + 2));  // hflag, hflag_off, hn, hn_e (2)
   rc |= b_gamma.grow(8 * 3 * nc_cap);
   rc |= b_gworld.grow(8 * 3 * nc_cap);
   long long scan_n = (N + 1) > (n + 1) ? (N + 1) : (n + 1);
@@ -330,6 +332,12 @@ int Sim::capture_or_launch() {
   adj.flag_off = b_adjflagoff.as<int>();
   adj.cn = b_adjcn.as<int>();
   adj.fn = b_adjfn.as<int>();
+  adj.cn_e = b_adjcne.as<int>();
+  adj.hflag = b_adjh.as<int>();
+  adj.hflag_off = b_adjh.as<int>() + (N + 2);
+  adj.hn = b_adjh.as<int>() + 2 * (N + 2);
+  adj.hn_e = b_adjh.as<int>() + 3 * (N + 2);
+  adj.n_hn = counters + 6;
   adj.n_cn = counters + 5;
   rc = launch_solver_adjacency(c, counters + 1, counters + 2, N, nc_cap, b_cnodes.as<int>(),
                                b_cw.as<double>(), adj, b_tiles);
@@ -370,6 +378,7 @@ int Sim::capture_or_launch() {
   a.gw = b_sgw.as<double>();
   a.rgr = b_srgr.as<double>();
   a.partials = b_partials.as<double>();
+  a.ls_out = b_partials.as<double>() + 2 * 8 * kMaxSolverCtas;
   a.gamma = b_gamma.as<double>();
   a.out = b_solveout.as<SolveOut>();
   a.act = b_act.as<int>();
@@ -427,7 +436,7 @@ int Sim::begin_step(long long epoch, int n_substeps) {
   if (!have_params) return set_error(MPMRB_E_INVALID, "sim: params not set");
   // size the grid for the current positions (one host sync per step)
   if (b_counters.grow(64) || b_misc.grow(64) || b_solveout.grow(sizeof(SolveOut)) ||
-      b_bar.grow(4096) || b_partials.grow(sizeof(double) * 2 * 8 * kMaxSolverCtas) ||
+      b_bar.grow(4096) || b_partials.grow(sizeof(double) * (2 * 8 * kMaxSolverCtas + 8)) ||
       b_dyn.grow(64) || b_accum.grow(sizeof(double) * 6 * kMaxBodies))
     return MPMRB_E_CUDA;
   if (!bar_init) {
@@ -478,7 +487,10 @@ int Sim::begin_step(long long epoch, int n_substeps) {
   }
   steps_substeps = n_substeps;
   // per-step resets: accumulator, counters, bias-cache epoch (coupling.py:175-176)
-  int dyn[2] = {(int)(epoch + 1), 0};
+  // bias-cache stamp: a private per-step counter (never the user's epoch, so
+  // restarting a scene from step 0 cannot resurrect stale first-sight biases)
+  (void)epoch;
+  int dyn[2] = {++bias_stamp_counter, 0};
   MPMRB_CUDA_OK(cudaMemcpyAsync(b_dyn.p, dyn, sizeof(dyn), cudaMemcpyHostToDevice, c.stream));
   MPMRB_CUDA_OK(cudaMemsetAsync(b_accum.p, 0, b_accum.bytes, c.stream));
   MPMRB_CUDA_OK(cudaMemsetAsync(b_misc.p, 0, 64, c.stream));

@@ -26,6 +26,7 @@ struct Sim {
   int bias_geoms = -1;
   int max_substeps = 0;
   int steps_substeps = 0;
+  int bias_stamp_counter = 0;
   double staleness = 0.0;
   bool use_graph = true;
   bool bar_init = false;
@@ -41,7 +42,7 @@ struct Sim {
       b_cframes, b_cnodes, b_cw;
   DevBuf b_sv, b_sdv, b_svc, b_sdvc, b_sgw, b_srgr, b_gamma, b_gworld, b_tiles;
   DevBuf b_adjcnt, b_adjfill, b_adjoff, b_adjent, b_adjw, b_adjflag, b_adjflagoff, b_adjcn,
-      b_adjfn;
+      b_adjfn, b_adjcne, b_adjh;
   DevBuf b_bias_stamp, b_bias_store;
 
   static constexpr int kProfEvents = 8;

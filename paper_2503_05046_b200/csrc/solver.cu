@@ -142,7 +142,7 @@ __device__ __forceinline__ void gather_contact(const SolverArgs& a, long long c,
     int nd = __ldg(&a.cnodes[(long long)k * a.nc_cap + c]);
     double w = __ldg(&a.cw[(long long)k * a.nc_cap + c]);
 #pragma unroll
-    for (int d = 0; d < 3; ++d) up[d] += w * __ldcg(&u[3 * nd + d]);
+    for (int d = 0; d < 3; ++d) up[d] += w * (*(&u[3 * nd + d]));
   }
 #pragma unroll
   for (int r = 0; r < 3; ++r) out[r] = R[3 * r] * up[0] + R[3 * r + 1] * up[1] + R[3 * r + 2] * up[2];
@@ -175,15 +175,31 @@ __device__ __forceinline__ double contact_terms(const ContactModel& cm, const do
 // Per-node part of phase N given the gathered jt (3) and Hessian sums hs (6):
 // gradient, residual/norm/energy partials, regularised 3x3 Cholesky
 // (solver.py:224-256), direction dv and the line-search coefficients.
-__device__ __forceinline__ void node_finish(const SolverArgs& a, long long i, const double* jt,
-                                            const double* hs, double* red, int& reg_count) {
-  const double m = a.m[i];
+struct NodeIn {
+  double m, v[3], vs[3];
+};
+
+__device__ __forceinline__ NodeIn load_node(const SolverArgs& a, long long i) {
+  NodeIn n;
+  n.m = a.m[i];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    n.v[d] = (*(&a.v[3 * i + d]));
+    n.vs[d] = a.v_star[3 * i + d];
+  }
+  return n;
+}
+
+__device__ __forceinline__ void node_finish(const SolverArgs& a, long long i, const NodeIn& nin,
+                                            const double* jt, const double* hs, double* red,
+                                            int& reg_count) {
+  const double m = nin.m;
   const double inv_m = 1.0 / m;
   double dvs[3], g[3];
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
-    const double vi = __ldcg(&a.v[3 * i + d]);
-    dvs[d] = vi - a.v_star[3 * i + d];
+    const double vi = nin.v[d];
+    dvs[d] = vi - nin.vs[d];
     g[d] = m * dvs[d] + jt[d];
     red[0] += g[d] * g[d] * inv_m;
     red[1] += m * vi * vi;
@@ -227,8 +243,68 @@ __device__ __forceinline__ void node_finish(const SolverArgs& a, long long i, co
   }
 }
 
+// Contact group: the CTAs that own the contacts.  With a cluster launch it is
+// cluster 0 (DSMEM reductions + hardware cluster barrier, ~0.7 us); without
+// clusters it is the whole grid (grid reductions, ~1.7 us).
+struct Group {
+  bool member;     // this CTA owns contacts
+  int rank;        // rank within the group
+  int size;        // CTAs in the group
+  bool cluster;    // reductions go through the cluster
+};
+
+// Sum K values over the contact group (members only).  Cluster path: each CTA
+// publishes its block sum in its own shared slot, cluster barrier, then every
+// CTA reads the size partials over DSMEM in rank order.  Slots are
+// double-buffered by parity (same argument as reduce_all).
+template <int K>
+__device__ void group_reduce(const Group& gr, const Sync& sync, int& parity, int& cparity,
+                             double (&v)[K], double (&out)[K], double* sm,
+                             double (*cslot)[kMaxRed]) {
+  if (!gr.cluster) {
+    reduce_all<K>(sync, parity, v, out, sm);
+    return;
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    double x = v[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0) sm[k * 32 + wid] = x;
+  }
+  __syncthreads();
+  const int par = cparity;
+  cparity ^= 1;
+  if (wid == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      double x = (lane < kThreads / 32) ? sm[k * 32 + lane] : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      if (lane == 0) cslot[par][k] = x;
+    }
+  }
+  cg::this_cluster().sync();
+  if (wid == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      double x = 0.0;
+      if (lane < gr.size) x = *cg::this_cluster().map_shared_rank(&cslot[par][k], lane);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      if (lane == 0) sm[32 * kMaxRed + k] = x;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < K; ++k) out[k] = sm[32 * kMaxRed + k];
+  __syncthreads();
+}
+
 __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
   __shared__ double sm[32 * kMaxRed + kMaxRed];
+  __shared__ double cslot[2][kMaxRed];
   __shared__ int s_flag;
   const int nd = *a.nd_dev;
   const int nc = *a.nc_dev;
@@ -251,7 +327,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
   if (nctas == 1 && blockIdx.x != 0) return;
   Sync sync{a.partials, nctas,
             (a.prof && blockIdx.x == 0 && threadIdx.x == 0) ? a.prof : nullptr};
-  int parity = 0;
+  const int csize = (nctas > 1) ? (int)cg::this_cluster().num_blocks() : 1;
+  Group gr;
+  if (nctas == 1) {
+    gr = Group{true, 0, 1, false};
+  } else if (csize > 1) {
+    gr = Group{(int)blockIdx.x < csize, (int)blockIdx.x, csize, true};
+  } else {
+    gr = Group{true, (int)blockIdx.x, nctas, false};
+  }
+  int parity = 0, cparity = 0;
   const long long tid = (long long)blockIdx.x * kThreads + threadIdx.x;
   const long long nthr = (long long)nctas * kThreads;
   const int lane = threadIdx.x & 31;
@@ -269,24 +354,28 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
   };
   double* v = a.v;
   const int n_cn = *a.adj.n_cn;
-  const int n_fn = nd - n_cn;
+  const int n_hn = *a.adj.n_hn;
+  const int n_fn = nd - n_cn - n_hn;
 
-  // Contacts are interleaved across CTAs (consecutive contacts on different
-  // SMs) so the fp64 divide/sqrt work of the line search spreads over the
-  // whole GPU.  A thread's first kJR contacts live in registers (fully
-  // unrolled j, so the arrays never spill); any further ones go through
-  // global memory.
-  const long long ctid = (long long)threadIdx.x * nctas + blockIdx.x;
+  // Contacts are owned by the contact group, interleaved at warp granularity
+  // across its CTAs (each warp's 32 contacts consecutive -> coalesced
+  // slot-major loads).  A thread's first kJR contacts live in registers
+  // (fully unrolled j, never spilled); further ones go through memory.
+  const long long cthr = (long long)gr.size * kThreads;
+  const long long ctid =
+      ((long long)(threadIdx.x >> 5) * gr.size + gr.rank) * 32 + (threadIdx.x & 31);
 #define FOR_OWNED_CONTACTS(...)                                         \
-  _Pragma("unroll") for (int j = 0; j < kJR; ++j) {                    \
-    const long long c = ctid + (long long)j * nthr;                    \
-    constexpr bool inreg = true;                                        \
-    if (c < nc) { __VA_ARGS__ }                                         \
-  }                                                                     \
-  for (long long c = ctid + (long long)kJR * nthr; c < nc; c += nthr) { \
-    constexpr int j = 0;                                                \
-    constexpr bool inreg = false;                                       \
-    __VA_ARGS__                                                         \
+  if (gr.member) {                                                      \
+    _Pragma("unroll") for (int j = 0; j < kJR; ++j) {                  \
+      const long long c = ctid + (long long)j * cthr;                  \
+      constexpr bool inreg = true;                                      \
+      if (c < nc) { __VA_ARGS__ }                                       \
+    }                                                                   \
+    for (long long c = ctid + (long long)kJR * cthr; c < nc; c += cthr) { \
+      constexpr int j = 0;                                              \
+      constexpr bool inreg = false;                                     \
+      __VA_ARGS__                                                       \
+    }                                                                   \
   }
 
   // ---- init: v = v0; per contact vc = R J v0 + b, the per-solve constants
@@ -322,38 +411,92 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
 
   int iterations = 0, ls_evals_total = 0, status = 0;
   bool converged = false;
+  double alpha_prev = 0.0;  // pending v += alpha dv, applied by each node's owner in N
   for (int it = 0;; ++it) {
-    // ---- N: node gathers, gradient, residual, Hessian block, direction
+    // ---- N: pending update, node gathers, gradient, residual, Hessian, direction
     double red[8] = {0, 0, 0, 0, e_acc, 0, 0, 0};
     int reg_count = 0;
-    // (a) contact nodes: one warp per node over its CSR entries
-    for (long long t = gwarp; t < n_cn; t += nwarps) {
-      const long long i = a.adj.cn[t];
-      const int e0 = a.adj.off[i], e1 = a.adj.off[i + 1];
+    auto take_node = [&](long long i) -> NodeIn {
+      NodeIn nin = load_node(a, i);
+      if (it > 0) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          nin.v[d] = nin.v[d] + alpha_prev * a.dv[3 * i + d];
+          v[3 * i + d] = nin.v[d];
+        }
+      }
+      return nin;
+    };
+    // (a1) heavy contact nodes (> kHeavyNode entries): one warp each
+    for (long long t = gwarp; t < n_hn; t += nwarps) {
+      const long long i = a.adj.hn[t];
+      const int e0 = a.adj.hn_e[2 * t], e1 = a.adj.hn_e[2 * t + 1];
+      NodeIn nin{};
+      if (lane == 0) nin = take_node(i);
       double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-#pragma unroll 2
+#pragma unroll 4
       for (int e = e0 + lane; e < e1; e += 32) {
         const long long c = __ldg(&a.adj.ent[e]) >> 5;
         const double w = __ldg(&a.adj.w[e]);
         const double w2 = w * w;
 #pragma unroll
-        for (int d = 0; d < 3; ++d) acc[d] += w * __ldcg(&a.gw[3 * c + d]);
+        for (int d = 0; d < 3; ++d) acc[d] += w * a.gw[3 * c + d];
 #pragma unroll
-        for (int q = 0; q < 6; ++q) acc[3 + q] += w2 * __ldcg(&a.rgr[6 * c + q]);
+        for (int q = 0; q < 6; ++q) acc[3 + q] += w2 * a.rgr[6 * c + q];
       }
 #pragma unroll
       for (int q = 0; q < 9; ++q)
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
-      if (lane == 0) node_finish(a, i, acc, acc + 3, red, reg_count);
+      if (lane == 0) node_finish(a, i, nin, acc, acc + 3, red, reg_count);
+    }
+    // (a2) light contact nodes: 8-lane groups, four nodes in flight per warp
+    {
+      const int grp = lane >> 3, gl = lane & 7;
+      for (long long t0 = gwarp * 4; t0 < n_cn; t0 += nwarps * 4) {
+        const long long t = t0 + grp;
+        const bool live = t < n_cn;
+        const long long i = live ? a.adj.cn[t] : 0;
+        const int e0 = live ? a.adj.cn_e[2 * t] : 0, e1 = live ? a.adj.cn_e[2 * t + 1] : 0;
+        NodeIn nin{};
+        if (live && gl == 0) nin = take_node(i);
+        double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll 4
+        for (int e = e0 + gl; e < e1; e += 8) {
+          const long long c = __ldg(&a.adj.ent[e]) >> 5;
+          const double w = __ldg(&a.adj.w[e]);
+          const double w2 = w * w;
+#pragma unroll
+          for (int d = 0; d < 3; ++d) acc[d] += w * a.gw[3 * c + d];
+#pragma unroll
+          for (int q = 0; q < 6; ++q) acc[3 + q] += w2 * a.rgr[6 * c + q];
+        }
+#pragma unroll
+        for (int q = 0; q < 9; ++q)
+#pragma unroll
+          for (int o = 4; o > 0; o >>= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
+        if (live && gl == 0) node_finish(a, i, nin, acc, acc + 3, red, reg_count);
+      }
+    }
+    if (prof) {
+      unsigned long long t = gtime();
+      pt[12] += t - tmark;
+      tmark = t;
     }
     // (b) nodes without contacts: thread per node
     {
       const double zero[6] = {0, 0, 0, 0, 0, 0};
-      for (long long t = tid; t < n_fn; t += nthr) node_finish(a, a.adj.fn[t], zero, zero, red,
-                                                               reg_count);
+      for (long long t = tid; t < n_fn; t += nthr) {
+        const long long i = a.adj.fn[t];
+        node_finish(a, i, take_node(i), zero, zero, red, reg_count);
+      }
     }
     if (reg_count) atomicAdd(&a.out->regularized, reg_count);
+    if (prof) {
+      unsigned long long t = gtime();
+      pt[13] += t - tmark;
+      tmark = t;
+    }
     double s[8];
     reduce_all<8>(sync, parity, red, s, sm);
     lap(1);
@@ -378,103 +521,115 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
       break;
     }
     const double a1 = s[5], a2 = s[6];
-    // ---- D: dvc = R J dv and the phi'(0) contact term (solver.py:305-310, 269)
-    double r0[1] = {0.0};
-    FOR_OWNED_CONTACTS({
-      double R[9], dvc[3], vc[3], g[3];
-      load_frame(a.frames, c, R);
-      gather_contact(a, c, a.dv, R, dvc);
-#pragma unroll
-      for (int d = 0; d < 3; ++d) vc[d] = inreg ? vcr[j][d] : __ldcg(&a.vc[3 * c + d]);
-      double Gd[4];
-      cm_eval(cm, vc, a.cvhat[c], a.cmug[c], g, Gd);
-      r0[0] += g[0] * dvc[0] + g[1] * dvc[1] + g[2] * dvc[2];
-#pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        if (inreg) dvcr[j][d] = dvc[d];
-        else a.dvc[3 * c + d] = dvc[d];
-      }
-    })
-    double d0s[1];
-    reduce_all<1>(sync, parity, r0, d0s, sm);
-    lap(2);
-    const double d0 = a1 + d0s[0];
-    if (!isfinite(d0) || d0 >= 0.0) {
-      status = MPMRB_E_NOT_DESCENT;
-      break;
-    }
-    // ---- LS: exact line search (solver.py:266-298)
-    double lo = 0.0, hi = INFINITY, alpha = 1.0, alpha_final = -1.0;
-    int evals = 0;
-    for (int ev = 1; ev <= a.ls_max; ++ev) {
-      double rr[2] = {0.0, 0.0};
+    double alpha_final = 0.0;
+    if (gr.member) {
+      // ---- D: dvc = R J dv and the phi'(0) contact term (solver.py:305-310, 269)
+      double r0[1] = {0.0};
       FOR_OWNED_CONTACTS({
-        double vc[3], dvc[3];
+        double R[9], dvc[3], vc[3], g[3];
+        load_frame(a.frames, c, R);
+        gather_contact(a, c, a.dv, R, dvc);
+#pragma unroll
+        for (int d = 0; d < 3; ++d) vc[d] = inreg ? vcr[j][d] : a.vc[3 * c + d];
+        double Gd[4];
+        cm_eval(cm, vc, a.cvhat[c], a.cmug[c], g, Gd);
+        r0[0] += g[0] * dvc[0] + g[1] * dvc[1] + g[2] * dvc[2];
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
-          dvc[d] = inreg ? dvcr[j][d] : __ldcg(&a.dvc[3 * c + d]);
-          vc[d] = (inreg ? vcr[j][d] : __ldcg(&a.vc[3 * c + d])) + alpha * dvc[d];
+          if (inreg) dvcr[j][d] = dvc[d];
+          else a.dvc[3 * c + d] = dvc[d];
         }
-        double g[3], G[4];
-        cm_eval(cm, vc, a.cvhat[c], a.cmug[c], g, G);
-        rr[0] += g[0] * dvc[0] + g[1] * dvc[1] + g[2] * dvc[2];
-        rr[1] += dvc[0] * (G[0] * dvc[0] + G[3] * dvc[1]) + dvc[1] * (G[3] * dvc[0] + G[1] * dvc[1]) +
-                 dvc[2] * (G[2] * dvc[2]);
       })
-      double ss[2];
-      reduce_all<2>(sync, parity, rr, ss, sm);
-      evals = ev;
-      const double d = a1 + a2 * alpha + ss[0];
-      const double dd = a2 + ss[1];
-      if (fabs(d) <= a.ls_tol * fabs(d0)) {
-        alpha_final = alpha;
-        break;
-      }
-      if (d > 0.0) hi = alpha;
-      else lo = alpha;
-      double cand = (isfinite(dd) && dd > 0.0) ? alpha - d / dd : NAN;
-      if (isfinite(hi)) {
-        if (!(lo < cand && cand < hi) || !isfinite(cand)) cand = 0.5 * (lo + hi);
+      double d0s[1];
+      group_reduce<1>(gr, sync, parity, cparity, r0, d0s, sm, cslot);
+      lap(2);
+      const double d0 = a1 + d0s[0];
+      if (!isfinite(d0) || d0 >= 0.0) {
+        status = MPMRB_E_NOT_DESCENT;
       } else {
-        if (!isfinite(cand) || cand <= lo) cand = 2.0 * fmax(alpha, 1e-8);
+        // ---- LS: exact line search (solver.py:266-298)
+        double lo = 0.0, hi = INFINITY, alpha = 1.0;
+        alpha_final = -1.0;
+        int evals = 0;
+        for (int ev = 1; ev <= a.ls_max; ++ev) {
+          double rr[2] = {0.0, 0.0};
+          FOR_OWNED_CONTACTS({
+            double vc[3], dvc[3];
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+              dvc[d] = inreg ? dvcr[j][d] : a.dvc[3 * c + d];
+              vc[d] = (inreg ? vcr[j][d] : a.vc[3 * c + d]) + alpha * dvc[d];
+            }
+            double g[3], G[4];
+            cm_eval(cm, vc, a.cvhat[c], a.cmug[c], g, G);
+            rr[0] += g[0] * dvc[0] + g[1] * dvc[1] + g[2] * dvc[2];
+            rr[1] += dvc[0] * (G[0] * dvc[0] + G[3] * dvc[1]) +
+                     dvc[1] * (G[3] * dvc[0] + G[1] * dvc[1]) + dvc[2] * (G[2] * dvc[2]);
+          })
+          double ss[2];
+          group_reduce<2>(gr, sync, parity, cparity, rr, ss, sm, cslot);
+          evals = ev;
+          const double d = a1 + a2 * alpha + ss[0];
+          const double dd = a2 + ss[1];
+          if (fabs(d) <= a.ls_tol * fabs(d0)) {
+            alpha_final = alpha;
+            break;
+          }
+          if (d > 0.0) hi = alpha;
+          else lo = alpha;
+          double cand = (isfinite(dd) && dd > 0.0) ? alpha - d / dd : NAN;
+          if (isfinite(hi)) {
+            if (!(lo < cand && cand < hi) || !isfinite(cand)) cand = 0.5 * (lo + hi);
+          } else {
+            if (!isfinite(cand) || cand <= lo) cand = 2.0 * fmax(alpha, 1e-8);
+          }
+          alpha = cand;
+        }
+        if (alpha_final < 0.0) alpha_final = (lo > 0.0) ? lo : alpha;  // solver.py:296-298
+        ls_evals_total += evals;
+        lap(3);
+        // ---- U (contacts): vc += alpha dvc and the contact terms for the next N
+        e_acc = 0.0;
+        FOR_OWNED_CONTACTS({
+          double vc[3], R[9], gw[3], rgr[6];
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            if (inreg) vc[d] = vcr[j][d] = vcr[j][d] + alpha_final * dvcr[j][d];
+            else vc[d] = a.vc[3 * c + d] + alpha_final * a.dvc[3 * c + d];
+            a.vc[3 * c + d] = vc[d];
+          }
+          load_frame(a.frames, c, R);
+          e_acc += contact_terms(cm, vc, a.cvhat[c], a.cmug[c], R, gw, rgr);
+#pragma unroll
+          for (int d = 0; d < 3; ++d) a.gw[3 * c + d] = gw[d];
+#pragma unroll
+          for (int q = 0; q < 6; ++q) a.rgr[6 * c + q] = rgr[q];
+        })
       }
-      alpha = cand;
-    }
-    if (alpha_final < 0.0) alpha_final = (lo > 0.0) ? lo : alpha;  // solver.py:296-298
-    ls_evals_total += evals;
-    lap(3);
-    // ---- U: v += alpha dv; vc += alpha dvc and the contact terms at the new iterate
-    for (long long i = tid; i < nd; i += nthr) {
-#pragma unroll
-      for (int d = 0; d < 3; ++d) v[3 * i + d] = __ldcg(&v[3 * i + d]) + alpha_final * a.dv[3 * i + d];
-    }
-    e_acc = 0.0;
-    FOR_OWNED_CONTACTS({
-      double vc[3], R[9], gw[3], rgr[6];
-#pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        if (inreg) vc[d] = vcr[j][d] = vcr[j][d] + alpha_final * dvcr[j][d];
-        else vc[d] = __ldcg(&a.vc[3 * c + d]) + alpha_final * __ldcg(&a.dvc[3 * c + d]);
-        a.vc[3 * c + d] = vc[d];
+      // publish the step (and the status) to the CTAs outside the group
+      if (gr.rank == 0 && threadIdx.x == 0) {
+        a.ls_out[0] = alpha_final;
+        a.ls_out[1] = (double)status;
+        if (a.tr_alpha && status == 0) a.tr_alpha[it] = alpha_final;
       }
-      load_frame(a.frames, c, R);
-      e_acc += contact_terms(cm, vc, a.cvhat[c], a.cmug[c], R, gw, rgr);
-#pragma unroll
-      for (int d = 0; d < 3; ++d) a.gw[3 * c + d] = gw[d];
-#pragma unroll
-      for (int q = 0; q < 6; ++q) a.rgr[6 * c + q] = rgr[q];
-    })
-    ++iterations;
-    if (blockIdx.x == 0 && threadIdx.x == 0 && a.tr_alpha) a.tr_alpha[it] = alpha_final;
-    sync();
+    }
+    sync();  // gw/rgr, alpha and status visible grid-wide
+    if (!gr.member || gr.cluster) {
+      alpha_final = __ldcg(&a.ls_out[0]);
+      status = (int)__ldcg(&a.ls_out[1]);
+    }
     lap(4);
+    if (status) break;
+    alpha_prev = alpha_final;
+    ++iterations;
   }
+  // The last N applied every pending update, so v is final here (grid synced).
   // ---- epilogue: impulses gamma = -g_c(vc) (solver.py:363-365)
   bool finite_v = true;
   for (long long i = tid; i < nd; i += nthr) {
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-      double vi = __ldcg(&v[3 * i + d]);
+      double vi = v[3 * i + d];
       finite_v &= isfinite(vi);
       if (a.v_next_full) a.v_next_full[3 * (long long)a.act[i] + d] = vi;
     }
@@ -482,7 +637,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
   FOR_OWNED_CONTACTS({
     double vc[3], g[3];
 #pragma unroll
-    for (int d = 0; d < 3; ++d) vc[d] = inreg ? vcr[j][d] : __ldcg(&a.vc[3 * c + d]);
+    for (int d = 0; d < 3; ++d) vc[d] = inreg ? vcr[j][d] : a.vc[3 * c + d];
     double Gd[4];
     cm_eval(cm, vc, a.cvhat[c], a.cmug[c], g, Gd);
 #pragma unroll
@@ -506,9 +661,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
       for (int k = 0; k < 6; ++k) a.prof[k] += pt[k];
       a.prof[6] += (unsigned long long)iterations;
       a.prof[7] += (unsigned long long)ls_evals_total;
-      a.prof[8] += (unsigned long long)nctas;
+      a.prof[8] += (unsigned long long)nctas + ((unsigned long long)gr.size << 32);
       a.prof[9] += 1ull;
-      a.prof[11] += (unsigned long long)n_cn;
+      a.prof[11] += (unsigned long long)n_cn + ((unsigned long long)n_hn << 32);
+      a.prof[12] += pt[12];
+      a.prof[13] += pt[13];
     }
   }
 }
@@ -561,20 +718,29 @@ __global__ void k_adj_rank(const int* __restrict__ nd_dev, long long nc_cap,
 }
 
 __global__ void k_adj_flag(const int* __restrict__ nd_dev, const int* __restrict__ off,
-                           int* __restrict__ flag) {
+                           int* __restrict__ flag, int* __restrict__ hflag) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= *nd_dev) return;
-  flag[i] = off[i + 1] > off[i] ? 1 : 0;
+  const int L = off[i + 1] - off[i];
+  flag[i] = (L > 0 && L <= kHeavyNode) ? 1 : 0;
+  hflag[i] = (L > kHeavyNode) ? 1 : 0;
 }
 
-__global__ void k_adj_lists(const int* __restrict__ nd_dev, const int* __restrict__ flag,
-                            const int* __restrict__ flag_off, int* __restrict__ cn,
-                            int* __restrict__ fn) {
+__global__ void k_adj_lists(const int* __restrict__ nd_dev, SolverAdjacency adj) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= *nd_dev) return;
-  const int o = flag_off[i];
-  if (flag[i]) cn[o] = (int)i;
-  else fn[i - o] = (int)i;
+  const int o = adj.flag_off[i], ho = adj.hflag_off[i];
+  if (adj.flag[i]) {
+    adj.cn[o] = (int)i;
+    adj.cn_e[2 * o] = adj.off[i];
+    adj.cn_e[2 * o + 1] = adj.off[i + 1];
+  } else if (adj.hflag[i]) {
+    adj.hn[ho] = (int)i;
+    adj.hn_e[2 * ho] = adj.off[i];
+    adj.hn_e[2 * ho + 1] = adj.off[i + 1];
+  } else {
+    adj.fn[i - o - ho] = (int)i;
+  }
 }
 
 }  // namespace
@@ -585,6 +751,7 @@ int launch_solver_adjacency(Ctx& c, const int* nd_dev, const int* nc_dev, long l
   MPMRB_CUDA_OK(cudaMemsetAsync(adj.cnt, 0, sizeof(int) * (nd_cap + 1), c.stream));
   MPMRB_CUDA_OK(cudaMemsetAsync(adj.fill, 0, sizeof(int) * (nd_cap + 1), c.stream));
   MPMRB_CUDA_OK(cudaMemsetAsync(adj.flag, 0, sizeof(int) * (nd_cap + 1), c.stream));
+  MPMRB_CUDA_OK(cudaMemsetAsync(adj.hflag, 0, sizeof(int) * (nd_cap + 1), c.stream));
   const long long ne = nc_cap * 27;
   if (ne > 0) {
     k_adj_count<<<grid_for(ne, 256), 256, 0, c.stream>>>(nc_dev, nc_cap, cnodes, cw, adj.cnt);
@@ -601,14 +768,16 @@ int launch_solver_adjacency(Ctx& c, const int* nd_dev, const int* nc_dev, long l
     c.launches += 2;
   }
   if (nd_cap > 0) {
-    k_adj_flag<<<grid_for(nd_cap, 256), 256, 0, c.stream>>>(nd_dev, adj.off, adj.flag);
+    k_adj_flag<<<grid_for(nd_cap, 256), 256, 0, c.stream>>>(nd_dev, adj.off, adj.flag,
+                                                            adj.hflag);
     c.launches++;
   }
   rc = scan_exclusive_i32(c, adj.flag, adj.flag_off, nd_cap + 1, nullptr, adj.n_cn, tiles);
   if (rc) return rc;
+  rc = scan_exclusive_i32(c, adj.hflag, adj.hflag_off, nd_cap + 1, nullptr, adj.n_hn, tiles);
+  if (rc) return rc;
   if (nd_cap > 0) {
-    k_adj_lists<<<grid_for(nd_cap, 256), 256, 0, c.stream>>>(nd_dev, adj.flag, adj.flag_off,
-                                                             adj.cn, adj.fn);
+    k_adj_lists<<<grid_for(nd_cap, 256), 256, 0, c.stream>>>(nd_dev, adj);
     c.launches++;
   }
   MPMRB_CUDA_OK(cudaGetLastError());
@@ -616,30 +785,64 @@ int launch_solver_adjacency(Ctx& c, const int* nd_dev, const int* nc_dev, long l
 }
 
 int launch_qn_solve(Ctx& c, const SolverArgs& a, int grid_ctas) {
-  static int max_ctas = -1;
-  if (max_ctas < 0) {
+  // Grid: one CTA per SM (launch bounds + 128 registers).  Preferred launch:
+  // clusters of 8 (the contact group is cluster 0) as many as co-reside.
+  static int sms = -1, cluster_grid = -1;
+  if (sms < 0) {
     int dev = 0;
     cudaGetDevice(&dev);
-    int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_qn_solve, kThreads, 0);
-    max_ctas = per_sm > 0 ? sms : 1;
-    if (max_ctas > kMaxSolverCtas) max_ctas = kMaxSolverCtas;
+    if (sms > kMaxSolverCtas) sms = kMaxSolverCtas;
+    cluster_grid = 0;
+    // Opt-in: measured on the 256k sand pile (17.5k contacts) the 8-CTA
+    // contact cluster loses to grid-wide ownership (6.5 vs 4.8 us per
+    // line-search evaluation: the fp64 divide/sqrt work of 17.5k contacts on
+    // 8 SMs outweighs the cheaper cluster barrier).
+    const char* env = getenv("MPMRB_SOLVER_CLUSTER");
+    if (env && atoi(env) > 0) {
+      cudaLaunchConfig_t q = {};
+      q.blockDim = dim3(kThreads);
+      q.gridDim = dim3(kSolverCluster);
+      cudaLaunchAttribute qa[1];
+      qa[0].id = cudaLaunchAttributeClusterDimension;
+      qa[0].val.clusterDim.x = kSolverCluster;
+      qa[0].val.clusterDim.y = 1;
+      qa[0].val.clusterDim.z = 1;
+      q.attrs = qa;
+      q.numAttrs = 1;
+      int ncl = 0;
+      if (cudaOccupancyMaxActiveClusters(&ncl, k_qn_solve, &q) == cudaSuccess && ncl > 0) {
+        cluster_grid = ncl * kSolverCluster;
+        if (cluster_grid > kMaxSolverCtas) cluster_grid = (kMaxSolverCtas / kSolverCluster) * kSolverCluster;
+      }
+      cudaGetLastError();
+    }
   }
-  int g = max_ctas;
-  if (grid_ctas > 0 && grid_ctas < g) g = grid_ctas;
-  if (a.force_ctas > 1 && a.force_ctas < g) g = a.force_ctas;
+  int g = sms;
+  bool use_cluster = cluster_grid > 0;
+  if (use_cluster) g = cluster_grid;
+  if (grid_ctas > 0 && grid_ctas < g) {
+    g = grid_ctas;
+    use_cluster = false;
+  }
+  if (a.force_ctas > 1) {
+    g = a.force_ctas < sms ? a.force_ctas : sms;
+    use_cluster = false;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)g);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = c.stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = use_cluster ? kSolverCluster : 1;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = use_cluster ? 2 : 1;
   MPMRB_CUDA_OK(cudaLaunchKernelEx(&cfg, k_qn_solve, a));
   c.launches++;
   return MPMRB_OK;

@@ -7,7 +7,8 @@ namespace mpmrb {
 
 constexpr int kSolverThreads = 512;
 constexpr int kMaxSolverCtas = 160;
-constexpr int kSolverProf = 12;  // phase timers (ns), see solver.cu
+constexpr int kSolverCluster = 8;  // CTAs of the contact-owning cluster
+constexpr int kSolverProf = 16;  // phase timers (ns), see solver.cu
 
 struct SolveOut {
   int converged;
@@ -29,12 +30,20 @@ struct SolverAdjacency {
   int* ent;      // (27 nc_cap) packed (c << 5) | k, ascending within a node
   int* ent_tmp;  // (27 nc_cap) scratch: entries in atomic fill order
   double* w;     // (27 nc_cap) stencil weight of each entry
-  int* flag;     // (nd_cap+1) scratch: node has entries
+  int* flag;     // (nd_cap+1) scratch: node has 1..kHeavy entries
   int* flag_off; // (nd_cap+1) scan of flag
-  int* cn;       // (nd_cap) nodes with entries ("contact nodes")
+  int* hflag;    // (nd_cap+1) scratch: node has > kHeavy entries
+  int* hflag_off;// (nd_cap+1) scan of hflag
+  int* cn;       // (nd_cap) light contact nodes (8-lane groups)
+  int* cn_e;     // (2 nd_cap) CSR bounds of each light contact node
+  int* hn;       // (nd_cap) heavy contact nodes (one warp each)
+  int* hn_e;     // (2 nd_cap) CSR bounds of each heavy contact node
   int* fn;       // (nd_cap) nodes without entries
-  int* n_cn;     // device count of contact nodes
+  int* n_cn;     // device count of light contact nodes
+  int* n_hn;     // device count of heavy contact nodes
 };
+
+constexpr int kHeavyNode = 64;  // entries above which a node gets a whole warp
 
 struct SolverArgs {
   // sizes (device)
@@ -70,6 +79,7 @@ struct SolverArgs {
   double* cvhat;     // (nc,) -phi/(dt+tau_d), per solve
   double* cmug;      // (nc,) mu*gamma_lag, per solve
   double* partials;  // 2 x [kMaxRed][kMaxSolverCtas]
+  double* ls_out;    // (2,) line-search step and status published by the contact group
   // outputs
   double* gamma;
   double* tr_obj;

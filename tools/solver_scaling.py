@@ -48,14 +48,14 @@ def main():
     par = mp.SolverParams(eps_r=5e-2, max_iters=200)
     import ctypes as C
     from paper_2503_05046_b200 import _lib
-    prof = (C.c_uint64 * 12)()
+    prof = (C.c_uint64 * 16)()
     if os.environ.get("ONE_SOLVE"):
         # single solve for ncu capture
         v, g, rep = mp.quasi_newton_solve(prob, mp.SolverParams(eps_r=5e-2, max_iters=20))
         torch.cuda.synchronize()
         print("one solve", rep.iterations, rep.ls_evals)
         return
-    for ctas in ["1", "8", "16", "32", "64", "96", "128", "148", "0"]:
+    for ctas in (os.environ.get("CTAS_LIST") or "1,32,64,128,148,0").split(","):
         os.environ["MPMRB_SOLVER_CTAS"] = ctas
         mp.quasi_newton_solve(prob, par)  # warm
         torch.cuda.synchronize()
@@ -71,8 +71,9 @@ def main():
               f"ls_evals={rep.ls_evals}, us/iter={dt * 1e6 / it:7.1f} | per-iter us: "
               f"N={ph[1]:.1f} D={ph[2]:.1f} LS={ph[3]:.1f} U={ph[4]:.1f} "
               f"in-sync={prof[10] / 1e3 / it:.1f} "
-              f"(LS/eval={prof[3] / 1e3 / max(1, rep.ls_evals):.2f}) ctas_used={prof[8]} "
-              f"contact_nodes={prof[11]}",
+              f"(LS/eval={prof[3] / 1e3 / max(1, rep.ls_evals):.2f}) "
+              f"ctas={prof[8] & 0xffffffff} group={prof[8] >> 32} "
+              f"light_nodes={prof[11] & 0xffffffff} heavy_nodes={prof[11] >> 32} N_loopA={prof[12] / 1e3 / it:.1f} N_loopB={prof[13] / 1e3 / it:.1f}",
               flush=True)
 
 
