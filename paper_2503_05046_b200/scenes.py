@@ -154,3 +154,55 @@ def scaled(scene: dict, **kw) -> dict:
     s = copy.deepcopy(scene)
     s.update(kw)
     return s
+
+
+# ------------------------------------------------------------------ interop
+
+def from_reference_state(ref) -> SimState:
+    """Build a device ``SimState`` from a reference ``mpmrb.coupling.SimState``
+    (coupling.py:87-112), duck-typed: particle arrays (particles.py:12-64) are
+    uploaded once, materials (materials.py:24-46), bodies (bodies.py:20-113),
+    step, contact and solver parameters are carried over field by field.
+    Rigid bodies are re-created from their public fields (the GPU path only
+    reads poses, velocities and geoms)."""
+    from .particles import ParticleSet
+    rp = ref.particles
+    particles = ParticleSet(np.asarray(rp.x), np.asarray(rp.v), np.asarray(rp.f),
+                            np.asarray(rp.c), np.asarray(rp.mass), np.asarray(rp.volume0),
+                            np.asarray(rp.material_id, dtype=np.int64))
+    mats = [Material(m.youngs_modulus, m.poisson_ratio, m.density,
+                     model=getattr(m, "model", "elastic"),
+                     friction_angle=getattr(m, "friction_angle", 30.0)) for m in ref.materials]
+    shapes = {"HalfSpace": lambda s: HalfSpace(normal=tuple(s.normal), offset=float(s.offset)),
+              "Sphere": lambda s: Sphere(radius=float(s.radius)),
+              "Box": lambda s: Box(half_extents=tuple(float(a) for a in s.half_extents)),
+              "Capsule": lambda s: Capsule(radius=float(s.radius),
+                                           half_length=float(s.half_length))}
+    bodies = []
+    for b in ref.bodies:
+        geoms = [GeomAttachment(shape=shapes[type(g.shape).__name__](g.shape),
+                                position=np.asarray(g.position, float),
+                                quat=np.asarray(g.quat, float), mu=float(g.mu)) for g in b.geoms]
+        traj = None
+        if getattr(b, "trajectory", None) is not None:
+            t = b.trajectory
+            traj = Trajectory(times=np.asarray(t.times), positions=np.asarray(t.positions),
+                              quats=np.asarray(t.quats))
+        kw = {} if b.kinematic else dict(mass=float(b.mass),
+                                         inertia_body=np.asarray(b.inertia_body, float))
+        bodies.append(RigidBody(name=b.name, kinematic=bool(b.kinematic), geoms=geoms,
+                                position=np.asarray(b.position, float),
+                                quat=np.asarray(b.quat, float), v=np.asarray(b.v, float),
+                                omega=np.asarray(b.omega, float), trajectory=traj, **kw))
+    cp, sp = ref.contact_params, ref.solver_params
+    st = SimState(particles=particles, materials=mats, bodies=bodies, h=float(ref.h),
+                  step=StepConfig(dt=float(ref.step.dt), substeps=int(ref.step.substeps),
+                                  gravity=tuple(float(a) for a in ref.step.gravity)),
+                  contact_params=ContactParams(stiffness=cp.stiffness, tau_d=cp.tau_d,
+                                               eps_v=cp.eps_v, margin=cp.margin),
+                  solver_params=SolverParams(eps_a=sp.eps_a, eps_r=sp.eps_r,
+                                             max_iters=sp.max_iters,
+                                             ls_max_iters=sp.ls_max_iters, ls_tol=sp.ls_tol))
+    st.time = float(getattr(ref, "time", 0.0))
+    st.step_index = int(getattr(ref, "step_index", 0))
+    return st
