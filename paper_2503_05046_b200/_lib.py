@@ -133,6 +133,7 @@ _SIGS = {
     "mpmrb_qn_solve": ([_P, C.POINTER(Problem), C.POINTER(SolverParamsC), _P, _P, _P, _P, _P, _P,
                         _P, C.POINTER(SolveReportC)], C.c_int),
     "mpmrb_solver_profile": ([_P, C.POINTER(C.c_uint64), C.c_int32], C.c_int),
+    "mpmrb_solver_profile_cta": ([_P, C.POINTER(C.c_uint64)], C.c_int),
     "mpmrb_sim_create":([_P, C.POINTER(C.c_void_p)], C.c_int),
     "mpmrb_sim_destroy": ([_P], C.c_int),
     "mpmrb_sim_set_particles": ([_P, C.POINTER(Particles)], C.c_int),

@@ -104,8 +104,8 @@ int mpmrb_create(int device, mpmrb_ctx** out) {
   cudaMemset(c->status, 0, sizeof(DevStatus));
   const char* prof = getenv("MPMRB_SOLVER_PROF");
   if (prof && atoi(prof) > 0) {
-    if (cudaMalloc(&c->solver_prof, 8 * kSolverProf) == cudaSuccess)
-      cudaMemset(c->solver_prof, 0, 8 * kSolverProf);
+    if (cudaMalloc(&c->solver_prof, 8 * kSolverProfWords) == cudaSuccess)
+      cudaMemset(c->solver_prof, 0, 8 * kSolverProfWords);
     else
       c->solver_prof = nullptr;
   }
@@ -121,7 +121,19 @@ int mpmrb_solver_profile(mpmrb_ctx* c, uint64_t* out_host, int32_t reset) {
   }
   MPMRB_CUDA_OK(cudaStreamSynchronize(c->stream));
   MPMRB_CUDA_OK(cudaMemcpy(out_host, c->solver_prof, 8 * kSolverProf, cudaMemcpyDeviceToHost));
-  if (reset) MPMRB_CUDA_OK(cudaMemset(c->solver_prof, 0, 8 * kSolverProf));
+  if (reset) MPMRB_CUDA_OK(cudaMemset(c->solver_prof, 0, 8 * kSolverProfWords));
+  return MPMRB_OK;
+}
+
+int mpmrb_solver_profile_cta(mpmrb_ctx* c, uint64_t* out_host) {
+  CHECK_CTX(c);
+  if (!c->solver_prof) {
+    std::memset(out_host, 0, 8 * (kSolverProfWords - kSolverProf));
+    return MPMRB_OK;
+  }
+  MPMRB_CUDA_OK(cudaStreamSynchronize(c->stream));
+  MPMRB_CUDA_OK(cudaMemcpy(out_host, c->solver_prof + kSolverProf,
+                           8 * (kSolverProfWords - kSolverProf), cudaMemcpyDeviceToHost));
   return MPMRB_OK;
 }
 
@@ -413,7 +425,8 @@ __global__ void k_problem_layout(const long long* __restrict__ nodes, const doub
   long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (e >= nc * 27) return;
   long long c = e / 27, k = e % 27;
-  cnodes[k * nc + c] = (int)nodes[e];
+  // dead slots (w = 0, solver.py:207-213) carry no node
+  cnodes[k * nc + c] = (w[e] == 0.0) ? -1 : (int)nodes[e];
   cw[k * nc + c] = w[e];
 }
 }  // namespace
@@ -430,13 +443,14 @@ extern "C" int mpmrb_qn_solve(mpmrb_ctx* c, const mpmrb_problem* pr,
   rc |= c->scratch[SS_SOLVER0].grow(4 * 27 * ncc);           // cnodes
   rc |= c->scratch[SS_SOLVER1].grow(8 * 27 * ncc);           // cw
   rc |= c->scratch[SS_SOLVER2].grow(8 * 3 * ndd);            // dv
-  rc |= c->scratch[SS_SOLVER3].grow(8 * 9 * ncc);            // gw (3), rgr (6)
+  rc |= c->scratch[SS_SOLVER3].grow(8 * kCellSumStride * 27 * ncc);  // cellsum
   rc |= c->scratch[SS_SOLVER4].grow(8 * 8 * ncc);            // vc, dvc, vhat, mug
-  rc |= c->scratch[SS_SOLVER5].grow(8 * (2 * 8 * kMaxSolverCtas + 8));  // partials, ls_out
-  rc |= c->scratch[SS_SOLVER6].grow(4096);                   // flags, sizes, SolveOut
-  rc |= c->scratch[SS_SOLVER7].grow(4 * 15 * (ndd + 2) + 64);  // adjacency int arrays
+  rc |= c->scratch[SS_SOLVER5].grow(8 * (2 * 8 * kMaxSolverCtas + 8));  // grid partials
+  rc |= c->scratch[SS_SOLVER6].grow(4096);                   // sizes, SolveOut
+  rc |= c->scratch[SS_SOLVER7].grow(4 * 12 * (ndd + 2) + 64);  // node adjacency ints
   rc |= c->scratch[SS_SOLVER8].grow(2 * 4 * 27 * ncc);       // adjacency entries (+tmp)
-  rc |= c->scratch[SS_PROBLEM].grow(8 * 27 * ncc);           // adjacency weights
+  rc |= c->scratch[SS_PROBLEM].grow(4 * 4 * (ncc + 2));      // contact groups
+  rc |= c->scratch[SS_HOSTINFO].grow(8 * kSolverSlotWords + 64);  // reduction slots + tags
   if (rc) return MPMRB_E_CUDA;
   char* misc = c->scratch[SS_SOLVER6].as<char>();
   int* sizes = (int*)(misc + 2048);
@@ -444,40 +458,48 @@ extern "C" int mpmrb_qn_solve(mpmrb_ctx* c, const mpmrb_problem* pr,
   MPMRB_CUDA_OK(cudaMemsetAsync(misc, 0, 4096, c->stream));
   int hs[2] = {(int)nd, (int)nc};
   MPMRB_CUDA_OK(cudaMemcpyAsync(sizes, hs, sizeof(hs), cudaMemcpyHostToDevice, c->stream));
+  unsigned long long* slots = c->scratch[SS_HOSTINFO].as<unsigned long long>();
+  unsigned* chan = reinterpret_cast<unsigned*>(slots + kSolverSlotWords);
+  {
+    MPMRB_CUDA_OK(cudaMemsetAsync(slots, 0, 8 * kSolverSlotWords, c->stream));
+    static const unsigned ch[4] = {1u, 1u, 1u, 1u};
+    MPMRB_CUDA_OK(cudaMemcpyAsync(chan, ch, sizeof(ch), cudaMemcpyHostToDevice, c->stream));
+  }
   if (nc > 0) {
     k_problem_layout<<<grid_for(nc * 27, 256), 256, 0, c->stream>>>(
         (const long long*)pr->nodes, pr->w, nc, c->scratch[SS_SOLVER0].as<int>(),
         c->scratch[SS_SOLVER1].as<double>());
     c->launches++;
   }
-  int* ai = c->scratch[SS_SOLVER7].as<int>();
-  SolverAdjacency adj{};
-  adj.cnt = ai;
-  adj.fill = ai + (ndd + 2);
-  adj.off = ai + 2 * (ndd + 2);
-  adj.flag = ai + 3 * (ndd + 2);
-  adj.flag_off = ai + 4 * (ndd + 2);
-  adj.cn = ai + 5 * (ndd + 2);
-  adj.fn = ai + 6 * (ndd + 2);
-  adj.cn_e = ai + 7 * (ndd + 2);
-  adj.hflag = ai + 9 * (ndd + 2);
-  adj.hflag_off = ai + 10 * (ndd + 2);
-  adj.hn = ai + 11 * (ndd + 2);
-  adj.hn_e = ai + 12 * (ndd + 2);
-  adj.n_cn = ai + 14 * (ndd + 2);
-  adj.n_hn = adj.n_cn + 1;
-  adj.ent = c->scratch[SS_SOLVER8].as<int>();
-  adj.ent_tmp = adj.ent + 27 * ncc;
-  adj.w = c->scratch[SS_PROBLEM].as<double>();
-  rc = launch_solver_adjacency(*c, sizes, sizes + 1, nd, nc, c->scratch[SS_SOLVER0].as<int>(),
-                               c->scratch[SS_SOLVER1].as<double>(), adj, c->scratch[SS_TILE]);
+  SolverSetup su{};
+  {
+    int* ni = c->scratch[SS_SOLVER7].as<int>();
+    su.cnt = ni;
+    su.fill = ni + (ndd + 2);
+    su.off = ni + 2 * (ndd + 2);
+    su.flag = ni + 3 * (ndd + 2);
+    su.flag_off = ni + 4 * (ndd + 2);
+    su.cn = ni + 5 * (ndd + 2);
+    su.fn = ni + 6 * (ndd + 2);
+    su.counts = ni + 7 * (ndd + 2);
+    su.cn_rec = reinterpret_cast<int4*>(ni + 8 * (ndd + 2));
+    int* ci = c->scratch[SS_PROBLEM].as<int>();
+    su.head = ci;
+    su.head_off = ci + (ncc + 2);
+    su.grp_of = ci + 2 * (ncc + 2);
+    su.grp_start = ci + 3 * (ncc + 2);
+    su.ent = c->scratch[SS_SOLVER8].as<int>();
+    su.ent_tmp = su.ent + 27 * ncc;
+  }
+  rc = launch_solver_setup(*c, sizes, sizes + 1, nd, nc, c->scratch[SS_SOLVER0].as<int>(), su,
+                           c->scratch[SS_TILE]);
   if (rc) return rc;
   SolverArgs a{};
   a.nd_dev = sizes;
   a.nc_dev = sizes + 1;
   a.nc_cap = nc;
   a.nd_cap = nd;
-  a.adj = adj;
+  a.su = su;
   a.prof = c->solver_prof;
   a.m = pr->m;
   a.v_star = pr->v_star;
@@ -501,14 +523,14 @@ extern "C" int mpmrb_qn_solve(mpmrb_ctx* c, const mpmrb_problem* pr,
   a.force_ctas = 0;
   a.v = v;
   a.dv = c->scratch[SS_SOLVER2].as<double>();
-  a.gw = c->scratch[SS_SOLVER3].as<double>();
-  a.rgr = a.gw + 3 * ncc;
+  a.cellsum = c->scratch[SS_SOLVER3].as<double>();
   a.vc = c->scratch[SS_SOLVER4].as<double>();
   a.dvc = a.vc + 3 * ncc;
   a.cvhat = a.vc + 6 * ncc;
   a.cmug = a.vc + 7 * ncc;
   a.partials = c->scratch[SS_SOLVER5].as<double>();
-  a.ls_out = a.partials + 2 * 8 * kMaxSolverCtas;
+  a.slots = slots;
+  a.chan = chan;
   a.gamma = gamma;
   a.tr_obj = objective;
   a.tr_res = residual;
@@ -519,6 +541,9 @@ extern "C" int mpmrb_qn_solve(mpmrb_ctx* c, const mpmrb_problem* pr,
   a.v_next_full = nullptr;
   const char* force = getenv("MPMRB_SOLVER_CTAS");
   if (force) a.force_ctas = atoi(force);
+  const char* force_ls = getenv("MPMRB_SOLVER_LS_CTAS");
+  if (force_ls) a.force_ls_ctas = atoi(force_ls);
+  a.debug = getenv("MPMRB_SOLVER_DEBUG") ? 1 : 0;
   rc = launch_qn_solve(*c, a, 0);
   if (rc) return rc;
   SolveOut h{};
@@ -551,6 +576,8 @@ int mpmrb_sim_create(mpmrb_ctx* c, mpmrb_sim** out) {
   if (getenv("MPMRB_NO_GRAPH")) s->use_graph = false;
   const char* force = getenv("MPMRB_SOLVER_CTAS");
   if (force) s->force_ctas = atoi(force);
+  const char* force_ls = getenv("MPMRB_SOLVER_LS_CTAS");
+  if (force_ls) s->force_ls_ctas = atoi(force_ls);
   *out = s;
   return MPMRB_OK;
 }
@@ -558,22 +585,7 @@ int mpmrb_sim_create(mpmrb_ctx* c, mpmrb_sim** out) {
 int mpmrb_sim_destroy(mpmrb_sim* s) {
   if (!s) return MPMRB_OK;
   cudaStreamSynchronize(s->ctx->stream);
-  DevBuf* bufs[] = {&s->b_mats, &s->b_geoms, &s->b_counters, &s->b_misc, &s->b_solveout,
-                    &s->b_bar, &s->b_partials, &s->b_dyn, &s->b_accum, &s->b_probe_hk,
-                    &s->b_probe_hv, &s->b_probe_uk, &s->b_probe_bk, &s->b_plankeys, &s->b_stats,
-                    &s->b_hkeys, &s->b_hvals, &s->b_ukeys, &s->b_bkeys, &s->b_mass, &s->b_mom,
-                    &s->b_vk, &s->b_vstar, &s->b_vnext, &s->b_active, &s->b_wcount, &s->b_woff,
-                    &s->b_act, &s->b_remap, &s->b_mc, &s->b_vstarc, &s->b_vkc, &s->b_cnt,
-                    &s->b_offs, &s->b_cpart, &s->b_cbody, &s->b_cphi, &s->b_cmu, &s->b_cgl,
-                    &s->b_cnormal, &s->b_cwit, &s->b_cbias, &s->b_cframes, &s->b_cnodes,
-                    &s->b_cw, &s->b_sv, &s->b_sgw, &s->b_srgr, &s->b_adjcnt, &s->b_adjfill,
-                    &s->b_adjoff, &s->b_adjent, &s->b_adjw, &s->b_adjflag,
-                    &s->b_adjflagoff, &s->b_adjcn, &s->b_adjfn, &s->b_adjcne, &s->b_adjh,
-                    &s->b_sdv,
-                    &s->b_svc,
-                    &s->b_sdvc, &s->b_gamma, &s->b_gworld, &s->b_tiles, &s->b_bias_stamp,
-                    &s->b_bias_store};
-  for (DevBuf* b : bufs) b->release();
+  // every DevBuf member frees itself (DevBuf::~DevBuf)
   delete s;
   return MPMRB_OK;
 }
@@ -685,7 +697,15 @@ int mpmrb_sim_last_contacts(mpmrb_sim* s, int64_t* n, const int32_t** particle,
   MPMRB_CUDA_OK(cudaStreamSynchronize(s->ctx->stream));
   MPMRB_CUDA_OK(cudaMemcpy(hc, s->b_counters.p, sizeof(hc), cudaMemcpyDeviceToHost));
   *n = hc[2];
-  *particle = (const int32_t*)s->b_cpart.p;
+  // contacts index the sim-internal (sorted) particles: map to the user's ids
+  long long cap = s->nc_cap;
+  if (hc[2] > 0) {
+    int rc = launch_map_ids(*s->ctx, s->b_cpart.as<int>(), s->b_perm.as<int>(),
+                            s->b_counters.as<int>() + 2, cap, s->b_cpart_user.as<int>());
+    if (rc) return rc;
+    MPMRB_CUDA_OK(cudaStreamSynchronize(s->ctx->stream));
+  }
+  *particle = (const int32_t*)s->b_cpart_user.p;
   *gamma_world = (const double*)s->b_gworld.p;
   return MPMRB_OK;
 }

@@ -21,6 +21,10 @@ int set_cuda_error(cudaError_t e, const char* expr, const char* file, int line);
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
   int grow(size_t need);  // returns MPMRB_OK or MPMRB_E_CUDA
   void release();
   template <class T>
@@ -112,6 +116,18 @@ int launch_g2p(Ctx& c, const GridDev& g, const ParticlesDev& p, const mpmrb_mate
 
 int launch_clamp(Ctx& c, const double* f, long long n, double* out, unsigned long long* nbad);
 int launch_health(Ctx& c, const double* x, const double* v, long long n, double h, int* bad);
+
+// reorder.cu: once-per-step (block, cell) particle order
+int launch_particle_sort(Ctx& c, const double* x, long long n, double h,
+                         const unsigned long long* hkeys, const int* hvals, long long hash_cap,
+                         long long n_blocks_cap, unsigned* keys2, int* vals2, int* perm_out);
+int launch_particle_gather(Ctx& c, const int* perm, long long n, const double* src, int width,
+                           double* dst);
+int launch_particle_scatter(Ctx& c, const int* perm, long long n, const double* src, int width,
+                            double* dst);
+int launch_gather_i64(Ctx& c, const int* perm, long long n, const long long* src, long long* dst);
+int launch_map_ids(Ctx& c, const int* ids, const int* perm, const int* n_dev, long long cap,
+                   int* out);
 
 // contact.cu
 int launch_contact_model(Ctx& c, const double* vc, const double* phi, const double* gl,

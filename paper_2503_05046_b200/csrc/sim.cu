@@ -80,9 +80,10 @@ __global__ void k_contact_prepare(GridDev g, const double* __restrict__ x,
         int node = stencil_node(s, sb, ox, oy, oz);
 #pragma unroll
         for (int d = 0; d < 3; ++d) vp[d] += w * v_k[3 * node + d];
-        int r = remap[node];
-        cnodes[(long long)k * nc_cap + c] = r < 0 ? 0 : r;
-        cw[(long long)k * nc_cap + c] = r < 0 ? 0.0 : w;
+        const int r = remap[node];
+        const bool dead = r < 0 || w == 0.0;  // dead slot: w = 0, no node (solver.py:207-213)
+        cnodes[(long long)k * nc_cap + c] = dead ? -1 : r;
+        cw[(long long)k * nc_cap + c] = dead ? 0.0 : w;
       }
   const double* R = frames + 9 * c;
   double vn = (R[6] * vp[0] + R[7] * vp[1] + R[8] * vp[2]) + bias[3 * c + 2];
@@ -206,6 +207,26 @@ int Sim::reserve(long long n, long long nb_needed) {
   }
   n_particles = n;
   int rc = 0;
+  {
+    const long long nn = n > 0 ? n : 1;
+    rc |= b_qd.grow(8 * 27 * nn);
+    rc |= b_qmid.grow(8 * nn);
+    rc |= b_perm.grow(4 * nn);
+    rc |= b_skeys.grow(4 * 2 * nn);
+    rc |= b_svals.grow(4 * 2 * nn);
+    rc |= b_cpart_user.grow(4 * (long long)(ngeom > 0 ? ngeom : 1) * nn);
+    if (rc) return MPMRB_E_CUDA;
+    double* d = b_qd.as<double>();
+    q.x = d;
+    q.v = d + 3 * nn;
+    q.f = d + 6 * nn;
+    q.c = d + 15 * nn;
+    q.mass = d + 24 * nn;
+    q.vol0 = d + 25 * nn;
+    q.plastic = d + 26 * nn;
+    q.mid = b_qmid.as<long long>();
+    q.n = n;
+  }
   rc |= b_hkeys.grow(8 * hash_cap);
   rc |= b_hvals.grow(4 * hash_cap);
   rc |= b_ukeys.grow(8 * nb_cap);
@@ -240,19 +261,10 @@ int Sim::reserve(long long n, long long nb_needed) {
   rc |= b_sdv.grow(8 * 3 * N);
   rc |= b_svc.grow(8 * 5 * nc_cap);  // vc (3), vhat, mu*gamma_lag
   rc |= b_sdvc.grow(8 * 3 * nc_cap);
-  rc |= b_sgw.grow(8 * 3 * nc_cap);
-  rc |= b_srgr.grow(8 * 6 * nc_cap);
-  rc |= b_adjcnt.grow(4 * (N + 1));
-  rc |= b_adjfill.grow(4 * (N + 1));
-  rc |= b_adjoff.grow(4 * (N + 1));
-  rc |= b_adjent.grow(2 * 4 * 27 * nc_cap);
-  rc |= b_adjw.grow(8 * 27 * nc_cap);
-  rc |= b_adjflag.grow(4 * (N + 1));
-  rc |= b_adjflagoff.grow(4 * (N + 1));
-  rc |= b_adjcn.grow(4 * (N + 1));
-  rc |= b_adjfn.grow(4 * (N + 1));
-  rc |= b_adjcne.grow(4 * 2 * (N + 1));
-  rc |= b_adjh.grow(4 * 5 * (N + 2));  // hflag, hflag_off, hn, hn_e (2)
+  rc |= b_su_c.grow(4 * 4 * (nc_cap + 2));  // head, head_off, grp_of, grp_start
+  rc |= b_su_n.grow(4 * 12 * (N + 2) + 64);  // cnt, fill, off, flag, flag_off, cn, fn, counts, cn_rec
+  rc |= b_su_ent.grow(2 * 4 * 27 * nc_cap);
+  rc |= b_cellsum.grow(8 * kCellSumStride * 27 * nc_cap);
   rc |= b_gamma.grow(8 * 3 * nc_cap);
   rc |= b_gworld.grow(8 * 3 * nc_cap);
   long long scan_n = (N + 1) > (n + 1) ? (N + 1) : (n + 1);
@@ -269,7 +281,7 @@ int Sim::capture_or_launch() {
   int rc;
   mark(0);
   // 1. grid (grid.py:71-103)
-  rc = launch_grid_build(c, p.x, n_particles, h, b_bkeys.as<long long>(), nb_cap,
+  rc = launch_grid_build(c, q.x, n_particles, h, b_bkeys.as<long long>(), nb_cap,
                          b_hkeys.as<unsigned long long>(), b_hvals.as<int>(), hash_cap,
                          b_ukeys.as<long long>(), counters + 0);
   if (rc) return rc;
@@ -279,7 +291,7 @@ int Sim::capture_or_launch() {
   MPMRB_CUDA_OK(cudaMemsetAsync(b_mom.p, 0, 8 * 6 * N, c.stream));
   double* mom_apic = b_mom.as<double>();
   double* mom_force = mom_apic + 3 * N;
-  rc = launch_p2g(c, g, p, b_mats.as<mpmrb_material>(), nmat, dt_s, b_mass.as<double>(), mom_apic,
+  rc = launch_p2g(c, g, q, b_mats.as<mpmrb_material>(), nmat, dt_s, b_mass.as<double>(), mom_apic,
                   mom_force);
   if (rc) return rc;
   mark(2);
@@ -308,12 +320,12 @@ int Sim::capture_or_launch() {
   ca.frames = b_cframes.as<double>();
   ca.bias = b_cbias.as<double>();
   ca.mu = b_cmu.as<double>();
-  rc = launch_detect(c, p.x, n_particles, b_geoms.as<mpmrb_geom>(), ngeom, margin,
+  rc = launch_detect(c, q.x, n_particles, b_geoms.as<mpmrb_geom>(), ngeom, margin,
                      b_cnt.as<int>(), b_offs.as<int>(), counters + 2, b_tiles, nc_cap,
                      b_bias_stamp.as<int>(), b_bias_store.as<double>(), b_dyn.as<int>(), ca);
   if (rc) return rc;
   k_contact_prepare<<<grid_for(nc_cap, 128), 128, 0, c.stream>>>(
-      g, p.x, counters + 2, nc_cap, ca.particle, ca.frames, ca.bias, ca.phi, b_vk.as<double>(),
+      g, q.x, counters + 2, nc_cap, ca.particle, ca.frames, ca.bias, ca.phi, b_vk.as<double>(),
       b_remap.as<int>(), K, den, b_cnodes.as<int>(), b_cw.as<double>(), b_cgl.as<double>(),
       c.status);
   c.launches++;
@@ -321,33 +333,35 @@ int Sim::capture_or_launch() {
   // 5. quasi-Newton solve on the device (solver.py:328-382)
   k_reset_solveout<<<1, 32, 0, c.stream>>>(b_solveout.as<SolveOut>());
   c.launches++;
-  SolverAdjacency adj{};
-  adj.cnt = b_adjcnt.as<int>();
-  adj.fill = b_adjfill.as<int>();
-  adj.off = b_adjoff.as<int>();
-  adj.ent = b_adjent.as<int>();
-  adj.ent_tmp = b_adjent.as<int>() + 27 * nc_cap;
-  adj.w = b_adjw.as<double>();
-  adj.flag = b_adjflag.as<int>();
-  adj.flag_off = b_adjflagoff.as<int>();
-  adj.cn = b_adjcn.as<int>();
-  adj.fn = b_adjfn.as<int>();
-  adj.cn_e = b_adjcne.as<int>();
-  adj.hflag = b_adjh.as<int>();
-  adj.hflag_off = b_adjh.as<int>() + (N + 2);
-  adj.hn = b_adjh.as<int>() + 2 * (N + 2);
-  adj.hn_e = b_adjh.as<int>() + 3 * (N + 2);
-  adj.n_hn = counters + 6;
-  adj.n_cn = counters + 5;
-  rc = launch_solver_adjacency(c, counters + 1, counters + 2, N, nc_cap, b_cnodes.as<int>(),
-                               b_cw.as<double>(), adj, b_tiles);
+  SolverSetup su{};
+  {
+    int* ci = b_su_c.as<int>();
+    su.head = ci;
+    su.head_off = ci + (nc_cap + 2);
+    su.grp_of = ci + 2 * (nc_cap + 2);
+    su.grp_start = ci + 3 * (nc_cap + 2);
+    int* ni = b_su_n.as<int>();
+    su.cnt = ni;
+    su.fill = ni + (N + 2);
+    su.off = ni + 2 * (N + 2);
+    su.flag = ni + 3 * (N + 2);
+    su.flag_off = ni + 4 * (N + 2);
+    su.cn = ni + 5 * (N + 2);
+    su.fn = ni + 6 * (N + 2);
+    su.counts = ni + 7 * (N + 2);
+    su.cn_rec = reinterpret_cast<int4*>(ni + 8 * (N + 2));
+    su.ent = b_su_ent.as<int>();
+    su.ent_tmp = su.ent + 27 * nc_cap;
+  }
+  rc = launch_solver_setup(c, counters + 1, counters + 2, N, nc_cap, b_cnodes.as<int>(), su,
+                           b_tiles);
   if (rc) return rc;
   SolverArgs a{};
   a.nd_dev = counters + 1;
   a.nc_dev = counters + 2;
   a.nc_cap = nc_cap;
   a.nd_cap = N;
-  a.adj = adj;
+  a.su = su;
   a.prof = c.solver_prof;
   a.m = b_mc.as<double>();
   a.v_star = b_vstarc.as<double>();
@@ -369,16 +383,18 @@ int Sim::capture_or_launch() {
   a.ls_max = sp.ls_max_iters;
   a.skip_if_no_contacts = 1;
   a.force_ctas = force_ctas;
+  a.force_ls_ctas = force_ls_ctas;
+  a.debug = getenv("MPMRB_SOLVER_DEBUG") ? 1 : 0;
   a.v = b_sv.as<double>();
   a.dv = b_sdv.as<double>();
   a.vc = b_svc.as<double>();
   a.cvhat = b_svc.as<double>() + 3 * nc_cap;
   a.cmug = b_svc.as<double>() + 4 * nc_cap;
   a.dvc = b_sdvc.as<double>();
-  a.gw = b_sgw.as<double>();
-  a.rgr = b_srgr.as<double>();
   a.partials = b_partials.as<double>();
-  a.ls_out = b_partials.as<double>() + 2 * 8 * kMaxSolverCtas;
+  a.cellsum = b_cellsum.as<double>();
+  a.slots = b_slots.as<unsigned long long>();
+  a.chan = reinterpret_cast<unsigned*>(b_slots.as<char>() + 8 * kSolverSlotWords);
   a.gamma = b_gamma.as<double>();
   a.out = b_solveout.as<SolveOut>();
   a.act = b_act.as<int>();
@@ -393,7 +409,7 @@ int Sim::capture_or_launch() {
   c.launches++;
   mark(6);
   // 6. G2P (mpm.py:118-138)
-  rc = launch_g2p(c, g, p, b_mats.as<mpmrb_material>(), nmat, b_vnext.as<double>(), dt_s,
+  rc = launch_g2p(c, g, q, b_mats.as<mpmrb_material>(), nmat, b_vnext.as<double>(), dt_s,
                   b_misc.as<unsigned long long>(), b_misc.as<int>() + 2);
   if (rc) return rc;
   mark(7);
@@ -437,15 +453,28 @@ int Sim::begin_step(long long epoch, int n_substeps) {
   // size the grid for the current positions (one host sync per step)
   if (b_counters.grow(64) || b_misc.grow(64) || b_solveout.grow(sizeof(SolveOut)) ||
       b_bar.grow(4096) || b_partials.grow(sizeof(double) * (2 * 8 * kMaxSolverCtas + 8)) ||
-      b_dyn.grow(64) || b_accum.grow(sizeof(double) * 6 * kMaxBodies))
+      b_dyn.grow(64) || b_accum.grow(sizeof(double) * 6 * kMaxBodies) ||
+      b_slots.grow(8 * kSolverSlotWords + 64))
     return MPMRB_E_CUDA;
+  if (!slots_init) {
+    // slot tags start at 0 and channel tags at 1, so no stale slot matches
+    MPMRB_CUDA_OK(cudaMemsetAsync(b_slots.p, 0, 8 * kSolverSlotWords, c.stream));
+    unsigned ch[4] = {1u, 1u, 1u, 1u};
+    MPMRB_CUDA_OK(cudaMemcpyAsync(b_slots.as<char>() + 8 * kSolverSlotWords, ch, sizeof(ch),
+                                  cudaMemcpyHostToDevice, c.stream));
+    MPMRB_CUDA_OK(cudaStreamSynchronize(c.stream));
+    slots_init = true;
+  }
   if (!bar_init) {
     MPMRB_CUDA_OK(cudaMemsetAsync(b_bar.p, 0, 64, c.stream));
     bar_init = true;
   }
   long long nb_probe_cap = nb_cap > 0 ? nb_cap : 1024;
+  long long probe_hcap = 0;
+  int nb_probe = 0;
   for (int attempt = 0; attempt < 8; ++attempt) {
     long long hcap = next_pow2(4 * nb_probe_cap);
+    probe_hcap = hcap;
     if (b_probe_hk.grow(8 * hcap) || b_probe_hv.grow(4 * hcap) || b_probe_uk.grow(8 * nb_probe_cap) ||
         b_probe_bk.grow(8 * nb_probe_cap))
       return MPMRB_E_CUDA;
@@ -475,7 +504,30 @@ int Sim::begin_step(long long epoch, int n_substeps) {
     if (st) return st;
     int rc2 = reserve(p.n, nb_host);
     if (rc2) return rc2;
+    nb_probe = nb_host;
     break;
+  }
+  // sim-internal particle order for this step: sorted by (block, cell) of the
+  // step-start positions, gathered from the user's arrays (scattered back in
+  // end_step)
+  if (p.n > 0) {
+    int rc = launch_particle_sort(c, p.x, p.n, h, b_probe_hk.as<unsigned long long>(),
+                                  b_probe_hv.as<int>(), probe_hcap, nb_probe > 0 ? nb_probe : 1,
+                                  b_skeys.as<unsigned>(), b_svals.as<int>(), b_perm.as<int>());
+    if (rc) return rc;
+    const int* perm = b_perm.as<int>();
+    rc = launch_particle_gather(c, perm, p.n, p.x, 3, q.x);
+    if (!rc) rc = launch_particle_gather(c, perm, p.n, p.v, 3, q.v);
+    if (!rc) rc = launch_particle_gather(c, perm, p.n, p.f, 9, q.f);
+    if (!rc) rc = launch_particle_gather(c, perm, p.n, p.c, 9, q.c);
+    if (!rc) rc = launch_particle_gather(c, perm, p.n, p.mass, 1, const_cast<double*>(q.mass));
+    if (!rc) rc = launch_particle_gather(c, perm, p.n, p.vol0, 1, const_cast<double*>(q.vol0));
+    if (!rc) rc = launch_gather_i64(c, perm, p.n, p.mid, const_cast<long long*>(q.mid));
+    if (!rc) {
+      if (p.plastic) rc = launch_particle_gather(c, perm, p.n, p.plastic, 1, q.plastic);
+      else MPMRB_CUDA_OK(cudaMemsetAsync(q.plastic, 0, 8 * p.n, c.stream));
+    }
+    if (rc) return rc;
   }
   if (max_substeps < n_substeps || !b_stats.p) {
     max_substeps = n_substeps > max_substeps ? n_substeps : max_substeps;
@@ -556,6 +608,16 @@ int Sim::end_step(mpmrb_step_stats* out, double* impulses_host) {
   MPMRB_CUDA_OK(cudaMemcpyAsync(acc, b_accum.p, sizeof(double) * 6 * kMaxBodies,
                                 cudaMemcpyDeviceToHost, c.stream));
   unsigned long long changed = 0;
+  if (p.n > 0) {
+    // internal order -> the user's arrays (reference order)
+    const int* perm = b_perm.as<int>();
+    int rc = launch_particle_scatter(c, perm, p.n, q.x, 3, p.x);
+    if (!rc) rc = launch_particle_scatter(c, perm, p.n, q.v, 3, p.v);
+    if (!rc) rc = launch_particle_scatter(c, perm, p.n, q.f, 9, p.f);
+    if (!rc) rc = launch_particle_scatter(c, perm, p.n, q.c, 9, p.c);
+    if (!rc && p.plastic) rc = launch_particle_scatter(c, perm, p.n, q.plastic, 1, p.plastic);
+    if (rc) return rc;
+  }
   if (p.n > 0) {
     int rc = launch_staleness(c, b_plankeys.as<uint16_t>(), p.x, p.n, h,
                               b_misc.as<unsigned long long>() + 4);

@@ -11,7 +11,8 @@ int launch_morton_only(Ctx& c, const double* x, long long n, double h, uint16_t*
 
 struct Sim {
   Ctx* ctx = nullptr;
-  ParticlesDev p{};
+  ParticlesDev p{};  // user arrays (reference order)
+  ParticlesDev q{};  // sim-internal copy sorted by (block, cell), used by the substeps
   bool have_particles = false;
   bool have_params = false;
   int nmat = 0;
@@ -21,6 +22,7 @@ struct Sim {
   double K = 0.0, den = 1.0, eps_v = 1e-4, margin = 0.0;
   mpmrb_solver_params sp{};
   int force_ctas = 0;
+  int force_ls_ctas = 0;
   long long nb_cap = 0, hash_cap = 0, nc_cap = 0, n_particles = -1;
   long long bias_n = -1;
   int bias_geoms = -1;
@@ -40,9 +42,12 @@ struct Sim {
   DevBuf b_mc, b_vstarc, b_vkc;
   DevBuf b_cnt, b_offs, b_cpart, b_cbody, b_cphi, b_cmu, b_cgl, b_cnormal, b_cwit, b_cbias,
       b_cframes, b_cnodes, b_cw;
-  DevBuf b_sv, b_sdv, b_svc, b_sdvc, b_sgw, b_srgr, b_gamma, b_gworld, b_tiles;
-  DevBuf b_adjcnt, b_adjfill, b_adjoff, b_adjent, b_adjw, b_adjflag, b_adjflagoff, b_adjcn,
-      b_adjfn, b_adjcne, b_adjh;
+  DevBuf b_sv, b_sdv, b_svc, b_sdvc, b_gamma, b_gworld, b_tiles;
+  // solver setup (groups + node adjacency), cellsum, reduction slots
+  DevBuf b_su_c, b_su_n, b_su_ent, b_cellsum, b_slots;
+  // sorted particle state: x, v (3n) f, c (9n) mass, vol0, plastic (n) doubles; mid (n) int64
+  DevBuf b_qd, b_qmid, b_perm, b_skeys, b_svals, b_cpart_user;
+  bool slots_init = false;
   DevBuf b_bias_stamp, b_bias_store;
 
   static constexpr int kProfEvents = 8;

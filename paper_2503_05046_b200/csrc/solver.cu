@@ -3,32 +3,40 @@
 // cooperative kernel: no host round trip per iteration or per line-search
 // evaluation.
 //
-// Layout.  The problem is restricted to active nodes (solver.py:197-221).
-// Per-contact stencils are slot-major [27][nc_cap].  A node->(contact, slot)
-// CSR adjacency (built once per solve, entries sorted) turns the J^T scatters
-// of the gradient and of the block-diagonal Hessian (solver.py:127-167) into
-// per-node gathers: no atomics and a fixed summation order, so a solve is
-// bitwise reproducible run to run.  Nodes with adjacency ("contact nodes",
-// typically a thin layer) are gathered by one warp each from a compacted
-// list; all other nodes take the cheap thread-per-node path.
+// Structure (v4).
+//  * Free nodes (active nodes no contact stencil touches) have g = m(v - v*),
+//    H = m I, so dv = -(v - v*) and v - v* shrinks by (1 - alpha) per step.
+//    Their whole contribution to every reduction is a closed form in
+//    P = prod(1 - alpha) and three sums taken once (S0, Q0, Q1 below); they
+//    are written once, in the epilogue, as v = v* + P (v0 - v*).  The
+//    iteration only touches contact nodes and contacts.
+//  * Contacts are grouped by identical stencils (all contacts of one grid cell
+//    share their 27 nodes).  The contact owners sum w R^T g_c and w^2 R^T G R
+//    per (group, slot) ("cellsum"); each contact node gathers its (group, slot)
+//    entries through a sorted CSR.  Fixed summation order, no atomics: a solve
+//    is bitwise reproducible run to run.
+//  * The exact line search (solver.py:266-298) runs on a small group of CTAs
+//    (sized to the contact count) whose all-reduces use fence-free
+//    self-validating slots (~1 us for 16 CTAs vs ~3 us for a 148-CTA grid
+//    sync, tools/reduce_bench.cu).  Each evaluation is closed form per contact:
+//    one rsqrt, no division.
 //
-// Phases per iteration (solver.py:338-357), each a grid-stride loop:
-//   N  nodes:    jt = J^T g_c, H_ii = m I + sum w^2 R^T G R (gathers), g,
-//                residual / norms / mass energy, 3x3 Cholesky -> dv, and the
-//                line-search coefficients a1, a2                    [reduce]
-//   D  contacts: dvc = R J dv, phi'(0) contact term                   [reduce]
-//   LS contacts: <= ls_max evaluations of phi'(a), phi''(a), contact
-//                data held in registers                        [reduce each]
-//   U  nodes v += a dv; contacts vc += a dvc, then g_c -> R^T g_c, G ->
-//      R^T G R and the contact energy for the next N               [grid sync]
-// Grid synchronisation is cooperative_groups::this_grid().sync() (measured
-// ~2 us per reduction on B200, flat in CTA count; tools/barrier_bench.cu).
-// Every CTA sums the per-CTA partials in the same fixed order, so all CTAs
-// take identical convergence and line-search decisions.
+// Phases per iteration (solver.py:338-357):
+//   N  contact nodes: pending v += alpha dv, gather cellsum -> J^T g and the
+//      Hessian block, gradient, residual/norms, 3x3 Cholesky -> dv, a1, a2;
+//      free-node terms in closed form                         [grid reduce]
+//   D  contacts: dvc = R J dv and phi'(0)            [gather to the LS group]
+//   LS group: <= ls_max evaluations                [group reduce each]
+//      -> alpha broadcast to every CTA
+//   U  contacts: vc += alpha dvc, contact gradient/Hessian -> cellsum
+//                                                             [grid sync]
 //
-// vc is advanced as vc + a dvc (= R J (v + a dv) + b exactly in real
+// vc is advanced as vc + alpha dvc (= R J (v + alpha dv) + b exactly in real
 // arithmetic) instead of being re-gathered from v; the difference is roundoff.
 #include <cooperative_groups.h>
+
+#include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "contact.cuh"
@@ -42,8 +50,15 @@ namespace mpmrb {
 namespace {
 
 constexpr int kThreads = kSolverThreads;
-constexpr int kMaxRed = 8;  // reduction lanes per call
-constexpr int kJR = 2;      // contacts per thread cached in registers
+constexpr int kChunk = 32;        // contacts per ownership chunk: one warp, one contact per lane
+constexpr int kWarps = kThreads / 32;
+constexpr int kMaxRed = 8;        // reduction lanes per grid reduce
+constexpr int kLS = 6;            // contacts per line-search thread held in registers
+
+// slot areas (64-bit words), see kSolverSlotWords
+constexpr long long kSlotA = 0;                                  // [2][ctas][2]  gather (1 value)
+constexpr long long kSlotB = kSlotA + 2LL * kMaxSolverCtas * 2;  // [2][ctas][4]  group (2 values)
+constexpr long long kSlotC = kSlotB + 2LL * kMaxSolverCtas * 4;  // [2][4]        broadcast (2)
 
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
@@ -51,6 +66,74 @@ __device__ __forceinline__ unsigned long long gtime() {
   return t;
 }
 
+// ------------------------------------------------------------ self-validating slots
+// A double is published as two 64-bit words (tag << 32 | half).  64-bit
+// aligned stores are single-copy atomic, so a reader that sees the current
+// tag in both words has the complete, current value: no fence or flag
+// ordering is needed for the scalars themselves.  Tags advance by one per use
+// of a channel and persist across solves (SolverArgs::chan).
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+// release / acquire fences at GPU scope (lighter than __threadfence's fence.sc)
+__device__ __forceinline__ void fence_acq_rel_gpu() {
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+__device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+template <int K>
+__device__ __forceinline__ void slot_publish(unsigned long long* slot, const double* v,
+                                             unsigned tag) {
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v[k]);
+    const unsigned long long t = (unsigned long long)tag << 32;
+    st_relaxed(slot + 2 * k, t | (b >> 32));
+    st_relaxed(slot + 2 * k + 1, t | (b & 0xffffffffull));
+  }
+}
+
+// Warp-wide: wait for n slots (<= 32*PER) of K doubles carrying `tag`, and
+// sum them in slot order (lane-strided partials then a butterfly: the same
+// order in every CTA, so all CTAs get bitwise-identical sums).
+template <int K, int PER, int SLEEP_NS = 0>
+__device__ __forceinline__ void slot_poll_sum(const unsigned long long* slots, int n,
+                                              unsigned tag, double* out) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long w[PER][2 * K];
+  bool ok;
+  do {
+    ok = true;
+#pragma unroll
+    for (int r = 0; r < PER; ++r) {
+      const int s = lane + 32 * r;
+#pragma unroll
+      for (int j = 0; j < 2 * K; ++j) {
+        w[r][j] = (s < n) ? ld_relaxed(slots + (long long)s * 2 * K + j)
+                          : ((unsigned long long)tag << 32);
+        ok &= (unsigned)(w[r][j] >> 32) == tag;
+      }
+    }
+    if (SLEEP_NS > 0 && !__all_sync(0xffffffffu, ok)) __nanosleep(SLEEP_NS);
+  } while (!__all_sync(0xffffffffu, ok));
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    double acc = 0.0;
+#pragma unroll
+    for (int r = 0; r < PER; ++r)
+      acc += __longlong_as_double((long long)(((w[r][2 * k] & 0xffffffffull) << 32) |
+                                              (w[r][2 * k + 1] & 0xffffffffull)));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    out[k] = acc;
+  }
+}
+
+// ------------------------------------------------------------ grid reductions
 struct Sync {
   double* partials;  // [2][kMaxRed][kMaxSolverCtas]
   int nctas;
@@ -66,16 +149,11 @@ struct Sync {
   }
 };
 
-// Sum K values over all threads of all participating CTAs; every thread
-// receives the totals.  Partials are double-buffered: a CTA racing into the
-// next reduction writes the other half while slower CTAs still read this one,
-// and the grid sync inside the next reduction closes the window.
+// Block sum of K values into sm[32*kMaxRed + k] (valid after the call's
+// trailing barrier in every thread of the CTA).
 template <int K>
-__device__ void reduce_all(const Sync& sync, int& parity, double (&v)[K], double (&out)[K],
-                           double* sm) {
+__device__ __forceinline__ void block_reduce(double (&v)[K], double* sm, double* res) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  double* part = sync.partials + parity * (kMaxRed * kMaxSolverCtas);
-  parity ^= 1;
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     double x = v[k];
@@ -90,17 +168,34 @@ __device__ void reduce_all(const Sync& sync, int& parity, double (&v)[K], double
       double x = (lane < kThreads / 32) ? sm[k * 32 + lane] : 0.0;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-      if (lane == 0) {
-        if (sync.nctas == 1) sm[32 * kMaxRed + k] = x;
-        else part[k * kMaxSolverCtas + blockIdx.x] = x;
-      }
+      res[k] = x;  // every lane of warp 0 holds the block sum
+    }
+  }
+}
+
+// Sum K values over all threads of all participating CTAs through a grid
+// sync; every thread receives the totals.  Partials are double-buffered: a
+// CTA racing into the next reduction writes the other half while slower CTAs
+// still read this one, and the grid sync inside the next reduction closes the
+// window.  The sync also orders all prior global writes (data barrier).
+template <int K>
+__device__ void reduce_all(const Sync& sync, int& parity, double (&v)[K], double (&out)[K],
+                           double* sm) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* part = sync.partials + parity * (kMaxRed * kMaxSolverCtas);
+  parity ^= 1;
+  double bs[K];
+  block_reduce<K>(v, sm, bs);
+  if (wid == 0 && lane == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      if (sync.nctas == 1) sm[32 * kMaxRed + k] = bs[k];
+      else part[k * kMaxSolverCtas + blockIdx.x] = bs[k];
     }
   }
   if (sync.nctas > 1) {
     sync();
     if (wid == 0) {
-      // all K x ceil(nctas/32) loads issued before the first add: one L2
-      // round trip instead of one per 32 CTAs per value
       constexpr int kR = (kMaxSolverCtas + 31) / 32;
       double x[K][kR];
 #pragma unroll
@@ -127,25 +222,136 @@ __device__ void reduce_all(const Sync& sync, int& parity, double (&v)[K], double
   __syncthreads();
 }
 
+// All-reduce of K values over the line-search group (CTAs 0..G-1) through
+// channel B slots; G == 1 is a plain block reduction.
+template <int K>
+__device__ void group_reduce(int G, unsigned long long* slots, unsigned& tag, double (&v)[K],
+                             double (&out)[K], double* sm) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double bs[K];
+  block_reduce<K>(v, sm, bs);
+  if (wid == 0) {
+    if (G == 1) {
+      if (lane == 0)
+#pragma unroll
+        for (int k = 0; k < K; ++k) sm[32 * kMaxRed + k] = bs[k];
+    } else {
+      unsigned long long* base = slots + kSlotB + (long long)(tag & 1u) * kMaxSolverCtas * 4;
+      if (lane == 0) slot_publish<K>(base + (long long)blockIdx.x * 2 * K, bs, tag);
+      double r[K];
+      slot_poll_sum<K, 2>(base, G, tag, r);
+      if (lane == 0)
+#pragma unroll
+        for (int k = 0; k < K; ++k) sm[32 * kMaxRed + k] = r[k];
+    }
+  }
+  if (G > 1) ++tag;
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < K; ++k) out[k] = sm[32 * kMaxRed + k];
+  __syncthreads();
+}
+
+// All-reduce of K values over the line-search group when it is cluster 0:
+// every CTA writes its block sum into slot [parity][rank] of EVERY CTA's
+// shared memory (st.shared::cluster), one hardware cluster barrier, then each
+// CTA sums the CL slots locally in rank order (identical in every CTA).
+constexpr int kMaxCluster = 16;
+template <int K>
+__device__ void cluster_reduce(int CL, double (*s_cl)[kMaxCluster][2], int& cpar,
+                               double (&v)[K], double (&out)[K], double* sm) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double bs[K];
+  block_reduce<K>(v, sm, bs);
+  cg::cluster_group cl = cg::this_cluster();
+  const int me = (int)cl.block_rank();
+  if (wid == 0 && lane < CL) {
+    double* dst = cl.map_shared_rank(&s_cl[cpar][me][0], lane);
+#pragma unroll
+    for (int k = 0; k < K; ++k) dst[k] = bs[k];
+  }
+  cl.sync();
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    double x = 0.0;
+    for (int r = 0; r < CL; ++r) x += s_cl[cpar][r][k];
+    out[k] = x;
+  }
+  cpar ^= 1;
+}
+
 __device__ __forceinline__ void load_frame(const double* fr, long long c, double* R) {
 #pragma unroll
   for (int k = 0; k < 9; ++k) R[k] = __ldg(fr + 9 * c + k);
 }
 
-// R (sum_k w_k u[node_k])
-__device__ __forceinline__ void gather_contact(const SolverArgs& a, long long c,
-                                               const double* __restrict__ u, const double* R,
-                                               double* out) {
-  double up[3] = {0.0, 0.0, 0.0};
-#pragma unroll 9
-  for (int k = 0; k < 27; ++k) {
-    int nd = __ldg(&a.cnodes[(long long)k * a.nc_cap + c]);
-    double w = __ldg(&a.cw[(long long)k * a.nc_cap + c]);
+// R (sum_k w_k u[node_k]); dead slots (node < 0) carry w = 0 and add nothing.
+// All 27 node indices are loaded first and the value loads carry no branch,
+// so the whole gather costs two dependent memory round trips (a branch on each
+// loaded index serialised 27 of them).  Weights come from global memory
+// (slot-major) or, when staged, from shared memory sw[k * 32 + lane].
+// u is written by other CTAs earlier in this kernel (ordered by a grid sync,
+// which also invalidates L1): plain coherent loads, no __restrict__ (that would
+// allow the non-coherent path) and no volatile asm (__ldcg would pin the loads
+// in program order behind the FMAs that consume them).
+template <bool kStaged>
+__device__ __forceinline__ void gather_contact_t(const SolverArgs& a, long long c,
+                                                 const double* u, const double* R,
+                                                 const double* sw, int lane, double* out) {
+  int nd[27];
 #pragma unroll
-    for (int d = 0; d < 3; ++d) up[d] += w * (*(&u[3 * nd + d]));
+  for (int k = 0; k < 27; ++k) nd[k] = __ldg(&a.cnodes[(long long)k * a.nc_cap + c]);
+  double up[3] = {0.0, 0.0, 0.0};
+  // three batches of nine slots: 27 value loads in flight per batch (register
+  // budget), i.e. one index round trip + three value round trips in total
+#pragma unroll
+  for (int b = 0; b < 3; ++b) {
+    double x[9], y[9], z[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {
+      const int k = 9 * b + q;
+      const long long j = 3LL * (nd[k] >= 0 ? nd[k] : 0);
+      x[q] = u[j];
+      y[q] = u[j + 1];
+      z[q] = u[j + 2];
+    }
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {
+      const int k = 9 * b + q;
+      const double w = kStaged ? sw[k * 32 + lane] : __ldg(&a.cw[(long long)k * a.nc_cap + c]);
+      if (nd[k] >= 0) {
+        up[0] += w * x[q];
+        up[1] += w * y[q];
+        up[2] += w * z[q];
+      }
+    }
   }
 #pragma unroll
   for (int r = 0; r < 3; ++r) out[r] = R[3 * r] * up[0] + R[3 * r + 1] * up[1] + R[3 * r + 2] * up[2];
+}
+
+__device__ __forceinline__ void gather_contact(const SolverArgs& a, long long c, const double* u,
+                                               const double* R, double* out) {
+  gather_contact_t<false>(a, c, u, R, nullptr, 0, out);
+}
+__device__ __forceinline__ void gather_contact_sw(const SolverArgs& a, long long c,
+                                                  const double* u, const double* R,
+                                                  const double* sw, int lane, double* out) {
+  gather_contact_t<true>(a, c, u, R, sw, lane, out);
+}
+
+// Stage the 27 stencil weights of the warp's chunk [c0, c0 + 32) into
+// sw[k * 32 + lane] (slot-major loads, coalesced, all in flight at once).
+__device__ __forceinline__ void stage_weights(const SolverArgs& a, long long c0, int nc,
+                                              double* sw) {
+  const int lane = threadIdx.x & 31;
+  const long long c = c0 + lane;
+  double w[27];
+#pragma unroll
+  for (int k = 0; k < 27; ++k) w[k] = (c < nc) ? __ldg(&a.cw[(long long)k * a.nc_cap + c]) : 0.0;
+#pragma unroll
+  for (int k = 0; k < 27; ++k) sw[k * 32 + lane] = w[k];
+  __syncwarp();
 }
 
 // From vc: world gradient gw = R^T g_c, Hessian block R^T G R (6 entries used
@@ -157,7 +363,6 @@ __device__ __forceinline__ double contact_terms(const ContactModel& cm, const do
   const double energy = cm_eval(cm, vc, vhat, mug, g, G);
 #pragma unroll
   for (int j = 0; j < 3; ++j) gw[j] = g[0] * R[j] + g[1] * R[3 + j] + g[2] * R[6 + j];
-  // GR = G @ R with G = [[G0,G3,0],[G3,G1,0],[0,0,G2]]
   double GR[9];
 #pragma unroll
   for (int j = 0; j < 3; ++j) {
@@ -172,23 +377,77 @@ __device__ __forceinline__ double contact_terms(const ContactModel& cm, const do
   return energy;
 }
 
+// Line-search derivative terms of one contact at step alpha (solver.py:
+// 266-325 with contact_model.py:75-111 along the line): adds g_c.dvc to d1 and
+// dvc^T G_c dvc to d2.  Closed form: one rsqrt, no division.
+__device__ __forceinline__ void ls_terms(const ContactModel& cm, double inv_eps, const double* vc,
+                                         const double* dvc, double vhat, double mug,
+                                         double alpha, double& d1, double& d2) {
+  const double gap = vhat - (vc[2] + alpha * dvc[2]);
+  d1 -= (cm.K * fmax(0.0, gap)) * dvc[2];
+  if (gap >= 0.0) d2 += cm.K * (dvc[2] * dvc[2]);
+  const double t0 = vc[0] + alpha * dvc[0], t1 = vc[1] + alpha * dvc[1];
+  const double s2 = t0 * t0 + t1 * t1;
+  const double td = t0 * dvc[0] + t1 * dvc[1];
+  const double dd = dvc[0] * dvc[0] + dvc[1] * dvc[1];
+  if (s2 > cm.eps_v * cm.eps_v) {
+    const double r = rsqrt(s2);
+    const double av = mug * r;
+    d1 += av * td;
+    d2 += av * (dd - (r * r) * (td * td));
+  } else {
+    const double av = mug * inv_eps;
+    d1 += av * td;
+    d2 += av * dd;
+  }
+}
+
+// The same with the per-line-search constants of a contact precomputed
+// (LsRec): gap0 = vhat - vc_n, dvn, K dvn^2, |dvt|^2, mu gamma_lag.
+struct LsRec {
+  double t0, t1, d0, d1, gap0, dvn, kdvn2, dd, mug;
+};
+__device__ __forceinline__ LsRec ls_rec(const ContactModel& cm, const double* vc,
+                                        const double* dvc, double vhat, double mug) {
+  LsRec r;
+  r.t0 = vc[0];
+  r.t1 = vc[1];
+  r.d0 = dvc[0];
+  r.d1 = dvc[1];
+  r.gap0 = vhat - vc[2];
+  r.dvn = dvc[2];
+  r.kdvn2 = cm.K * (dvc[2] * dvc[2]);
+  r.dd = dvc[0] * dvc[0] + dvc[1] * dvc[1];
+  r.mug = mug;
+  return r;
+}
+__device__ __forceinline__ void ls_terms_rec(const ContactModel& cm, double eps2, double inv_eps,
+                                             const LsRec& c, double alpha, double& d1,
+                                             double& d2) {
+  const double gap = c.gap0 - alpha * c.dvn;
+  if (gap > 0.0) d1 -= (cm.K * gap) * c.dvn;
+  if (gap >= 0.0) d2 += c.kdvn2;
+  const double t0 = c.t0 + alpha * c.d0, t1 = c.t1 + alpha * c.d1;
+  const double s2 = t0 * t0 + t1 * t1;
+  const double td = t0 * c.d0 + t1 * c.d1;
+  if (s2 > eps2) {
+    const double r = rsqrt(s2);
+    const double av = c.mug * r;
+    d1 += av * td;
+    d2 += av * (c.dd - (r * r) * (td * td));
+  } else {
+    const double av = c.mug * inv_eps;
+    d1 += av * td;
+    d2 += av * c.dd;
+  }
+}
+
 // Per-node part of phase N given the gathered jt (3) and Hessian sums hs (6):
 // gradient, residual/norm/energy partials, regularised 3x3 Cholesky
 // (solver.py:224-256), direction dv and the line-search coefficients.
 struct NodeIn {
   double m, v[3], vs[3];
 };
-
-__device__ __forceinline__ NodeIn load_node(const SolverArgs& a, long long i) {
-  NodeIn n;
-  n.m = a.m[i];
-#pragma unroll
-  for (int d = 0; d < 3; ++d) {
-    n.v[d] = (*(&a.v[3 * i + d]));
-    n.vs[d] = a.v_star[3 * i + d];
-  }
-  return n;
-}
 
 __device__ __forceinline__ void node_finish(const SolverArgs& a, long long i, const NodeIn& nin,
                                             const double* jt, const double* hs, double* red,
@@ -243,68 +502,75 @@ __device__ __forceinline__ void node_finish(const SolverArgs& a, long long i, co
   }
 }
 
-// Contact group: the CTAs that own the contacts.  With a cluster launch it is
-// cluster 0 (DSMEM reductions + hardware cluster barrier, ~0.7 us); without
-// clusters it is the whole grid (grid reductions, ~1.7 us).
-struct Group {
-  bool member;     // this CTA owns contacts
-  int rank;        // rank within the group
-  int size;        // CTAs in the group
-  bool cluster;    // reductions go through the cluster
-};
-
-// Sum K values over the contact group (members only).  Cluster path: each CTA
-// publishes its block sum in its own shared slot, cluster barrier, then every
-// CTA reads the size partials over DSMEM in rank order.  Slots are
-// double-buffered by parity (same argument as reduce_all).
-template <int K>
-__device__ void group_reduce(const Group& gr, const Sync& sync, int& parity, int& cparity,
-                             double (&v)[K], double (&out)[K], double* sm,
-                             double (*cslot)[kMaxRed]) {
-  if (!gr.cluster) {
-    reduce_all<K>(sync, parity, v, out, sm);
-    return;
-  }
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+// Phase U (and the init) on one warp chunk of contacts [c0, c0 + 32): new
+// contact velocity, contact gradient / Hessian / energy, then the per
+// (group, slot) sums (groups never cross a chunk).  Warp-synchronous; s_gw is
+// this warp's 32 x 9 scratch.
+__device__ __forceinline__ void contact_update_chunk(const SolverArgs& a, const ContactModel& cm,
+                                                     long long c0, int nc, bool init,
+                                                     double alpha, double* s_gw,
+                                                     const double* s_w, double& e_acc) {
+  const int lane = threadIdx.x & 31;
+  const long long c = c0 + lane;
+  if (c < nc) {
+    double R[9], vc[3], gw[3], rgr[6], vhat, mug;
+    load_frame(a.frames, c, R);
+    if (init) {
+      gather_contact_sw(a, c, a.v0, R, s_w, lane, vc);
 #pragma unroll
-  for (int k = 0; k < K; ++k) {
-    double x = v[k];
+      for (int d = 0; d < 3; ++d) vc[d] += a.bias[3 * c + d];
+      vhat = -a.phi[c] / cm.den;
+      mug = a.mu[c] * a.gamma_lag[c];
+      a.cvhat[c] = vhat;
+      a.cmug[c] = mug;
+    } else {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-    if (lane == 0) sm[k * 32 + wid] = x;
-  }
-  __syncthreads();
-  const int par = cparity;
-  cparity ^= 1;
-  if (wid == 0) {
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      double x = (lane < kThreads / 32) ? sm[k * 32 + lane] : 0.0;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-      if (lane == 0) cslot[par][k] = x;
+      for (int d = 0; d < 3; ++d) vc[d] = a.vc[3 * c + d] + alpha * a.dvc[3 * c + d];
+      vhat = a.cvhat[c];
+      mug = a.cmug[c];
     }
+#pragma unroll
+    for (int d = 0; d < 3; ++d) a.vc[3 * c + d] = vc[d];
+    e_acc += contact_terms(cm, vc, vhat, mug, R, gw, rgr);
+    double* sg = s_gw + 9 * lane;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) sg[d] = gw[d];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) sg[3 + q] = rgr[q];
   }
-  cg::this_cluster().sync();
-  if (wid == 0) {
+  __syncwarp();
+  const long long c_last = (c0 + kChunk < nc ? c0 + kChunk : nc) - 1;
+  const int g0 = a.su.grp_of[c0], g1 = a.su.grp_of[c_last];
+  const int pairs = (g1 - g0 + 1) * 27;
+  for (int p = lane; p < pairs; p += 32) {
+    const int g = g0 + p / 27, k = p - (p / 27) * 27;
+    const int cs = a.su.grp_start[g], ce = a.su.grp_start[g + 1];
+    double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    for (int cc = cs; cc < ce; ++cc) {
+      const double w = s_w[k * 32 + (cc - c0)];
+      const double w2 = w * w;
+      const double* sg = s_gw + 9 * (cc - c0);
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      double x = 0.0;
-      if (lane < gr.size) x = *cg::this_cluster().map_shared_rank(&cslot[par][k], lane);
+      for (int d = 0; d < 3; ++d) acc[d] += w * sg[d];
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-      if (lane == 0) sm[32 * kMaxRed + k] = x;
+      for (int q = 3; q < 9; ++q) acc[q] += w2 * sg[q];
     }
+    double2* out = reinterpret_cast<double2*>(a.cellsum + ((long long)g * 27 + k) * kCellSumStride);
+    out[0] = make_double2(acc[0], acc[1]);
+    out[1] = make_double2(acc[2], acc[3]);
+    out[2] = make_double2(acc[4], acc[5]);
+    out[3] = make_double2(acc[6], acc[7]);
+    out[4] = make_double2(acc[8], 0.0);
   }
-  __syncthreads();
-#pragma unroll
-  for (int k = 0; k < K; ++k) out[k] = sm[32 * kMaxRed + k];
-  __syncthreads();
+  __syncwarp();
 }
 
 __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
   __shared__ double sm[32 * kMaxRed + kMaxRed];
-  __shared__ double cslot[2][kMaxRed];
+  __shared__ double s_gw[kWarps * kChunk * 9];
+  extern __shared__ double s_dyn[];  // [kWarps][27][32] staged stencil weights
+  __shared__ double s_bc[4];
+  __shared__ double s_cl[2][kMaxCluster][2];
   __shared__ int s_flag;
   const int nd = *a.nd_dev;
   const int nc = *a.nc_dev;
@@ -325,24 +591,41 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
   if (a.force_ctas == 0 && nc <= 1024 && nd <= 8192) nctas = 1;
   if (a.force_ctas == 1) nctas = 1;
   if (nctas == 1 && blockIdx.x != 0) return;
+  // line-search group: ~3 contacts per thread, at least one CTA
+  int G = 1;
+  const int CL = (nctas > 1) ? (int)cg::this_cluster().num_blocks() : 1;
+  int cpar = 0;
+  if (nctas > 1 && CL > 1) {
+    G = CL;  // the line-search group is cluster 0 (DSMEM reductions)
+  } else if (nctas > 1) {
+    G = (a.force_ls_ctas > 0) ? a.force_ls_ctas : (nc + kThreads * kLS - 1) / (kThreads * kLS);
+    if (G < 1) G = 1;
+    if (G > nctas) G = nctas;
+    if (G > 64) G = 64;  // slot_poll_sum<.., 2> polls at most 64 slots
+  }
+  const bool in_group = (int)blockIdx.x < G;
+  const int ng = a.su.counts[0];
+  const int n_cn = a.su.counts[1];
+  const int n_fn = nd - n_cn;
+  (void)ng;
+  unsigned tagA = a.chan[0], tagB = a.chan[1], tagC = a.chan[2];
   Sync sync{a.partials, nctas,
             (a.prof && blockIdx.x == 0 && threadIdx.x == 0) ? a.prof : nullptr};
-  const int csize = (nctas > 1) ? (int)cg::this_cluster().num_blocks() : 1;
-  Group gr;
-  if (nctas == 1) {
-    gr = Group{true, 0, 1, false};
-  } else if (csize > 1) {
-    gr = Group{(int)blockIdx.x < csize, (int)blockIdx.x, csize, true};
-  } else {
-    gr = Group{true, (int)blockIdx.x, nctas, false};
-  }
-  int parity = 0, cparity = 0;
+  int parity = 0;
   const long long tid = (long long)blockIdx.x * kThreads + threadIdx.x;
   const long long nthr = (long long)nctas * kThreads;
-  const int lane = threadIdx.x & 31;
-  const long long gwarp = tid >> 5, nwarps = nthr >> 5;
   const ContactModel cm{a.K, a.den, a.eps_v};
+  const double inv_eps = 1.0 / a.eps_v;
   const bool prof = a.prof && blockIdx.x == 0 && threadIdx.x == 0;
+  const bool cprof = a.prof && threadIdx.x == 0;  // per-CTA phase work times
+  unsigned long long cta_t0 = 0, cta_acc[3] = {0, 0, 0};
+  auto cta_start = [&]() {
+    if (cprof) cta_t0 = gtime();
+  };
+  auto cta_stop = [&](int ph) {
+    __syncthreads();
+    if (cprof) cta_acc[ph] += gtime() - cta_t0;
+  };
   unsigned long long pt[kSolverProf] = {0};
   unsigned long long tmark = prof ? gtime() : 0ull;
   auto lap = [&](int slot) {
@@ -353,150 +636,124 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
     }
   };
   double* v = a.v;
-  const int n_cn = *a.adj.n_cn;
-  const int n_hn = *a.adj.n_hn;
-  const int n_fn = nd - n_cn - n_hn;
+  // Work is interleaved across CTAs at warp granularity so that small node /
+  // contact counts still spread over every SM: virtual thread id vt puts 32
+  // consecutive items on one warp and consecutive warps on consecutive CTAs.
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long vt = ((long long)wid * nctas + blockIdx.x) * 32 + lane;
+  const long long chunk0 = ((long long)wid * nctas + blockIdx.x) * kChunk;
+  const long long chunk_step = (long long)nctas * kThreads;
+  double* s_gw_w = s_gw + wid * (kChunk * 9);
+  double* s_w_w = s_dyn + wid * (27 * kChunk);
+  // every warp owns at most one chunk: its weights stay staged for the solve
+  const bool resident = (long long)nc <= (long long)nctas * kThreads;
 
-  // Contacts are owned by the contact group, interleaved at warp granularity
-  // across its CTAs (each warp's 32 contacts consecutive -> coalesced
-  // slot-major loads).  A thread's first kJR contacts live in registers
-  // (fully unrolled j, never spilled); further ones go through memory.
-  const long long cthr = (long long)gr.size * kThreads;
-  const long long ctid =
-      ((long long)(threadIdx.x >> 5) * gr.size + gr.rank) * 32 + (threadIdx.x & 31);
-#define FOR_OWNED_CONTACTS(...)                                         \
-  if (gr.member) {                                                      \
-    _Pragma("unroll") for (int j = 0; j < kJR; ++j) {                  \
-      const long long c = ctid + (long long)j * cthr;                  \
-      constexpr bool inreg = true;                                      \
-      if (c < nc) { __VA_ARGS__ }                                       \
-    }                                                                   \
-    for (long long c = ctid + (long long)kJR * cthr; c < nc; c += cthr) { \
-      constexpr int j = 0;                                              \
-      constexpr bool inreg = false;                                     \
-      __VA_ARGS__                                                       \
-    }                                                                   \
-  }
-
-  // ---- init: v = v0; per contact vc = R J v0 + b, the per-solve constants
-  // vhat = -phi/(dt+tau_d) and mu*gamma_lag, and the contact terms
-  for (long long i = tid; i < nd; i += nthr) {
+  // ---- init: contact nodes v = v0; free-node sums; contacts
+  for (long long t = vt; t < n_cn; t += nthr) {
+    const long long i = a.su.cn[t];
 #pragma unroll
     for (int d = 0; d < 3; ++d) v[3 * i + d] = a.v0[3 * i + d];
   }
-  double vcr[kJR][3], dvcr[kJR][3];
-  double e_acc = 0.0;
-  FOR_OWNED_CONTACTS({
-    double R[9], vc[3], gw[3], rgr[6];
-    load_frame(a.frames, c, R);
-    gather_contact(a, c, a.v0, R, vc);
+  double S0 = 0.0, Q0 = 0.0, Q1 = 0.0;
+  double e_acc = 0.0;  // this thread's contact energy at the current vc
+  {
+    double r3[3] = {0.0, 0.0, 0.0};
+    for (long long t = vt; t < n_fn; t += nthr) {
+      const long long i = a.su.fn[t];
+      const double m = a.m[i];
 #pragma unroll
-    for (int d = 0; d < 3; ++d) vc[d] += a.bias[3 * c + d];
-    const double vhat = -a.phi[c] / cm.den;
-    const double mug = a.mu[c] * a.gamma_lag[c];
-    a.cvhat[c] = vhat;
-    a.cmug[c] = mug;
-    e_acc += contact_terms(cm, vc, vhat, mug, R, gw, rgr);
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      a.vc[3 * c + d] = vc[d];
-      a.gw[3 * c + d] = gw[d];
-      if (inreg) vcr[j][d] = vc[d];
+      for (int d = 0; d < 3; ++d) {
+        const double vs = a.v_star[3 * i + d];
+        const double e0 = a.v0[3 * i + d] - vs;
+        r3[0] += m * e0 * e0;
+        r3[1] += m * vs * vs;
+        r3[2] += m * vs * e0;
+      }
     }
-#pragma unroll
-    for (int e = 0; e < 6; ++e) a.rgr[6 * c + e] = rgr[e];
-  })
-  sync();
+    for (long long c0 = chunk0; c0 < nc; c0 += chunk_step)
+    {
+      stage_weights(a, c0, nc, s_w_w);
+      contact_update_chunk(a, cm, c0, nc, true, 0.0, s_gw_w, s_w_w, e_acc);
+    }
+    double s3[3];
+    reduce_all<3>(sync, parity, r3, s3, sm);  // also publishes vc / cellsum grid-wide
+    S0 = s3[0];
+    Q0 = s3[1];
+    Q1 = s3[2];
+  }
   lap(0);
 
   int iterations = 0, ls_evals_total = 0, status = 0;
   bool converged = false;
   double alpha_prev = 0.0;  // pending v += alpha dv, applied by each node's owner in N
+  double P = 1.0;           // free nodes: v - v* = P (v0 - v*)
   for (int it = 0;; ++it) {
-    // ---- N: pending update, node gathers, gradient, residual, Hessian, direction
+    // ---- N: pending update, gathers, gradient, residual, Hessian, direction
     double red[8] = {0, 0, 0, 0, e_acc, 0, 0, 0};
     int reg_count = 0;
-    auto take_node = [&](long long i) -> NodeIn {
-      NodeIn nin = load_node(a, i);
-      if (it > 0) {
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          nin.v[d] = nin.v[d] + alpha_prev * a.dv[3 * i + d];
-          v[3 * i + d] = nin.v[d];
-        }
-      }
-      return nin;
-    };
-    // (a1) heavy contact nodes (> kHeavyNode entries): one warp each
-    for (long long t = gwarp; t < n_hn; t += nwarps) {
-      const long long i = a.adj.hn[t];
-      const int e0 = a.adj.hn_e[2 * t], e1 = a.adj.hn_e[2 * t + 1];
-      NodeIn nin{};
-      if (lane == 0) nin = take_node(i);
-      double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-#pragma unroll 4
-      for (int e = e0 + lane; e < e1; e += 32) {
-        const long long c = __ldg(&a.adj.ent[e]) >> 5;
-        const double w = __ldg(&a.adj.w[e]);
-        const double w2 = w * w;
-#pragma unroll
-        for (int d = 0; d < 3; ++d) acc[d] += w * a.gw[3 * c + d];
-#pragma unroll
-        for (int q = 0; q < 6; ++q) acc[3 + q] += w2 * a.rgr[6 * c + q];
-      }
-#pragma unroll
-      for (int q = 0; q < 9; ++q)
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
-      if (lane == 0) node_finish(a, i, nin, acc, acc + 3, red, reg_count);
-    }
-    // (a2) light contact nodes: 8-lane groups, four nodes in flight per warp
+    cta_start();
+    if (it > 0) P *= (1.0 - alpha_prev);
     {
-      const int grp = lane >> 3, gl = lane & 7;
-      for (long long t0 = gwarp * 4; t0 < n_cn; t0 += nwarps * 4) {
+      // 4 lanes per contact node (8 nodes per warp), warp-interleaved over CTAs
+      const int grp = lane >> 2, gl = lane & 3;
+      const long long vw = (long long)wid * nctas + blockIdx.x, nw = (long long)nctas * kWarps;
+      for (long long t0 = vw * 8; t0 < n_cn; t0 += nw * 8) {
         const long long t = t0 + grp;
         const bool live = t < n_cn;
-        const long long i = live ? a.adj.cn[t] : 0;
-        const int e0 = live ? a.adj.cn_e[2 * t] : 0, e1 = live ? a.adj.cn_e[2 * t + 1] : 0;
-        NodeIn nin{};
-        if (live && gl == 0) nin = take_node(i);
+        const int4 rec = live ? a.su.cn_rec[t] : make_int4(0, 0, 0, 0);
+        const long long i = rec.x;
+        NodeIn nin;
+        if (live && gl == 0) {
+          nin.m = a.m[i];
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            nin.v[d] = v[3 * i + d];
+            nin.vs[d] = a.v_star[3 * i + d];
+          }
+          if (it > 0) {
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+              nin.v[d] = nin.v[d] + alpha_prev * a.dv[3 * i + d];
+              v[3 * i + d] = nin.v[d];
+            }
+          }
+        }
         double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-#pragma unroll 4
-        for (int e = e0 + gl; e < e1; e += 8) {
-          const long long c = __ldg(&a.adj.ent[e]) >> 5;
-          const double w = __ldg(&a.adj.w[e]);
-          const double w2 = w * w;
-#pragma unroll
-          for (int d = 0; d < 3; ++d) acc[d] += w * a.gw[3 * c + d];
-#pragma unroll
-          for (int q = 0; q < 6; ++q) acc[3 + q] += w2 * a.rgr[6 * c + q];
+#pragma unroll 2
+        for (int e = rec.y + gl; e < rec.z; e += 4) {
+          const int key = __ldg(&a.su.ent[e]);
+          const double2* src = reinterpret_cast<const double2*>(
+              a.cellsum + ((long long)(key >> 5) * 27 + (key & 31)) * kCellSumStride);
+          const double2 q0 = src[0], q1 = src[1], q2 = src[2], q3 = src[3], q4 = src[4];
+          acc[0] += q0.x;
+          acc[1] += q0.y;
+          acc[2] += q1.x;
+          acc[3] += q1.y;
+          acc[4] += q2.x;
+          acc[5] += q2.y;
+          acc[6] += q3.x;
+          acc[7] += q3.y;
+          acc[8] += q4.x;
         }
 #pragma unroll
         for (int q = 0; q < 9; ++q)
 #pragma unroll
-          for (int o = 4; o > 0; o >>= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
+          for (int o = 2; o > 0; o >>= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
         if (live && gl == 0) node_finish(a, i, nin, acc, acc + 3, red, reg_count);
       }
     }
-    if (prof) {
-      unsigned long long t = gtime();
-      pt[12] += t - tmark;
-      tmark = t;
-    }
-    // (b) nodes without contacts: thread per node
-    {
-      const double zero[6] = {0, 0, 0, 0, 0, 0};
-      for (long long t = tid; t < n_fn; t += nthr) {
-        const long long i = a.adj.fn[t];
-        node_finish(a, i, take_node(i), zero, zero, red, reg_count);
-      }
+    lap(6);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      // free nodes in closed form: g = m P e0, dv = -P e0
+      const double p2s = P * P * S0;
+      red[0] += p2s;
+      red[1] += Q0 + 2.0 * P * Q1 + p2s;
+      red[3] += p2s;
+      red[5] -= p2s;
+      red[6] += p2s;
     }
     if (reg_count) atomicAdd(&a.out->regularized, reg_count);
-    if (prof) {
-      unsigned long long t = gtime();
-      pt[13] += t - tmark;
-      tmark = t;
-    }
+    cta_stop(0);
     double s[8];
     reduce_all<8>(sync, parity, red, s, sm);
     lap(1);
@@ -521,53 +778,123 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
       break;
     }
     const double a1 = s[5], a2 = s[6];
-    double alpha_final = 0.0;
-    if (gr.member) {
-      // ---- D: dvc = R J dv and the phi'(0) contact term (solver.py:305-310, 269)
-      double r0[1] = {0.0};
-      FOR_OWNED_CONTACTS({
-        double R[9], dvc[3], vc[3], g[3];
+
+    // ---- D: dvc = R J dv and the phi'(0) contact term (solver.py:305-310, 269)
+    double r0 = 0.0;
+    cta_start();
+    const bool dbg = a.debug && it == 5 && blockIdx.x == 0 && threadIdx.x == 0;
+    unsigned long long td[6] = {0, 0, 0, 0, 0, 0};
+    if (dbg) td[0] = gtime();
+    for (long long c0 = chunk0; c0 < nc; c0 += chunk_step) {
+      const long long c = c0 + lane;
+      if (c < nc) {
+        double R[9], dvc[3], vc[3];
         load_frame(a.frames, c, R);
-        gather_contact(a, c, a.dv, R, dvc);
-#pragma unroll
-        for (int d = 0; d < 3; ++d) vc[d] = inreg ? vcr[j][d] : a.vc[3 * c + d];
-        double Gd[4];
-        cm_eval(cm, vc, a.cvhat[c], a.cmug[c], g, Gd);
-        r0[0] += g[0] * dvc[0] + g[1] * dvc[1] + g[2] * dvc[2];
+        if (dbg) {
+          double sR = R[0] + R[4];
+          td[1] = gtime() + (sR == 12345.0);
+        }
+        if (resident) gather_contact_sw(a, c, a.dv, R, s_w_w, lane, dvc);
+        else gather_contact(a, c, a.dv, R, dvc);
+        if (dbg) td[2] = gtime() + (dvc[0] == 12345.0);
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
-          if (inreg) dvcr[j][d] = dvc[d];
-          else a.dvc[3 * c + d] = dvc[d];
+          a.dvc[3 * c + d] = dvc[d];
+          vc[d] = a.vc[3 * c + d];
         }
-      })
-      double d0s[1];
-      group_reduce<1>(gr, sync, parity, cparity, r0, d0s, sm, cslot);
-      lap(2);
-      const double d0 = a1 + d0s[0];
+        double dd2 = 0.0;
+        ls_terms(cm, inv_eps, vc, dvc, a.cvhat[c], a.cmug[c], 0.0, r0, dd2);
+        if (dbg) td[3] = gtime() + (r0 == 12345.0);
+      }
+    }
+    __syncwarp();
+    if (dbg) td[4] = gtime();
+    lap(7);
+    cta_stop(1);
+    if (dbg) {
+      td[5] = gtime();
+      printf("D timeline (ns): frame %llu gather %llu ls %llu warp %llu cta %llu\n",
+             td[1] - td[0], td[2] - td[1], td[3] - td[2], td[4] - td[3], td[5] - td[4]);
+    }
+    // hand the contact data and the phi'(0) partials to the group
+    double d0s = 0.0;
+    if (nctas == 1) {
+      double rr[1] = {r0}, ss[1];
+      group_reduce<1>(1, a.slots, tagB, rr, ss, sm);
+      d0s = ss[0];
+    } else {
+      double rr[1] = {r0}, bs[1];
+      block_reduce<1>(rr, sm, bs);
+      unsigned long long* base = a.slots + kSlotA + (long long)(tagA & 1u) * kMaxSolverCtas * 2;
+      if (threadIdx.x == 0) {
+        fence_acq_rel_gpu();  // release this CTA's dvc writes (bar.sync made them CTA-visible)
+        slot_publish<1>(base + 2LL * blockIdx.x, bs, tagA);
+      }
+      if (in_group && threadIdx.x < 32) {
+        double r[1];
+        slot_poll_sum<1, (kMaxSolverCtas + 31) / 32>(base, nctas, tagA, r);
+        fence_acq_rel_gpu();  // acquire: the producers' dvc writes are visible below
+        if (threadIdx.x == 0) s_bc[0] = r[0];
+      }
+      ++tagA;
+      __syncthreads();
+      d0s = s_bc[0];
+      __syncthreads();
+    }
+    lap(2);
+    double alpha_final = 0.0;
+    if (in_group) {
+      const double d0 = a1 + d0s;
       if (!isfinite(d0) || d0 >= 0.0) {
         status = MPMRB_E_NOT_DESCENT;
       } else {
-        // ---- LS: exact line search (solver.py:266-298)
+        // ---- LS: exact line search (solver.py:266-298) over the group
+        const long long gtid = (long long)blockIdx.x * kThreads + threadIdx.x;
+        const long long gthr = (long long)G * kThreads;
+        const double eps2 = cm.eps_v * cm.eps_v;
+        LsRec lv[kLS];
+#pragma unroll
+        for (int j = 0; j < kLS; ++j) {
+          const long long c = gtid + j * gthr;
+          double vc[3] = {0.0, 0.0, 0.0}, dvc[3] = {0.0, 0.0, 0.0}, vh = 0.0, mg = 0.0;
+          if (c < nc) {  // absent contacts keep dvc = 0, mug = 0 and add exactly 0
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+              vc[d] = __ldcg(&a.vc[3 * c + d]);
+              dvc[d] = __ldcg(&a.dvc[3 * c + d]);
+            }
+            vh = __ldcg(&a.cvhat[c]);
+            mg = __ldcg(&a.cmug[c]);
+          }
+          lv[j] = ls_rec(cm, vc, dvc, vh, mg);
+        }
         double lo = 0.0, hi = INFINITY, alpha = 1.0;
         alpha_final = -1.0;
         int evals = 0;
         for (int ev = 1; ev <= a.ls_max; ++ev) {
+          unsigned long long tls0 = prof ? gtime() : 0ull;
           double rr[2] = {0.0, 0.0};
-          FOR_OWNED_CONTACTS({
+#pragma unroll
+          for (int j = 0; j < kLS; ++j) ls_terms_rec(cm, eps2, inv_eps, lv[j], alpha, rr[0], rr[1]);
+          for (long long c = gtid + kLS * gthr; c < nc; c += gthr) {
             double vc[3], dvc[3];
 #pragma unroll
             for (int d = 0; d < 3; ++d) {
-              dvc[d] = inreg ? dvcr[j][d] : a.dvc[3 * c + d];
-              vc[d] = (inreg ? vcr[j][d] : a.vc[3 * c + d]) + alpha * dvc[d];
+              vc[d] = __ldcg(&a.vc[3 * c + d]);
+              dvc[d] = __ldcg(&a.dvc[3 * c + d]);
             }
-            double g[3], G[4];
-            cm_eval(cm, vc, a.cvhat[c], a.cmug[c], g, G);
-            rr[0] += g[0] * dvc[0] + g[1] * dvc[1] + g[2] * dvc[2];
-            rr[1] += dvc[0] * (G[0] * dvc[0] + G[3] * dvc[1]) +
-                     dvc[1] * (G[3] * dvc[0] + G[1] * dvc[1]) + dvc[2] * (G[2] * dvc[2]);
-          })
+            ls_terms(cm, inv_eps, vc, dvc, __ldcg(&a.cvhat[c]), __ldcg(&a.cmug[c]), alpha, rr[0],
+                     rr[1]);
+          }
           double ss[2];
-          group_reduce<2>(gr, sync, parity, cparity, rr, ss, sm, cslot);
+          unsigned long long tls1 = prof ? gtime() : 0ull;
+          if (CL > 1) cluster_reduce<2>(CL, s_cl, cpar, rr, ss, sm);
+          else group_reduce<2>(G, a.slots, tagB, rr, ss, sm);
+          if (prof) {
+            unsigned long long tls2 = gtime();
+            pt[12] += tls1 - tls0;
+            pt[13] += tls2 - tls1;
+          }
           evals = ev;
           const double d = a1 + a2 * alpha + ss[0];
           const double dd = a2 + ss[1];
@@ -587,68 +914,88 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
         }
         if (alpha_final < 0.0) alpha_final = (lo > 0.0) ? lo : alpha;  // solver.py:296-298
         ls_evals_total += evals;
-        lap(3);
-        // ---- U (contacts): vc += alpha dvc and the contact terms for the next N
-        e_acc = 0.0;
-        FOR_OWNED_CONTACTS({
-          double vc[3], R[9], gw[3], rgr[6];
-#pragma unroll
-          for (int d = 0; d < 3; ++d) {
-            if (inreg) vc[d] = vcr[j][d] = vcr[j][d] + alpha_final * dvcr[j][d];
-            else vc[d] = a.vc[3 * c + d] + alpha_final * a.dvc[3 * c + d];
-            a.vc[3 * c + d] = vc[d];
-          }
-          load_frame(a.frames, c, R);
-          e_acc += contact_terms(cm, vc, a.cvhat[c], a.cmug[c], R, gw, rgr);
-#pragma unroll
-          for (int d = 0; d < 3; ++d) a.gw[3 * c + d] = gw[d];
-#pragma unroll
-          for (int q = 0; q < 6; ++q) a.rgr[6 * c + q] = rgr[q];
-        })
       }
-      // publish the step (and the status) to the CTAs outside the group
-      if (gr.rank == 0 && threadIdx.x == 0) {
-        a.ls_out[0] = alpha_final;
-        a.ls_out[1] = (double)status;
-        if (a.tr_alpha && status == 0) a.tr_alpha[it] = alpha_final;
+      if (nctas > 1 && blockIdx.x == 0 && threadIdx.x == 0) {
+        const double pub[2] = {alpha_final, (double)status};
+        slot_publish<2>(a.slots + kSlotC + (long long)(tagC & 1u) * 4, pub, tagC);
+      }
+      if (blockIdx.x == 0 && threadIdx.x == 0 && a.tr_alpha && status == 0)
+        a.tr_alpha[it] = alpha_final;
+    } else if (threadIdx.x < 32) {
+      double r[2];
+      slot_poll_sum<2, 1, 256>(a.slots + kSlotC + (long long)(tagC & 1u) * 4, 1, tagC, r);
+      if (threadIdx.x == 0) {
+        s_bc[0] = r[0];
+        s_bc[1] = r[1];
       }
     }
-    sync();  // gw/rgr, alpha and status visible grid-wide
-    if (!gr.member || gr.cluster) {
-      alpha_final = __ldcg(&a.ls_out[0]);
-      status = (int)__ldcg(&a.ls_out[1]);
+    if (nctas > 1) {
+      ++tagC;
+      __syncthreads();
+      if (!in_group) {
+        alpha_final = s_bc[0];
+        status = (int)s_bc[1];
+      }
+      __syncthreads();
     }
-    lap(4);
+    lap(3);
     if (status) break;
+    // ---- U: vc += alpha dvc, contact terms -> cellsum for the next N
+    e_acc = 0.0;
+    cta_start();
+    for (long long c0 = chunk0; c0 < nc; c0 += chunk_step)
+    {
+      if (!resident) stage_weights(a, c0, nc, s_w_w);
+      contact_update_chunk(a, cm, c0, nc, false, alpha_final, s_gw_w, s_w_w, e_acc);
+    }
+    lap(8);
+    cta_stop(2);
+    sync();  // cellsum and vc visible grid-wide
+    lap(4);
     alpha_prev = alpha_final;
     ++iterations;
   }
-  // The last N applied every pending update, so v is final here (grid synced).
-  // ---- epilogue: impulses gamma = -g_c(vc) (solver.py:363-365)
+  // The last N applied every pending update, so contact-node v is final here.
+  // ---- epilogue: free nodes in closed form, scatter, impulses (solver.py:363-365)
   bool finite_v = true;
-  for (long long i = tid; i < nd; i += nthr) {
+  for (long long t = vt; t < n_cn; t += nthr) {
+    const long long i = a.su.cn[t];
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-      double vi = v[3 * i + d];
+      const double vi = v[3 * i + d];
       finite_v &= isfinite(vi);
       if (a.v_next_full) a.v_next_full[3 * (long long)a.act[i] + d] = vi;
     }
   }
-  FOR_OWNED_CONTACTS({
-    double vc[3], g[3];
+  for (long long t = vt; t < n_fn; t += nthr) {
+    const long long i = a.su.fn[t];
 #pragma unroll
-    for (int d = 0; d < 3; ++d) vc[d] = inreg ? vcr[j][d] : a.vc[3 * c + d];
-    double Gd[4];
-    cm_eval(cm, vc, a.cvhat[c], a.cmug[c], g, Gd);
+    for (int d = 0; d < 3; ++d) {
+      const double vs = a.v_star[3 * i + d];
+      const double vi = vs + P * (a.v0[3 * i + d] - vs);
+      v[3 * i + d] = vi;
+      finite_v &= isfinite(vi);
+      if (a.v_next_full) a.v_next_full[3 * (long long)a.act[i] + d] = vi;
+    }
+  }
+  for (long long c0 = chunk0; c0 < nc; c0 += chunk_step) {
+    const long long c = c0 + lane;
+    if (c < nc) {
+      double vc[3], g[3], Gd[4];
 #pragma unroll
-    for (int d = 0; d < 3; ++d) a.gamma[3 * c + d] = -g[d];
-  })
-#undef FOR_OWNED_CONTACTS
+      for (int d = 0; d < 3; ++d) vc[d] = a.vc[3 * c + d];
+      cm_eval(cm, vc, a.cvhat[c], a.cmug[c], g, Gd);
+#pragma unroll
+      for (int d = 0; d < 3; ++d) a.gamma[3 * c + d] = -g[d];
+    }
+  }
   if (threadIdx.x == 0) s_flag = 0;
   __syncthreads();
   if (!finite_v) s_flag = 1;
   __syncthreads();
   if (s_flag && threadIdx.x == 0) atomicOr(&a.out->status_flags, 1);
+  if (cprof)
+    for (int ph = 0; ph < 3; ++ph) a.prof[kSolverProf + ph * 160 + blockIdx.x] += cta_acc[ph];
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     a.out->converged = converged ? 1 : 0;
     a.out->iterations = iterations;
@@ -656,171 +1003,226 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
     a.out->status = status;
     a.out->n_contacts = nc;
     a.out->n_dofs = 3 * nd;
+    a.chan[0] = tagA;
+    a.chan[1] = tagB;
+    a.chan[2] = tagC;
     if (prof) {
       lap(5);
       for (int k = 0; k < 6; ++k) a.prof[k] += pt[k];
+      a.prof[14] += pt[6] + ((unsigned long long)pt[7] << 32);
+      a.prof[15] += pt[8];
       a.prof[6] += (unsigned long long)iterations;
       a.prof[7] += (unsigned long long)ls_evals_total;
-      a.prof[8] += (unsigned long long)nctas + ((unsigned long long)gr.size << 32);
+      a.prof[8] += (unsigned long long)nctas + ((unsigned long long)G << 32);
       a.prof[9] += 1ull;
-      a.prof[11] += (unsigned long long)n_cn + ((unsigned long long)n_hn << 32);
+      a.prof[11] += (unsigned long long)n_cn + ((unsigned long long)ng << 32);
       a.prof[12] += pt[12];
       a.prof[13] += pt[13];
     }
   }
 }
 
-// ---------------------------------------------------------------- adjacency
+// ---------------------------------------------------------------- setup
 
-__global__ void k_adj_count(const int* __restrict__ nc_dev, long long nc_cap,
-                            const int* __restrict__ cnodes, const double* __restrict__ cw,
-                            int* __restrict__ cnt) {
-  const long long nc = *nc_dev;
-  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (e >= nc * 27) return;
-  const long long k = e / nc, c = e - k * nc;
-  if (cw[k * nc_cap + c] != 0.0) atomicAdd(&cnt[cnodes[k * nc_cap + c]], 1);
+constexpr int kSetupThreads = 256;
+
+__device__ __forceinline__ bool same_stencil(const int* __restrict__ cnodes, long long nc_cap,
+                                             long long c, long long d) {
+  bool same = true;
+#pragma unroll 9
+  for (int k = 0; k < 27; ++k)
+    same &= __ldg(&cnodes[(long long)k * nc_cap + c]) == __ldg(&cnodes[(long long)k * nc_cap + d]);
+  return same;
 }
 
-__global__ void k_adj_fill(const int* __restrict__ nc_dev, long long nc_cap,
-                           const int* __restrict__ cnodes, const double* __restrict__ cw,
-                           const int* __restrict__ off, int* __restrict__ fill,
-                           int* __restrict__ ent) {
+__global__ void k_su_heads(const int* __restrict__ nc_dev, long long nc_cap,
+                           const int* __restrict__ cnodes, int* __restrict__ head) {
   const long long nc = *nc_dev;
-  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (e >= nc * 27) return;
-  const long long k = e / nc, c = e - k * nc;
-  if (cw[k * nc_cap + c] == 0.0) return;
-  const int node = cnodes[k * nc_cap + c];
-  const int pos = off[node] + atomicAdd(&fill[node], 1);
-  ent[pos] = (int)((c << 5) | k);
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < nc;
+       c += (long long)gridDim.x * blockDim.x)
+    head[c] = (c % kChunk == 0 || !same_stencil(cnodes, nc_cap, c, c - 1)) ? 1 : 0;
+}
+
+__global__ void k_su_groups(const int* __restrict__ nc_dev, const int* __restrict__ head,
+                            const int* __restrict__ head_off, const int* __restrict__ counts,
+                            int* __restrict__ grp_of, int* __restrict__ grp_start) {
+  const long long nc = *nc_dev;
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < nc;
+       c += (long long)gridDim.x * blockDim.x) {
+    const int h = head[c], o = head_off[c];
+    grp_of[c] = o + h - 1;
+    if (h) grp_start[o] = (int)c;
+    if (c == 0) grp_start[counts[0]] = (int)nc;
+  }
+}
+
+__global__ void k_su_count(const int* __restrict__ counts, long long nc_cap,
+                           const int* __restrict__ cnodes, const int* __restrict__ grp_start,
+                           int* __restrict__ cnt) {
+  const long long np = (long long)counts[0] * 27;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < np;
+       p += (long long)gridDim.x * blockDim.x) {
+    const long long g = p / 27, k = p - g * 27;
+    const int node = cnodes[k * nc_cap + grp_start[g]];
+    if (node >= 0) atomicAdd(&cnt[node], 1);
+  }
+}
+
+__global__ void k_su_fill(const int* __restrict__ counts, long long nc_cap,
+                          const int* __restrict__ cnodes, const int* __restrict__ grp_start,
+                          const int* __restrict__ off, int* __restrict__ fill,
+                          int* __restrict__ ent_tmp) {
+  const long long np = (long long)counts[0] * 27;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < np;
+       p += (long long)gridDim.x * blockDim.x) {
+    const long long g = p / 27, k = p - g * 27;
+    const int node = cnodes[k * nc_cap + grp_start[g]];
+    if (node < 0) continue;
+    const int pos = off[node] + atomicAdd(&fill[node], 1);
+    ent_tmp[pos] = (int)((g << 5) | k);
+  }
 }
 
 // Place every entry at its sorted position inside its node's segment: the
-// rank is the number of smaller keys in the same segment (keys are unique),
-// so the gathers sum in (contact, slot) order regardless of the atomic fill
-// order.  Entry-parallel: O(L) work per entry, no serial per-node sort.
-__global__ void k_adj_rank(const int* __restrict__ nd_dev, long long nc_cap,
-                           const int* __restrict__ cnodes, const double* __restrict__ cw,
-                           const int* __restrict__ off, const int* __restrict__ ent_u,
-                           int* __restrict__ ent, double* __restrict__ wout) {
-  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const int total = off[*nd_dev];
-  if (e >= total) return;
-  const int key = ent_u[e];
-  const long long c = key >> 5, k = key & 31;
-  const int node = cnodes[k * nc_cap + c];
-  const int b = off[node], en = off[node + 1];
-  int rank = 0;
-  for (int p = b; p < en; ++p) rank += (__ldg(&ent_u[p]) < key) ? 1 : 0;
-  ent[b + rank] = key;
-  wout[b + rank] = cw[k * nc_cap + c];
-}
-
-__global__ void k_adj_flag(const int* __restrict__ nd_dev, const int* __restrict__ off,
-                           int* __restrict__ flag, int* __restrict__ hflag) {
-  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i >= *nd_dev) return;
-  const int L = off[i + 1] - off[i];
-  flag[i] = (L > 0 && L <= kHeavyNode) ? 1 : 0;
-  hflag[i] = (L > kHeavyNode) ? 1 : 0;
-}
-
-__global__ void k_adj_lists(const int* __restrict__ nd_dev, SolverAdjacency adj) {
-  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i >= *nd_dev) return;
-  const int o = adj.flag_off[i], ho = adj.hflag_off[i];
-  if (adj.flag[i]) {
-    adj.cn[o] = (int)i;
-    adj.cn_e[2 * o] = adj.off[i];
-    adj.cn_e[2 * o + 1] = adj.off[i + 1];
-  } else if (adj.hflag[i]) {
-    adj.hn[ho] = (int)i;
-    adj.hn_e[2 * ho] = adj.off[i];
-    adj.hn_e[2 * ho + 1] = adj.off[i + 1];
-  } else {
-    adj.fn[i - o - ho] = (int)i;
+// rank is the number of smaller keys in the same segment (keys are unique).
+__global__ void k_su_rank(const int* __restrict__ nd_dev, long long nc_cap,
+                          const int* __restrict__ cnodes, const int* __restrict__ grp_start,
+                          const int* __restrict__ off, const int* __restrict__ ent_tmp,
+                          int* __restrict__ ent) {
+  const long long total = off[*nd_dev];
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int key = ent_tmp[e];
+    const long long g = key >> 5, k = key & 31;
+    const int node = cnodes[k * nc_cap + grp_start[g]];
+    const int b = off[node], en = off[node + 1];
+    int rank = 0;
+    for (int p = b; p < en; ++p) rank += (__ldg(&ent_tmp[p]) < key) ? 1 : 0;
+    ent[b + rank] = key;
   }
+}
+
+__global__ void k_su_flag(const int* __restrict__ nd_dev, const int* __restrict__ cnt,
+                          int* __restrict__ flag) {
+  const long long nd = *nd_dev;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nd;
+       i += (long long)gridDim.x * blockDim.x)
+    flag[i] = cnt[i] > 0 ? 1 : 0;
+}
+
+__global__ void k_su_lists(const int* __restrict__ nd_dev, const int* __restrict__ flag,
+                           const int* __restrict__ flag_off, const int* __restrict__ off,
+                           int* __restrict__ cn, int4* __restrict__ cn_rec,
+                           int* __restrict__ fn) {
+  const long long nd = *nd_dev;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nd;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int o = flag_off[i];
+    if (flag[i]) {
+      cn[o] = (int)i;
+      cn_rec[o] = make_int4((int)i, off[i], off[i + 1], 0);
+    } else {
+      fn[i - o] = (int)i;
+    }
+  }
+}
+
+unsigned su_grid(long long cap) {
+  long long b = (cap + kSetupThreads - 1) / kSetupThreads;
+  if (b < 1) b = 1;
+  if (b > 148 * 8) b = 148 * 8;
+  return (unsigned)b;
 }
 
 }  // namespace
 
-int launch_solver_adjacency(Ctx& c, const int* nd_dev, const int* nc_dev, long long nd_cap,
-                            long long nc_cap, const int* cnodes, const double* cw,
-                            const SolverAdjacency& adj, DevBuf& tiles) {
-  MPMRB_CUDA_OK(cudaMemsetAsync(adj.cnt, 0, sizeof(int) * (nd_cap + 1), c.stream));
-  MPMRB_CUDA_OK(cudaMemsetAsync(adj.fill, 0, sizeof(int) * (nd_cap + 1), c.stream));
-  MPMRB_CUDA_OK(cudaMemsetAsync(adj.flag, 0, sizeof(int) * (nd_cap + 1), c.stream));
-  MPMRB_CUDA_OK(cudaMemsetAsync(adj.hflag, 0, sizeof(int) * (nd_cap + 1), c.stream));
-  const long long ne = nc_cap * 27;
-  if (ne > 0) {
-    k_adj_count<<<grid_for(ne, 256), 256, 0, c.stream>>>(nc_dev, nc_cap, cnodes, cw, adj.cnt);
-    c.launches++;
-  }
-  // exclusive scan over nd+1 entries (the trailing zero makes off[nd] the total)
-  int rc = scan_exclusive_i32(c, adj.cnt, adj.off, nd_cap + 1, nullptr, nullptr, tiles);
+int launch_solver_setup(Ctx& c, const int* nd_dev, const int* nc_dev, long long nd_cap,
+                        long long nc_cap, const int* cnodes, const SolverSetup& su,
+                        DevBuf& tiles) {
+  MPMRB_CUDA_OK(cudaMemsetAsync(su.cnt, 0, sizeof(int) * (nd_cap + 1), c.stream));
+  MPMRB_CUDA_OK(cudaMemsetAsync(su.fill, 0, sizeof(int) * (nd_cap + 1), c.stream));
+  MPMRB_CUDA_OK(cudaMemsetAsync(su.flag, 0, sizeof(int) * (nd_cap + 1), c.stream));
+  MPMRB_CUDA_OK(cudaMemsetAsync(su.counts, 0, sizeof(int) * 2, c.stream));
+  const long long ncc = nc_cap > 0 ? nc_cap : 1;
+  k_su_heads<<<su_grid(ncc), kSetupThreads, 0, c.stream>>>(nc_dev, nc_cap, cnodes, su.head);
+  int rc = scan_exclusive_i32(c, su.head, su.head_off, ncc, nc_dev, su.counts + 0, tiles);
   if (rc) return rc;
-  if (ne > 0) {
-    k_adj_fill<<<grid_for(ne, 256), 256, 0, c.stream>>>(nc_dev, nc_cap, cnodes, cw, adj.off,
-                                                        adj.fill, adj.ent_tmp);
-    k_adj_rank<<<grid_for(ne, 256), 256, 0, c.stream>>>(nd_dev, nc_cap, cnodes, cw, adj.off,
-                                                        adj.ent_tmp, adj.ent, adj.w);
-    c.launches += 2;
-  }
-  if (nd_cap > 0) {
-    k_adj_flag<<<grid_for(nd_cap, 256), 256, 0, c.stream>>>(nd_dev, adj.off, adj.flag,
-                                                            adj.hflag);
-    c.launches++;
-  }
-  rc = scan_exclusive_i32(c, adj.flag, adj.flag_off, nd_cap + 1, nullptr, adj.n_cn, tiles);
+  k_su_groups<<<su_grid(ncc), kSetupThreads, 0, c.stream>>>(nc_dev, su.head, su.head_off,
+                                                            su.counts, su.grp_of, su.grp_start);
+  k_su_count<<<su_grid(27 * ncc), kSetupThreads, 0, c.stream>>>(su.counts, nc_cap, cnodes,
+                                                                 su.grp_start, su.cnt);
+  c.launches += 3;
+  // exclusive scan over nd_cap+1 entries (cnt is zero past nd: off[nd] = total)
+  rc = scan_exclusive_i32(c, su.cnt, su.off, nd_cap + 1, nullptr, nullptr, tiles);
   if (rc) return rc;
-  rc = scan_exclusive_i32(c, adj.hflag, adj.hflag_off, nd_cap + 1, nullptr, adj.n_hn, tiles);
+  k_su_fill<<<su_grid(27 * ncc), kSetupThreads, 0, c.stream>>>(su.counts, nc_cap, cnodes,
+                                                                su.grp_start, su.off, su.fill,
+                                                                su.ent_tmp);
+  k_su_rank<<<su_grid(27 * ncc), kSetupThreads, 0, c.stream>>>(nd_dev, nc_cap, cnodes,
+                                                                su.grp_start, su.off, su.ent_tmp,
+                                                                su.ent);
+  k_su_flag<<<su_grid(nd_cap + 1), kSetupThreads, 0, c.stream>>>(nd_dev, su.cnt, su.flag);
+  c.launches += 3;
+  rc = scan_exclusive_i32(c, su.flag, su.flag_off, nd_cap + 1, nullptr, su.counts + 1, tiles);
   if (rc) return rc;
-  if (nd_cap > 0) {
-    k_adj_lists<<<grid_for(nd_cap, 256), 256, 0, c.stream>>>(nd_dev, adj);
-    c.launches++;
-  }
+  k_su_lists<<<su_grid(nd_cap + 1), kSetupThreads, 0, c.stream>>>(
+      nd_dev, su.flag, su.flag_off, su.off, su.cn, su.cn_rec, su.fn);
+  c.launches++;
   MPMRB_CUDA_OK(cudaGetLastError());
   return MPMRB_OK;
 }
 
 int launch_qn_solve(Ctx& c, const SolverArgs& a, int grid_ctas) {
-  // Grid: one CTA per SM (launch bounds + 128 registers).  Preferred launch:
-  // clusters of 8 (the contact group is cluster 0) as many as co-reside.
-  static int sms = -1, cluster_grid = -1;
+  // Grid: one CTA per SM (launch bounds + 128 registers), cooperative,
+  // launched as clusters of CL CTAs (cluster 0 is the line-search group) when
+  // CL clusters fill the GPU; MPMRB_SOLVER_CLUSTER=0 disables clusters.
+  static int sms = -1, cl_size = 0, cl_grid = 0;
   if (sms < 0) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (sms > kMaxSolverCtas) sms = kMaxSolverCtas;
-    cluster_grid = 0;
-    // Opt-in: measured on the 256k sand pile (17.5k contacts) the 8-CTA
-    // contact cluster loses to grid-wide ownership (6.5 vs 4.8 us per
-    // line-search evaluation: the fp64 divide/sqrt work of 17.5k contacts on
-    // 8 SMs outweighs the cheaper cluster barrier).
+    int want = 0;  // measured: slot reductions over a 12-16 CTA group beat 4-CTA clusters
     const char* env = getenv("MPMRB_SOLVER_CLUSTER");
-    if (env && atoi(env) > 0) {
+    if (env) want = atoi(env);
+    if (want > kMaxCluster) want = kMaxCluster;
+    if (want > 1)
+      cudaFuncSetAttribute(k_qn_solve, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    for (int cs = want; cs > 1; cs /= 2) {
       cudaLaunchConfig_t q = {};
       q.blockDim = dim3(kThreads);
-      q.gridDim = dim3(kSolverCluster);
+      q.gridDim = dim3(cs);
       cudaLaunchAttribute qa[1];
       qa[0].id = cudaLaunchAttributeClusterDimension;
-      qa[0].val.clusterDim.x = kSolverCluster;
+      qa[0].val.clusterDim.x = cs;
       qa[0].val.clusterDim.y = 1;
       qa[0].val.clusterDim.z = 1;
       q.attrs = qa;
       q.numAttrs = 1;
       int ncl = 0;
-      if (cudaOccupancyMaxActiveClusters(&ncl, k_qn_solve, &q) == cudaSuccess && ncl > 0) {
-        cluster_grid = ncl * kSolverCluster;
-        if (cluster_grid > kMaxSolverCtas) cluster_grid = (kMaxSolverCtas / kSolverCluster) * kSolverCluster;
+      q.dynamicSmemBytes = sizeof(double) * kWarps * 27 * kChunk;
+      cudaFuncSetAttribute(k_qn_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)q.dynamicSmemBytes);
+      cudaError_t qe = cudaOccupancyMaxActiveClusters(&ncl, k_qn_solve, &q);
+      if (getenv("MPMRB_SOLVER_VERBOSE"))
+        fprintf(stderr, "solver: cluster %d -> max active clusters %d (%s)\n", cs, ncl,
+                cudaGetErrorString(qe));
+      if (qe == cudaSuccess && ncl > 0) {
+        int g = ncl * cs;
+        if (g > sms) g = (sms / cs) * cs;
+        // keep clusters only if they still cover >= 85% of the SMs
+        if (g * 100 >= sms * 85) {
+          cl_size = cs;
+          cl_grid = g;
+          break;
+        }
       }
       cudaGetLastError();
     }
   }
   int g = sms;
-  bool use_cluster = cluster_grid > 0;
-  if (use_cluster) g = cluster_grid;
+  bool use_cluster = cl_size > 1;
+  if (use_cluster) g = cl_grid;
   if (grid_ctas > 0 && grid_ctas < g) {
     g = grid_ctas;
     use_cluster = false;
@@ -832,13 +1234,19 @@ int launch_qn_solve(Ctx& c, const SolverArgs& a, int grid_ctas) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)g);
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = 0;
+  static bool smem_set = false;
+  const int dyn = (int)(sizeof(double) * kWarps * 27 * kChunk);
+  if (!smem_set) {
+    MPMRB_CUDA_OK(cudaFuncSetAttribute(k_qn_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+    smem_set = true;
+  }
+  cfg.dynamicSmemBytes = dyn;
   cfg.stream = c.stream;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
   attr[1].id = cudaLaunchAttributeClusterDimension;
-  attr[1].val.clusterDim.x = use_cluster ? kSolverCluster : 1;
+  attr[1].val.clusterDim.x = use_cluster ? cl_size : 1;
   attr[1].val.clusterDim.y = 1;
   attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;

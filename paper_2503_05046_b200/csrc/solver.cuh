@@ -5,10 +5,12 @@
 
 namespace mpmrb {
 
-constexpr int kSolverThreads = 512;
+constexpr int kSolverThreads = 256;
 constexpr int kMaxSolverCtas = 160;
-constexpr int kSolverCluster = 8;  // CTAs of the contact-owning cluster
 constexpr int kSolverProf = 16;  // phase timers (ns), see solver.cu
+// + per-CTA work time (ns) of the N, D and U phases: [16 + phase*kMaxSolverCtas + cta]
+constexpr int kSolverProfWords = 16 + 3 * 160;
+constexpr int kCellSumStride = 10;  // 9 channels (J^T g: 3, R^T G R: 6) padded to 80 B
 
 struct SolveOut {
   int converged;
@@ -21,29 +23,31 @@ struct SolveOut {
   int n_dofs;
 };
 
-// Node -> (contact, slot) adjacency of one solve (built by
-// launch_solver_adjacency from the contact stencils).
-struct SolverAdjacency {
-  int* cnt;      // (nd_cap+1) scratch
-  int* fill;     // (nd_cap+1) scratch
-  int* off;      // (nd_cap+1) CSR offsets
-  int* ent;      // (27 nc_cap) packed (c << 5) | k, ascending within a node
-  int* ent_tmp;  // (27 nc_cap) scratch: entries in atomic fill order
-  double* w;     // (27 nc_cap) stencil weight of each entry
-  int* flag;     // (nd_cap+1) scratch: node has 1..kHeavy entries
-  int* flag_off; // (nd_cap+1) scan of flag
-  int* hflag;    // (nd_cap+1) scratch: node has > kHeavy entries
-  int* hflag_off;// (nd_cap+1) scan of hflag
-  int* cn;       // (nd_cap) light contact nodes (8-lane groups)
-  int* cn_e;     // (2 nd_cap) CSR bounds of each light contact node
-  int* hn;       // (nd_cap) heavy contact nodes (one warp each)
-  int* hn_e;     // (2 nd_cap) CSR bounds of each heavy contact node
-  int* fn;       // (nd_cap) nodes without entries
-  int* n_cn;     // device count of light contact nodes
-  int* n_hn;     // device count of heavy contact nodes
+// Per-solve structure built by launch_solver_setup from the contact stencils.
+//
+// Contact groups: maximal runs of consecutive contacts with identical stencil
+// node lists (the contacts of one grid cell share all 27 nodes), never
+// crossing a 512-contact chunk boundary.  The J^T scatters of the gradient and
+// of the block-diagonal Hessian are accumulated per (group, slot) by the
+// contact owners, and gathered per node through a node -> (group, slot) CSR
+// whose entries are sorted: a fixed summation order, no atomics.
+struct SolverSetup {
+  int* head;       // (nc_cap+1) scratch: contact starts a group
+  int* head_off;   // (nc_cap+1) exclusive scan of head
+  int* grp_of;     // (nc_cap) group of each contact
+  int* grp_start;  // (nc_cap+1) first contact of each group, [ng] = nc
+  int* cnt;        // (nd_cap+1) scratch: entries per node
+  int* fill;       // (nd_cap+1) scratch
+  int* off;        // (nd_cap+1) CSR offsets
+  int* ent_tmp;    // (27 nc_cap) scratch: entries in atomic fill order
+  int* ent;        // (27 nc_cap) packed (group << 5) | slot, ascending within a node
+  int* flag;       // (nd_cap+1) scratch: node has entries
+  int* flag_off;   // (nd_cap+1) exclusive scan of flag
+  int* cn;         // (nd_cap) contact nodes (ascending)
+  int* fn;         // (nd_cap) free nodes (ascending)
+  int4* cn_rec;    // (nd_cap) per contact node: (node, CSR begin, CSR end, 0)
+  int* counts;     // device [0] n_groups, [1] n_contact_nodes
 };
-
-constexpr int kHeavyNode = 64;  // entries above which a node gets a whole warp
 
 struct SolverArgs {
   // sizes (device)
@@ -55,7 +59,7 @@ struct SolverArgs {
   const double* m;
   const double* v_star;
   const double* v0;
-  const int* cnodes;   // [27][nc_cap]
+  const int* cnodes;   // [27][nc_cap], -1 on dead (w = 0) slots
   const double* cw;    // [27][nc_cap]
   const double* frames;
   const double* bias;
@@ -63,23 +67,25 @@ struct SolverArgs {
   const double* mu;
   const double* gamma_lag;
   double K, den, eps_v;
-  SolverAdjacency adj;
+  SolverSetup su;
   // solver parameters (solver.py:35-49)
   double eps_a, eps_r, ls_tol;
   int max_iters, ls_max;
   int skip_if_no_contacts;
   int force_ctas;  // 0 = automatic
+  int force_ls_ctas;  // 0 = automatic
+  int debug;          // MPMRB_SOLVER_DEBUG: printf a phase timeline of iteration 5
   // work (device)
-  double* v;
-  double* dv;
-  double* vc;
-  double* dvc;
-  double* gw;        // (nc,3) R^T g_c
-  double* rgr;       // (nc,6) R^T G R (00,11,22,10,20,21)
-  double* cvhat;     // (nc,) -phi/(dt+tau_d), per solve
-  double* cmug;      // (nc,) mu*gamma_lag, per solve
-  double* partials;  // 2 x [kMaxRed][kMaxSolverCtas]
-  double* ls_out;    // (2,) line-search step and status published by the contact group
+  double* v;         // (nd,3) solution (contact nodes during the solve, all at the end)
+  double* dv;        // (nd,3)
+  double* vc;        // (nc,3) contact velocities
+  double* dvc;       // (nc,3)
+  double* cvhat;     // (nc,) -phi/(dt+tau_d)
+  double* cmug;      // (nc,) mu*gamma_lag
+  double* cellsum;   // (27 nc_cap, kCellSumStride) per (group, slot) sums
+  double* partials;  // [2][8][kMaxSolverCtas] grid reductions
+  unsigned long long* slots;  // self-validating reduction slots (see solver.cu)
+  unsigned* chan;    // [4] channel tags carried across solves
   // outputs
   double* gamma;
   double* tr_obj;
@@ -93,10 +99,13 @@ struct SolverArgs {
   double* v_next_full;
 };
 
-// Build the adjacency from cnodes/cw (w != 0 slots only).
-int launch_solver_adjacency(Ctx& c, const int* nd_dev, const int* nc_dev, long long nd_cap,
-                            long long nc_cap, const int* cnodes, const double* cw,
-                            const SolverAdjacency& adj, DevBuf& tiles);
+// words of the self-validating slot area (solver.cu)
+constexpr long long kSolverSlotWords = 2LL * kMaxSolverCtas * 2 + 2LL * kMaxSolverCtas * 4 + 2 * 4;
+
+// Build groups + node adjacency from cnodes/cw.
+int launch_solver_setup(Ctx& c, const int* nd_dev, const int* nc_dev, long long nd_cap,
+                        long long nc_cap, const int* cnodes, const SolverSetup& su,
+                        DevBuf& tiles);
 int launch_qn_solve(Ctx& c, const SolverArgs& a, int grid_ctas);
 
 }  // namespace mpmrb

@@ -28,6 +28,17 @@ def build_problem(steps=16, hx=0.2):
         mp.advance_step(st)
     dt_s = sc["dt"] / sc["substeps"]
     p = st.particles
+    if not os.environ.get("NO_SORT"):
+        # the fused path solves on (block, cell)-sorted particles; do the same
+        import numpy as np
+        x = p.x.cpu().numpy()
+        cell = np.floor(x / st.h - 0.5).astype(np.int64)
+        blk = cell >> 2
+        order = np.lexsort((cell[:, 2] & 3, cell[:, 1] & 3, cell[:, 0] & 3,
+                            blk[:, 2], blk[:, 1], blk[:, 0]))
+        idx = torch.as_tensor(order, device=p.x.device)
+        for k in ("x", "v", "f", "c", "mass", "volume0", "material_id", "plastic"):
+            setattr(p, k, getattr(p, k)[idx].contiguous())
     grid = mp.SparseGrid.allocate(p.x, st.h)
     stencil = mp.build_stencil(p.x, grid)
     plan = mp.build_sort_plan(p.x, st.h, 0)
@@ -55,25 +66,43 @@ def main():
         torch.cuda.synchronize()
         print("one solve", rep.iterations, rep.ls_evals)
         return
-    for ctas in (os.environ.get("CTAS_LIST") or "1,32,64,128,148,0").split(","):
+    for spec in (os.environ.get("CTAS_LIST") or "0").split(","):
+        ctas, _, ls = spec.partition(":")
         os.environ["MPMRB_SOLVER_CTAS"] = ctas
+        os.environ["MPMRB_SOLVER_LS_CTAS"] = ls or "0"
         mp.quasi_newton_solve(prob, par)  # warm
         torch.cuda.synchronize()
         _lib.lib().mpmrb_solver_profile(_lib.ctx(), prof, 1)
-        t0 = time.perf_counter()
-        v, g, rep = mp.quasi_newton_solve(prob, par)
-        torch.cuda.synchronize()
-        dt = time.perf_counter() - t0
+        reps = int(os.environ.get("REPS", "3"))
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            v, g, rep = mp.quasi_newton_solve(prob, par)
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - t0)
+        print("   solve ms:", " ".join(f"{1e3 * t:.2f}" for t in ts), flush=True)
+        dt = sum(ts) / reps
+        ctap = (C.c_uint64 * 480)()
+        _lib.lib().mpmrb_solver_profile_cta(_lib.ctx(), ctap)
         _lib.lib().mpmrb_solver_profile(_lib.ctx(), prof, 1)
-        it = max(1, rep.iterations)
+        it = max(1, rep.iterations) * reps
+        import numpy as np
+        cp = np.frombuffer(ctap, dtype=np.uint64).reshape(3, 160).astype(float) / 1e3 / it
+        ncta = int(prof[8] & 0xffffffff)
+        for ph, name in enumerate("NDU"):
+            v = cp[ph, :ncta]
+            print(f"   per-CTA {name} work us/iter: mean {v.mean():.2f} max {v.max():.2f} "
+                  f"(cta {int(v.argmax())}) min {v.min():.2f}", flush=True)
         ph = [prof[k] / 1e3 / it for k in range(6)]
-        print(f"ctas={ctas:>4}: {dt * 1e3:8.2f} ms, iters={rep.iterations}, "
-              f"ls_evals={rep.ls_evals}, us/iter={dt * 1e6 / it:7.1f} | per-iter us: "
-              f"N={ph[1]:.1f} D={ph[2]:.1f} LS={ph[3]:.1f} U={ph[4]:.1f} "
+        nw, dw, uw = (prof[14] & 0xffffffff) / 1e3 / it, (prof[14] >> 32) / 1e3 / it, prof[15] / 1e3 / it
+        print(f"ctas={spec:>7}: {dt * 1e3:8.2f} ms, iters={rep.iterations}, "
+              f"ls_evals={rep.ls_evals}, us/iter={dt * 1e6 * reps / it:7.1f} | per-iter us: "
+              f"N={ph[1]:.1f} (work {nw:.1f}) D={ph[2]:.1f} (work {dw:.1f}) LS={ph[3]:.1f} U={ph[4]:.1f} (work {uw:.1f}) "
               f"in-sync={prof[10] / 1e3 / it:.1f} "
-              f"(LS/eval={prof[3] / 1e3 / max(1, rep.ls_evals):.2f}) "
-              f"ctas={prof[8] & 0xffffffff} group={prof[8] >> 32} "
-              f"light_nodes={prof[11] & 0xffffffff} heavy_nodes={prof[11] >> 32} N_loopA={prof[12] / 1e3 / it:.1f} N_loopB={prof[13] / 1e3 / it:.1f}",
+              f"(LS/eval={prof[3] / 1e3 / max(1, rep.ls_evals * reps):.2f}) "
+              f"ctas={prof[8] & 0xffffffff} ls_group={prof[8] >> 32} "
+              f"contact_nodes={prof[11] & 0xffffffff} groups={prof[11] >> 32} "
+              f"ls_compute/eval={prof[12] / 1e3 / max(1, rep.ls_evals * reps):.2f} ls_reduce/eval={prof[13] / 1e3 / max(1, rep.ls_evals * reps):.2f}",
               flush=True)
 
 
