@@ -260,10 +260,11 @@ int mpmrb_qn_solve(mpmrb_ctx* ctx, const mpmrb_problem* prob_host,
  * [0] init [1] node phase [2] dvc phase [3] line search [4] update
  * [5] epilogue [6] iterations [7] line-search evals [8] sum of CTAs [9] solves. */
 int mpmrb_solver_profile(mpmrb_ctx* ctx, uint64_t* out_host /*16*/, int32_t reset);
-/* Per-CTA work time (ns) of the node (N), direction (D) and update (U) phases
- * accumulated like mpmrb_solver_profile: out_host[phase * 160 + cta], 480 words
- * (diagnostics of load balance across the cooperative grid). */
-int mpmrb_solver_profile_cta(mpmrb_ctx* ctx, uint64_t* out_host /*480*/);
+/* Per-CTA time (ns) of the node (N), direction (D), update (U) phases and of
+ * the node-phase grid reduction, accumulated like mpmrb_solver_profile:
+ * out_host[phase * 160 + cta], 800 words (diagnostics of load balance across
+ * the cooperative grid). */
+int mpmrb_solver_profile_cta(mpmrb_ctx* ctx, uint64_t* out_host /*800*/);
 
 /* ------------------------------------------------------------------ fused substep */
 /* coupling.py:115-219 as a device pipeline: one CUDA graph per substep. */

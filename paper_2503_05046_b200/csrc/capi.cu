@@ -126,6 +126,7 @@ int mpmrb_solver_profile(mpmrb_ctx* c, uint64_t* out_host, int32_t reset) {
 }
 
 int mpmrb_solver_profile_cta(mpmrb_ctx* c, uint64_t* out_host) {
+  static_assert(kSolverProfWords - kSolverProf == 800, "profile layout");
   CHECK_CTX(c);
   if (!c->solver_prof) {
     std::memset(out_host, 0, 8 * (kSolverProfWords - kSolverProf));
@@ -450,7 +451,7 @@ extern "C" int mpmrb_qn_solve(mpmrb_ctx* c, const mpmrb_problem* pr,
   rc |= c->scratch[SS_SOLVER7].grow(4 * 12 * (ndd + 2) + 64);  // node adjacency ints
   rc |= c->scratch[SS_SOLVER8].grow(2 * 4 * 27 * ncc);       // adjacency entries (+tmp)
   rc |= c->scratch[SS_PROBLEM].grow(4 * 4 * (ncc + 2));      // contact groups
-  rc |= c->scratch[SS_HOSTINFO].grow(8 * kSolverSlotWords + 64);  // reduction slots + tags
+  rc |= c->scratch[SS_HOSTINFO].grow(kSolverSyncBytes);  // reduction slots, tags, barrier
   if (rc) return MPMRB_E_CUDA;
   char* misc = c->scratch[SS_SOLVER6].as<char>();
   int* sizes = (int*)(misc + 2048);
@@ -461,8 +462,8 @@ extern "C" int mpmrb_qn_solve(mpmrb_ctx* c, const mpmrb_problem* pr,
   unsigned long long* slots = c->scratch[SS_HOSTINFO].as<unsigned long long>();
   unsigned* chan = reinterpret_cast<unsigned*>(slots + kSolverSlotWords);
   {
-    MPMRB_CUDA_OK(cudaMemsetAsync(slots, 0, 8 * kSolverSlotWords, c->stream));
-    static const unsigned ch[4] = {1u, 1u, 1u, 1u};
+    MPMRB_CUDA_OK(cudaMemsetAsync(slots, 0, kSolverSyncBytes, c->stream));
+    static const unsigned ch[4] = {1u, 1u, 1u, 0u};
     MPMRB_CUDA_OK(cudaMemcpyAsync(chan, ch, sizeof(ch), cudaMemcpyHostToDevice, c->stream));
   }
   if (nc > 0) {
@@ -531,6 +532,7 @@ extern "C" int mpmrb_qn_solve(mpmrb_ctx* c, const mpmrb_problem* pr,
   a.partials = c->scratch[SS_SOLVER5].as<double>();
   a.slots = slots;
   a.chan = chan;
+  a.bar = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(slots) + 8 * kSolverSlotWords + 64);
   a.gamma = gamma;
   a.tr_obj = objective;
   a.tr_res = residual;
@@ -544,6 +546,7 @@ extern "C" int mpmrb_qn_solve(mpmrb_ctx* c, const mpmrb_problem* pr,
   const char* force_ls = getenv("MPMRB_SOLVER_LS_CTAS");
   if (force_ls) a.force_ls_ctas = atoi(force_ls);
   a.debug = getenv("MPMRB_SOLVER_DEBUG") ? 1 : 0;
+  a.ls_mode = getenv("MPMRB_LS_MODE") ? atoi(getenv("MPMRB_LS_MODE")) : 0;
   rc = launch_qn_solve(*c, a, 0);
   if (rc) return rc;
   SolveOut h{};

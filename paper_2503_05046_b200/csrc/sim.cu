@@ -91,44 +91,43 @@ __global__ void k_contact_prepare(GridDev g, const double* __restrict__ x,
   gamma_lag[c] = K * fmax(0.0, vhat - vn);
 }
 
-struct SubstepStat {
-  int nb, n_act, nc, iters, converged, ls_evals, regularized, status;
-};
 
-// Reactions on bodies (coupling.py:58-66, 141-144) in a fixed order, plus the
-// per-substep statistics record.
-__global__ void __launch_bounds__(512) k_substep_end(
-    const int* __restrict__ counters /*nb, n_act, nc*/, const SolveOut* __restrict__ so,
-    const double* __restrict__ gamma, const double* __restrict__ frames,
-    const double* __restrict__ witness, const int* __restrict__ cbody,
-    const mpmrb_geom* __restrict__ geoms, int ngeom, int nbody, long long nc_cap,
-    double* __restrict__ accum, double* __restrict__ gamma_world, int* __restrict__ substep_idx,
-    SubstepStat* __restrict__ stats, int max_substeps, DevStatus* st) {
+// Reactions on bodies (coupling.py:58-66, 141-144), pass 1: gamma_world =
+// gamma^T R per contact and per-CTA partial sums of -gamma_world and
+// -arm x gamma_world per body (grid-stride over the device contact count).
+constexpr int kReactCtas = 148;
+constexpr int kReactThreads = 256;
+
+__global__ void __launch_bounds__(kReactThreads) k_reactions(
+    const int* __restrict__ counters /*nb, n_act, nc*/, const double* __restrict__ gamma,
+    const double* __restrict__ frames, const double* __restrict__ witness,
+    const int* __restrict__ cbody, const mpmrb_geom* __restrict__ geoms, int ngeom, int nbody,
+    long long nc_cap, double* __restrict__ gamma_world, double* __restrict__ partial) {
   __shared__ double red[32];
   __shared__ double body_pos[kMaxBodies][3];
-  int nc = min((long long)counters[2], nc_cap);
+  const long long nc = min((long long)counters[2], nc_cap);
   for (int gi = threadIdx.x; gi < ngeom; gi += blockDim.x) {
     int b = geoms[gi].body;
     if (b < kMaxBodies)
       for (int d = 0; d < 3; ++d) body_pos[b][d] = geoms[gi].body_pos[d];
   }
   __syncthreads();
-  // gamma_world = gamma^T R per contact
-  for (int c = threadIdx.x; c < nc; c += blockDim.x) {
-    const double* R = frames + 9 * c;
-    const double* gm = gamma + 3 * c;
-#pragma unroll
-    for (int j = 0; j < 3; ++j)
-      gamma_world[3 * c + j] = gm[0] * R[j] + gm[1] * R[3 + j] + gm[2] * R[6 + j];
-  }
-  __syncthreads();
-  for (int b = 0; b < nbody && b < kMaxBodies; ++b) {
+  const int nb = nbody < kMaxBodies ? nbody : kMaxBodies;
+  for (int b = 0; b < nb; ++b) {
     double acc[6] = {0, 0, 0, 0, 0, 0};
-    for (int c = threadIdx.x; c < nc; c += blockDim.x) {
+    for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < nc;
+         c += (long long)gridDim.x * blockDim.x) {
+      const double* R = frames + 9 * c;
+      const double* gm = gamma + 3 * c;
+      double gw[3];
+#pragma unroll
+      for (int j = 0; j < 3; ++j) gw[j] = gm[0] * R[j] + gm[1] * R[3 + j] + gm[2] * R[6 + j];
+      if (b == 0)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) gamma_world[3 * c + j] = gw[j];
       if (cbody[c] != b) continue;
-      double gw[3] = {gamma_world[3 * c], gamma_world[3 * c + 1], gamma_world[3 * c + 2]};
-      double arm[3] = {witness[3 * c] - body_pos[b][0], witness[3 * c + 1] - body_pos[b][1],
-                       witness[3 * c + 2] - body_pos[b][2]};
+      const double arm[3] = {witness[3 * c] - body_pos[b][0], witness[3 * c + 1] - body_pos[b][1],
+                             witness[3 * c + 2] - body_pos[b][2]};
       acc[0] += gw[0];
       acc[1] += gw[1];
       acc[2] += gw[2];
@@ -137,11 +136,34 @@ __global__ void __launch_bounds__(512) k_substep_end(
       acc[5] += arm[0] * gw[1] - arm[1] * gw[0];
     }
     for (int e = 0; e < 6; ++e) {
-      double s = block_sum<512>(acc[e], red);
-      if (threadIdx.x == 0) accum[6 * b + e] -= s;
+      const double s = block_sum<kReactThreads>(acc[e], red);
+      if (threadIdx.x == 0) partial[((long long)b * 6 + e) * kReactCtas + blockIdx.x] = s;
     }
   }
-  if (threadIdx.x == 0) {
+}
+
+struct SubstepStat {
+  int nb, n_act, nc, iters, converged, ls_evals, regularized, status;
+};
+
+// Pass 2 (one warp): accumulate the partials in CTA order into the step's
+// impulse accumulator, plus the per-substep statistics record.
+__global__ void k_substep_end(const int* __restrict__ counters, const SolveOut* __restrict__ so,
+                              const double* __restrict__ partial, int nbody,
+                              double* __restrict__ accum, int* __restrict__ substep_idx,
+                              SubstepStat* __restrict__ stats, int max_substeps, DevStatus* st) {
+  const int lane = threadIdx.x;
+  const int nb = nbody < kMaxBodies ? nbody : kMaxBodies;
+  const bool any = counters[2] > 0;
+  for (int q = 0; q < nb * 6; ++q) {
+    double x = 0.0;
+    if (any)
+      for (int k = lane; k < kReactCtas; k += 32) x += partial[(long long)q * kReactCtas + k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0) accum[q] -= x;
+  }
+  if (lane == 0) {
     int k = *substep_idx;
     if (k < max_substeps) {
       SubstepStat r;
@@ -156,6 +178,7 @@ __global__ void __launch_bounds__(512) k_substep_end(
       stats[k] = r;
     }
     *substep_idx = k + 1;
+    const int nc = counters[2];
     if (nc > 0 && so->status) raise_status(st, so->status, 60, k);
     if (nc > 0 && (so->status_flags & 1)) raise_status(st, MPMRB_E_NONFINITE, 61, k);
   }
@@ -385,6 +408,7 @@ int Sim::capture_or_launch() {
   a.force_ctas = force_ctas;
   a.force_ls_ctas = force_ls_ctas;
   a.debug = getenv("MPMRB_SOLVER_DEBUG") ? 1 : 0;
+  a.ls_mode = getenv("MPMRB_LS_MODE") ? atoi(getenv("MPMRB_LS_MODE")) : 0;
   a.v = b_sv.as<double>();
   a.dv = b_sdv.as<double>();
   a.vc = b_svc.as<double>();
@@ -395,6 +419,7 @@ int Sim::capture_or_launch() {
   a.cellsum = b_cellsum.as<double>();
   a.slots = b_slots.as<unsigned long long>();
   a.chan = reinterpret_cast<unsigned*>(b_slots.as<char>() + 8 * kSolverSlotWords);
+  a.bar = reinterpret_cast<unsigned*>(b_slots.as<char>() + 8 * kSolverSlotWords + 64);
   a.gamma = b_gamma.as<double>();
   a.out = b_solveout.as<SolveOut>();
   a.act = b_act.as<int>();
@@ -402,11 +427,14 @@ int Sim::capture_or_launch() {
   rc = launch_qn_solve(c, a, 0);
   if (rc) return rc;
   mark(5);
-  k_substep_end<<<1, 512, 0, c.stream>>>(
-      counters, b_solveout.as<SolveOut>(), b_gamma.as<double>(), ca.frames, ca.witness,
-      ca.body, b_geoms.as<mpmrb_geom>(), ngeom, nbody, nc_cap, b_accum.as<double>(),
-      b_gworld.as<double>(), counters + 3, b_stats.as<SubstepStat>(), max_substeps, c.status);
-  c.launches++;
+  k_reactions<<<kReactCtas, kReactThreads, 0, c.stream>>>(
+      counters, b_gamma.as<double>(), ca.frames, ca.witness, ca.body, b_geoms.as<mpmrb_geom>(),
+      ngeom, nbody, nc_cap, b_gworld.as<double>(), b_react.as<double>());
+  k_substep_end<<<1, 32, 0, c.stream>>>(counters, b_solveout.as<SolveOut>(),
+                                       b_react.as<double>(), nbody, b_accum.as<double>(),
+                                       counters + 3, b_stats.as<SubstepStat>(), max_substeps,
+                                       c.status);
+  c.launches += 2;
   mark(6);
   // 6. G2P (mpm.py:118-138)
   rc = launch_g2p(c, g, q, b_mats.as<mpmrb_material>(), nmat, b_vnext.as<double>(), dt_s,
@@ -454,12 +482,13 @@ int Sim::begin_step(long long epoch, int n_substeps) {
   if (b_counters.grow(64) || b_misc.grow(64) || b_solveout.grow(sizeof(SolveOut)) ||
       b_bar.grow(4096) || b_partials.grow(sizeof(double) * (2 * 8 * kMaxSolverCtas + 8)) ||
       b_dyn.grow(64) || b_accum.grow(sizeof(double) * 6 * kMaxBodies) ||
-      b_slots.grow(8 * kSolverSlotWords + 64))
+      b_react.grow(sizeof(double) * 6 * kMaxBodies * kReactCtas) ||
+      b_slots.grow(kSolverSyncBytes))
     return MPMRB_E_CUDA;
   if (!slots_init) {
     // slot tags start at 0 and channel tags at 1, so no stale slot matches
-    MPMRB_CUDA_OK(cudaMemsetAsync(b_slots.p, 0, 8 * kSolverSlotWords, c.stream));
-    unsigned ch[4] = {1u, 1u, 1u, 1u};
+    MPMRB_CUDA_OK(cudaMemsetAsync(b_slots.p, 0, kSolverSyncBytes, c.stream));
+    unsigned ch[4] = {1u, 1u, 1u, 0u};
     MPMRB_CUDA_OK(cudaMemcpyAsync(b_slots.as<char>() + 8 * kSolverSlotWords, ch, sizeof(ch),
                                   cudaMemcpyHostToDevice, c.stream));
     MPMRB_CUDA_OK(cudaStreamSynchronize(c.stream));

@@ -47,6 +47,7 @@ struct Sim {
   DevBuf b_su_c, b_su_n, b_su_ent, b_cellsum, b_slots;
   // sorted particle state: x, v (3n) f, c (9n) mass, vol0, plastic (n) doubles; mid (n) int64
   DevBuf b_qd, b_qmid, b_perm, b_skeys, b_svals, b_cpart_user;
+  DevBuf b_react;  // per-CTA reaction partials
   bool slots_init = false;
   DevBuf b_bias_stamp, b_bias_store;
 

@@ -59,6 +59,7 @@ constexpr int kLS = 6;            // contacts per line-search thread held in reg
 constexpr long long kSlotA = 0;                                  // [2][ctas][2]  gather (1 value)
 constexpr long long kSlotB = kSlotA + 2LL * kMaxSolverCtas * 2;  // [2][ctas][4]  group (2 values)
 constexpr long long kSlotC = kSlotB + 2LL * kMaxSolverCtas * 4;  // [2][4]        broadcast (2)
+constexpr long long kSlotL = kSlotC + 2LL * 4;                     // [2][4]        group leader sum
 
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
@@ -134,18 +135,54 @@ __device__ __forceinline__ void slot_poll_sum(const unsigned long long* slots, i
 }
 
 // ------------------------------------------------------------ grid reductions
+// Grid barrier: one acq_rel arrival atomic per CTA on a counter, the last
+// arriver resets it and releases a generation word that the others poll with
+// a short sleep between polls.  Polling a separate word with backoff keeps the
+// pollers off the counter's L2 slice: cg::this_grid().sync() spins every CTA
+// on the arrival word itself, which under load delayed the release by ~10 us
+// (tools/solver_scaling.py per-CTA timeline).
+__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 struct Sync {
   double* partials;  // [2][kMaxRed][kMaxSolverCtas]
   int nctas;
   unsigned long long* prof;  // CTA 0 / thread 0 only: [10] time inside grid syncs
+  unsigned long long* cta_in_sync;  // thread 0 of each CTA (profiling only)
+  unsigned* bar;     // [0] arrival count, [32] generation (separate 128 B lines)
+  unsigned* gen;     // this CTA's view of the generation (thread 0)
   __device__ __forceinline__ void operator()() const {
     if (nctas == 1) {
       __syncthreads();
       return;
     }
-    unsigned long long t0 = prof ? gtime() : 0ull;
-    cg::this_grid().sync();
+    unsigned long long t0 = (prof || cta_in_sync) ? gtime() : 0ull;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const unsigned target = *gen + 1u;
+      const unsigned old = atom_add_acq_rel(bar, 1u);
+      if (old == (unsigned)nctas - 1u) {
+        atomicExch(bar, 0u);
+        st_release_u32(bar + 32, target);
+      } else {
+        while (ld_acquire_u32(bar + 32) != target) __nanosleep(64);
+      }
+      *gen = target;
+    }
+    __syncthreads();
     if (prof) atomicAdd(prof + 10, gtime() - t0);
+    if (cta_in_sync) *cta_in_sync += gtime() - t0;
   }
 };
 
@@ -226,7 +263,7 @@ __device__ void reduce_all(const Sync& sync, int& parity, double (&v)[K], double
 // channel B slots; G == 1 is a plain block reduction.
 template <int K>
 __device__ void group_reduce(int G, unsigned long long* slots, unsigned& tag, double (&v)[K],
-                             double (&out)[K], double* sm) {
+                             double (&out)[K], double* sm, int mode = 0) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double bs[K];
   block_reduce<K>(v, sm, bs);
@@ -239,7 +276,20 @@ __device__ void group_reduce(int G, unsigned long long* slots, unsigned& tag, do
       unsigned long long* base = slots + kSlotB + (long long)(tag & 1u) * kMaxSolverCtas * 4;
       if (lane == 0) slot_publish<K>(base + (long long)blockIdx.x * 2 * K, bs, tag);
       double r[K];
-      slot_poll_sum<K, 2>(base, G, tag, r);
+      if (mode == 2) {
+        // leader tree: CTA 0 sums the G slots and republishes the total
+        unsigned long long* lead = slots + kSlotL + (long long)(tag & 1u) * 4;
+        if (blockIdx.x == 0) {
+          slot_poll_sum<K, 2>(base, G, tag, r);
+          if (lane == 0) slot_publish<K>(lead, r, tag);
+        } else {
+          slot_poll_sum<K, 1>(lead, 1, tag, r);
+        }
+      } else if (mode == 1) {
+        slot_poll_sum<K, 2, 32>(base, G, tag, r);
+      } else {
+        slot_poll_sum<K, 2>(base, G, tag, r);
+      }
       if (lane == 0)
 #pragma unroll
         for (int k = 0; k < K; ++k) sm[32 * kMaxRed + k] = r[k];
@@ -598,7 +648,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
   if (nctas > 1 && CL > 1) {
     G = CL;  // the line-search group is cluster 0 (DSMEM reductions)
   } else if (nctas > 1) {
-    G = (a.force_ls_ctas > 0) ? a.force_ls_ctas : (nc + kThreads * kLS - 1) / (kThreads * kLS);
+    // ~4 contacts per thread (measured optimum between per-evaluation compute
+    // and the all-to-all reduction latency, which grows with the group)
+    G = (a.force_ls_ctas > 0) ? a.force_ls_ctas : (nc + kThreads * 4 - 1) / (kThreads * 4);
     if (G < 1) G = 1;
     if (G > nctas) G = nctas;
     if (G > 64) G = 64;  // slot_poll_sum<.., 2> polls at most 64 slots
@@ -609,8 +661,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
   const int n_fn = nd - n_cn;
   (void)ng;
   unsigned tagA = a.chan[0], tagB = a.chan[1], tagC = a.chan[2];
+  unsigned long long in_sync_acc = 0;
+  unsigned bar_gen = a.chan[3];  // generation word persists across solves
   Sync sync{a.partials, nctas,
-            (a.prof && blockIdx.x == 0 && threadIdx.x == 0) ? a.prof : nullptr};
+            (a.prof && blockIdx.x == 0 && threadIdx.x == 0) ? a.prof : nullptr,
+            (a.prof && threadIdx.x == 0) ? &in_sync_acc : nullptr, a.bar, &bar_gen};
   int parity = 0;
   const long long tid = (long long)blockIdx.x * kThreads + threadIdx.x;
   const long long nthr = (long long)nctas * kThreads;
@@ -618,7 +673,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
   const double inv_eps = 1.0 / a.eps_v;
   const bool prof = a.prof && blockIdx.x == 0 && threadIdx.x == 0;
   const bool cprof = a.prof && threadIdx.x == 0;  // per-CTA phase work times
-  unsigned long long cta_t0 = 0, cta_acc[3] = {0, 0, 0};
+  unsigned long long cta_t0 = 0, cta_acc[5] = {0, 0, 0, 0, 0};
   auto cta_start = [&]() {
     if (cprof) cta_t0 = gtime();
   };
@@ -692,6 +747,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
     double red[8] = {0, 0, 0, 0, e_acc, 0, 0, 0};
     int reg_count = 0;
     cta_start();
+    const unsigned long long cta_t0_n = (a.debug && it == 5 && threadIdx.x == 0) ? gtime() : 0ull;
     if (it > 0) P *= (1.0 - alpha_prev);
     {
       // 4 lanes per contact node (8 nodes per warp), warp-interleaved over CTAs
@@ -753,9 +809,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
       red[6] += p2s;
     }
     if (reg_count) atomicAdd(&a.out->regularized, reg_count);
+    unsigned long long tdbg0 = (a.debug && it == 5 && threadIdx.x == 0) ? gtime() : 0ull;
     cta_stop(0);
+    unsigned long long tdbg1 = (a.debug && it == 5 && threadIdx.x == 0) ? gtime() : 0ull;
+    cta_start();
     double s[8];
     reduce_all<8>(sync, parity, red, s, sm);
+    cta_stop(3);
+    if (a.debug && it == 5 && threadIdx.x == 0)
+      printf("NDBG cta %d nstart %llu warp0_end %llu cta_end %llu reduce_end %llu\n", blockIdx.x,
+             cta_t0_n, tdbg0, tdbg1, gtime());
     lap(1);
     const double residual = sqrt(s[0]);
     const double threshold = a.eps_a + a.eps_r * fmax(sqrt(s[1]), sqrt(s[2]));
@@ -889,7 +952,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
           double ss[2];
           unsigned long long tls1 = prof ? gtime() : 0ull;
           if (CL > 1) cluster_reduce<2>(CL, s_cl, cpar, rr, ss, sm);
-          else group_reduce<2>(G, a.slots, tagB, rr, ss, sm);
+          else group_reduce<2>(G, a.slots, tagB, rr, ss, sm, a.ls_mode);
           if (prof) {
             unsigned long long tls2 = gtime();
             pt[12] += tls1 - tls0;
@@ -995,7 +1058,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
   __syncthreads();
   if (s_flag && threadIdx.x == 0) atomicOr(&a.out->status_flags, 1);
   if (cprof)
-    for (int ph = 0; ph < 3; ++ph) a.prof[kSolverProf + ph * 160 + blockIdx.x] += cta_acc[ph];
+    for (int ph = 0; ph < 4; ++ph) a.prof[kSolverProf + ph * 160 + blockIdx.x] += cta_acc[ph];
+  if (cprof) a.prof[kSolverProf + 4 * 160 + blockIdx.x] += in_sync_acc;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     a.out->converged = converged ? 1 : 0;
     a.out->iterations = iterations;
@@ -1006,6 +1070,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
     a.chan[0] = tagA;
     a.chan[1] = tagB;
     a.chan[2] = tagC;
+    if (nctas > 1) a.chan[3] = bar_gen;
     if (prof) {
       lap(5);
       for (int k = 0; k < 6; ++k) a.prof[k] += pt[k];

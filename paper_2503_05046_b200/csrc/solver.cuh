@@ -9,7 +9,7 @@ constexpr int kSolverThreads = 256;
 constexpr int kMaxSolverCtas = 160;
 constexpr int kSolverProf = 16;  // phase timers (ns), see solver.cu
 // + per-CTA work time (ns) of the N, D and U phases: [16 + phase*kMaxSolverCtas + cta]
-constexpr int kSolverProfWords = 16 + 3 * 160;
+constexpr int kSolverProfWords = 16 + 5 * 160;
 constexpr int kCellSumStride = 10;  // 9 channels (J^T g: 3, R^T G R: 6) padded to 80 B
 
 struct SolveOut {
@@ -75,6 +75,7 @@ struct SolverArgs {
   int force_ctas;  // 0 = automatic
   int force_ls_ctas;  // 0 = automatic
   int debug;          // MPMRB_SOLVER_DEBUG: printf a phase timeline of iteration 5
+  int ls_mode;        // line-search group reduction: 0 all-to-all, 1 + backoff, 2 leader
   // work (device)
   double* v;         // (nd,3) solution (contact nodes during the solve, all at the end)
   double* dv;        // (nd,3)
@@ -85,7 +86,8 @@ struct SolverArgs {
   double* cellsum;   // (27 nc_cap, kCellSumStride) per (group, slot) sums
   double* partials;  // [2][8][kMaxSolverCtas] grid reductions
   unsigned long long* slots;  // self-validating reduction slots (see solver.cu)
-  unsigned* chan;    // [4] channel tags carried across solves
+  unsigned* chan;    // [4] channel tags carried across solves ([3]: barrier generation)
+  unsigned* bar;     // grid barrier words: [0] count, [32] generation (zeroed once)
   // outputs
   double* gamma;
   double* tr_obj;
@@ -100,7 +102,9 @@ struct SolverArgs {
 };
 
 // words of the self-validating slot area (solver.cu)
-constexpr long long kSolverSlotWords = 2LL * kMaxSolverCtas * 2 + 2LL * kMaxSolverCtas * 4 + 2 * 4;
+constexpr long long kSolverSlotWords = 2LL * kMaxSolverCtas * 2 + 2LL * kMaxSolverCtas * 4 + 2 * 4 + 2 * 4;
+// the slot buffer is followed by chan[4] (64 B) and the barrier words (256 B)
+constexpr long long kSolverSyncBytes = 8 * kSolverSlotWords + 64 + 256;
 
 // Build groups + node adjacency from cnodes/cw.
 int launch_solver_setup(Ctx& c, const int* nd_dev, const int* nc_dev, long long nd_cap,

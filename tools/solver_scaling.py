@@ -49,6 +49,16 @@ def build_problem(steps=16, hx=0.2):
     con.gamma_lag = normal_impulse(vcs[:, 2], con.phi, st.contact_params, dt_s)
     prob, act = mp.build_contact_problem(grid, stencil, con, st.contact_params, dt_s, plan, 0)
     print(f"n={p.n} contacts={prob.n_contacts} active nodes={prob.m.shape[0]}", flush=True)
+    import numpy as np
+    nodes = prob.nodes.cpu().numpy() if hasattr(prob.nodes, "cpu") else np.asarray(prob.nodes)
+    same = np.all(nodes[1:] == nodes[:-1], axis=1)
+    runs = 1 + int((~same).sum())
+    pc = con.particle.cpu().numpy() if hasattr(con.particle, "cpu") else np.asarray(con.particle)
+    xc = p.x.cpu().numpy()[pc]
+    cc = np.floor(xc / st.h - 0.5).astype(np.int64)
+    samec = np.all(cc[1:] == cc[:-1], axis=1)
+    print(f"   stencil runs={runs} base-cell runs={1 + int((~samec).sum())} "
+          f"distinct cells={len(np.unique(cc, axis=0))}", flush=True)
     return prob
 
 
@@ -82,14 +92,14 @@ def main():
             ts.append(time.perf_counter() - t0)
         print("   solve ms:", " ".join(f"{1e3 * t:.2f}" for t in ts), flush=True)
         dt = sum(ts) / reps
-        ctap = (C.c_uint64 * 480)()
+        ctap = (C.c_uint64 * 800)()
         _lib.lib().mpmrb_solver_profile_cta(_lib.ctx(), ctap)
         _lib.lib().mpmrb_solver_profile(_lib.ctx(), prof, 1)
         it = max(1, rep.iterations) * reps
         import numpy as np
-        cp = np.frombuffer(ctap, dtype=np.uint64).reshape(3, 160).astype(float) / 1e3 / it
+        cp = np.frombuffer(ctap, dtype=np.uint64).reshape(5, 160).astype(float) / 1e3 / it
         ncta = int(prof[8] & 0xffffffff)
-        for ph, name in enumerate("NDU"):
+        for ph, name in enumerate(["N", "D", "U", "N-reduce", "in-grid-sync (all)"]):
             v = cp[ph, :ncta]
             print(f"   per-CTA {name} work us/iter: mean {v.mean():.2f} max {v.max():.2f} "
                   f"(cta {int(v.argmax())}) min {v.min():.2f}", flush=True)
