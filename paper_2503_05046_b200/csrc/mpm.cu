@@ -152,7 +152,11 @@ __global__ void __launch_bounds__(kP2GThreads, 4) k_p2g(GridDev g, ParticlesDev 
   }
   const int cx = hi[0] - lo[0] + 1, cy = hi[1] - lo[1] + 1, cz = hi[2] - lo[2] + 1;
   const int nx = cx + 2, ny = cy + 2, nz = cz + 2;
-  if ((long long)nx * ny * nz > kWarpTile) {
+  // tiled path: <= kWarpTile nodes and <= 2 blocks per axis (flush lookup)
+  const bool spans2 = (((lo[0] + nx - 1) >> 2) - (lo[0] >> 2) <= 1) &&
+                      (((lo[1] + ny - 1) >> 2) - (lo[1] >> 2) <= 1) &&
+                      (((lo[2] + nz - 1) >> 2) - (lo[2] >> 2) <= 1);
+  if ((long long)nx * ny * nz > kWarpTile || !spans2) {
     // spread warp: per-particle scatter with global atomics
     if (live) {
       Stencil1 s;
@@ -264,8 +268,24 @@ __global__ void __launch_bounds__(kP2GThreads, 4) k_p2g(GridDev g, ParticlesDev 
     }
     __syncwarp();
   }
-  // 5. flush: one atomic per (node, channel)
-  for (int q = lane; q < nnode; q += 32) {
+  // 5. flush: one atomic per (node, channel).  The tile spans at most 2
+  // blocks per axis (<= 8 blocks, nodes <= 10 per axis): lanes 0-7 resolve
+  // one block each through the hash table, the others read them by shuffle.
+  const int blo0 = lo[0] >> 2, blo1 = lo[1] >> 2, blo2 = lo[2] >> 2;
+  int myblk = -1;
+  if (lane < 8) {
+    int64_t bkey;
+    if (pack_block(blo0 + ((lane >> 2) & 1), blo1 + ((lane >> 1) & 1), blo2 + (lane & 1), &bkey))
+      myblk = hash_find(g.hkeys, g.hvals, g.mask, (uint64_t)bkey);
+  }
+  for (int q0 = 0; q0 < nnode; q0 += 32) {
+    const int q = q0 + lane;
+    const bool inb = q < nnode;
+    const int qz = inb ? q % nz : 0, qy = inb ? (q / nz) % ny : 0, qx = inb ? q / (nz * ny) : 0;
+    const int gx = lo[0] + qx, gy = lo[1] + qy, gz = lo[2] + qz;
+    const int bsel = (((gx >> 2) - blo0) << 2) | (((gy >> 2) - blo1) << 1) | ((gz >> 2) - blo2);
+    const int blk = __shfl_sync(0xffffffffu, myblk, bsel & 7);
+    if (!inb) continue;
     double v[7];
     bool any = false;
 #pragma unroll
@@ -274,12 +294,6 @@ __global__ void __launch_bounds__(kP2GThreads, 4) k_p2g(GridDev g, ParticlesDev 
       any |= v[ch] != 0.0;
     }
     if (!any) continue;
-    const int qz = q % nz, qy = (q / nz) % ny, qx = q / (nz * ny);
-    const int gx = lo[0] + qx, gy = lo[1] + qy, gz = lo[2] + qz;
-    int64_t bkey;
-    int blk = -1;
-    if (pack_block(gx >> 2, gy >> 2, gz >> 2, &bkey))
-      blk = hash_find(g.hkeys, g.hvals, g.mask, (uint64_t)bkey);
     if (blk < 0) {
       raise_status(st, MPMRB_E_ALLOCATION, 22, w0);
       continue;

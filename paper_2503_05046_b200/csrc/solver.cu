@@ -52,6 +52,7 @@ namespace {
 constexpr int kThreads = kSolverThreads;
 constexpr int kChunk = 32;        // contacts per ownership chunk: one warp, one contact per lane
 constexpr int kWarps = kThreads / 32;
+constexpr int kSwStride = 33;  // staged weights sw[k * 33 + lane]: rows padded (bank conflicts)
 constexpr int kMaxRed = 8;        // reduction lanes per grid reduce
 constexpr int kLS = 6;            // contacts per line-search thread held in registers
 
@@ -339,7 +340,7 @@ __device__ __forceinline__ void load_frame(const double* fr, long long c, double
 // All 27 node indices are loaded first and the value loads carry no branch,
 // so the whole gather costs two dependent memory round trips (a branch on each
 // loaded index serialised 27 of them).  Weights come from global memory
-// (slot-major) or, when staged, from shared memory sw[k * 32 + lane].
+// (slot-major) or, when staged, from shared memory sw[k * kSwStride + lane].
 // u is written by other CTAs earlier in this kernel (ordered by a grid sync,
 // which also invalidates L1): plain coherent loads, no __restrict__ (that would
 // allow the non-coherent path) and no volatile asm (__ldcg would pin the loads
@@ -368,7 +369,7 @@ __device__ __forceinline__ void gather_contact_t(const SolverArgs& a, long long 
 #pragma unroll
     for (int q = 0; q < 9; ++q) {
       const int k = 9 * b + q;
-      const double w = kStaged ? sw[k * 32 + lane] : __ldg(&a.cw[(long long)k * a.nc_cap + c]);
+      const double w = kStaged ? sw[k * kSwStride + lane] : __ldg(&a.cw[(long long)k * a.nc_cap + c]);
       if (nd[k] >= 0) {
         up[0] += w * x[q];
         up[1] += w * y[q];
@@ -391,7 +392,7 @@ __device__ __forceinline__ void gather_contact_sw(const SolverArgs& a, long long
 }
 
 // Stage the 27 stencil weights of the warp's chunk [c0, c0 + 32) into
-// sw[k * 32 + lane] (slot-major loads, coalesced, all in flight at once).
+// sw[k * kSwStride + lane] (slot-major loads, coalesced, all in flight at once).
 __device__ __forceinline__ void stage_weights(const SolverArgs& a, long long c0, int nc,
                                               double* sw) {
   const int lane = threadIdx.x & 31;
@@ -400,7 +401,7 @@ __device__ __forceinline__ void stage_weights(const SolverArgs& a, long long c0,
 #pragma unroll
   for (int k = 0; k < 27; ++k) w[k] = (c < nc) ? __ldg(&a.cw[(long long)k * a.nc_cap + c]) : 0.0;
 #pragma unroll
-  for (int k = 0; k < 27; ++k) sw[k * 32 + lane] = w[k];
+  for (int k = 0; k < 27; ++k) sw[k * kSwStride + lane] = w[k];
   __syncwarp();
 }
 
@@ -559,9 +560,12 @@ __device__ __forceinline__ void node_finish(const SolverArgs& a, long long i, co
 __device__ __forceinline__ void contact_update_chunk(const SolverArgs& a, const ContactModel& cm,
                                                      long long c0, int nc, bool init,
                                                      double alpha, double* s_gw,
-                                                     const double* s_w, double& e_acc) {
+                                                     const double* s_w, double& e_acc,
+                                                     bool dbg = false) {
   const int lane = threadIdx.x & 31;
   const long long c = c0 + lane;
+  unsigned long long tu[5] = {0, 0, 0, 0, 0};
+  if (dbg) tu[0] = gtime();
   if (c < nc) {
     double R[9], vc[3], gw[3], rgr[6], vhat, mug;
     load_frame(a.frames, c, R);
@@ -581,7 +585,9 @@ __device__ __forceinline__ void contact_update_chunk(const SolverArgs& a, const 
     }
 #pragma unroll
     for (int d = 0; d < 3; ++d) a.vc[3 * c + d] = vc[d];
+    if (dbg) tu[1] = gtime() + (vc[0] == 12345.0);
     e_acc += contact_terms(cm, vc, vhat, mug, R, gw, rgr);
+    if (dbg) tu[2] = gtime() + (gw[0] == 12345.0);
     double* sg = s_gw + 9 * lane;
 #pragma unroll
     for (int d = 0; d < 3; ++d) sg[d] = gw[d];
@@ -591,13 +597,22 @@ __device__ __forceinline__ void contact_update_chunk(const SolverArgs& a, const 
   __syncwarp();
   const long long c_last = (c0 + kChunk < nc ? c0 + kChunk : nc) - 1;
   const int g0 = a.su.grp_of[c0], g1 = a.su.grp_of[c_last];
-  const int pairs = (g1 - g0 + 1) * 27;
-  for (int p = lane; p < pairs; p += 32) {
-    const int g = g0 + p / 27, k = p - (p / 27) * 27;
-    const int cs = a.su.grp_start[g], ce = a.su.grp_start[g + 1];
+  const int ngc = g1 - g0 + 1;  // <= 32 groups in a chunk
+  const int pairs = ngc * 27;
+  // group bounds of the chunk, one group per lane (one load round trip)
+  const int my_gs = (lane <= ngc) ? a.su.grp_start[g0 + lane] : 0;
+  const int gs_32 = (ngc == 32) ? a.su.grp_start[g0 + 32] : 0;
+  for (int p0 = 0; p0 < pairs; p0 += 32) {
+    const int p = p0 + lane;
+    const int gl = p < pairs ? p / 27 : 0, k = p - gl * 27;
+    const int g = g0 + gl;
+    const int cs = __shfl_sync(0xffffffffu, my_gs, gl);
+    const int ce_sh = __shfl_sync(0xffffffffu, my_gs, (gl + 1) & 31);
+    const int ce = (gl + 1 < 32) ? ce_sh : gs_32;
+    if (p >= pairs) continue;
     double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
     for (int cc = cs; cc < ce; ++cc) {
-      const double w = s_w[k * 32 + (cc - c0)];
+      const double w = s_w[k * kSwStride + (cc - c0)];
       const double w2 = w * w;
       const double* sg = s_gw + 9 * (cc - c0);
 #pragma unroll
@@ -613,6 +628,11 @@ __device__ __forceinline__ void contact_update_chunk(const SolverArgs& a, const 
     out[4] = make_double2(acc[8], 0.0);
   }
   __syncwarp();
+  if (dbg) {
+    tu[3] = gtime();
+    printf("U timeline (ns): loads %llu terms %llu pairs %llu (pairs=%d)\n", tu[1] - tu[0],
+           tu[2] - tu[1], tu[3] - tu[2], pairs);
+  }
 }
 
 __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
@@ -699,7 +719,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
   const long long chunk0 = ((long long)wid * nctas + blockIdx.x) * kChunk;
   const long long chunk_step = (long long)nctas * kThreads;
   double* s_gw_w = s_gw + wid * (kChunk * 9);
-  double* s_w_w = s_dyn + wid * (27 * kChunk);
+  double* s_w_w = s_dyn + wid * (27 * kSwStride);
   // every warp owns at most one chunk: its weights stay staged for the solve
   const bool resident = (long long)nc <= (long long)nctas * kThreads;
 
@@ -775,21 +795,33 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
           }
         }
         double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-#pragma unroll 2
-        for (int e = rec.y + gl; e < rec.z; e += 4) {
-          const int key = __ldg(&a.su.ent[e]);
-          const double2* src = reinterpret_cast<const double2*>(
-              a.cellsum + ((long long)(key >> 5) * 27 + (key & 31)) * kCellSumStride);
-          const double2 q0 = src[0], q1 = src[1], q2 = src[2], q3 = src[3], q4 = src[4];
-          acc[0] += q0.x;
-          acc[1] += q0.y;
-          acc[2] += q1.x;
-          acc[3] += q1.y;
-          acc[4] += q2.x;
-          acc[5] += q2.y;
-          acc[6] += q3.x;
-          acc[7] += q3.y;
-          acc[8] += q4.x;
+        // up to 4 entries per lane per pass: all keys, then all records, in flight
+        for (int eb = rec.y + gl; eb < rec.z; eb += 16) {
+          int key[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) key[j] = (eb + 4 * j < rec.z) ? __ldg(&a.su.ent[eb + 4 * j]) : -1;
+          double2 q[4][5];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const double2* src = reinterpret_cast<const double2*>(
+                a.cellsum + ((long long)((key[j] < 0 ? 0 : key[j]) >> 5) * 27 + (key[j] & 31)) *
+                                kCellSumStride);
+#pragma unroll
+            for (int r = 0; r < 5; ++r) q[j][r] = src[r];
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            if (key[j] < 0) continue;
+            acc[0] += q[j][0].x;
+            acc[1] += q[j][0].y;
+            acc[2] += q[j][1].x;
+            acc[3] += q[j][1].y;
+            acc[4] += q[j][2].x;
+            acc[5] += q[j][2].y;
+            acc[6] += q[j][3].x;
+            acc[7] += q[j][3].y;
+            acc[8] += q[j][4].x;
+          }
         }
 #pragma unroll
         for (int q = 0; q < 9; ++q)
@@ -1009,7 +1041,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
     for (long long c0 = chunk0; c0 < nc; c0 += chunk_step)
     {
       if (!resident) stage_weights(a, c0, nc, s_w_w);
-      contact_update_chunk(a, cm, c0, nc, false, alpha_final, s_gw_w, s_w_w, e_acc);
+      contact_update_chunk(a, cm, c0, nc, false, alpha_final, s_gw_w, s_w_w, e_acc,
+                           a.debug && it == 5 && blockIdx.x == 0 && threadIdx.x == 0);
     }
     lap(8);
     cta_stop(2);
@@ -1265,7 +1298,7 @@ int launch_qn_solve(Ctx& c, const SolverArgs& a, int grid_ctas) {
       q.attrs = qa;
       q.numAttrs = 1;
       int ncl = 0;
-      q.dynamicSmemBytes = sizeof(double) * kWarps * 27 * kChunk;
+      q.dynamicSmemBytes = sizeof(double) * kWarps * 27 * kSwStride;
       cudaFuncSetAttribute(k_qn_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)q.dynamicSmemBytes);
       cudaError_t qe = cudaOccupancyMaxActiveClusters(&ncl, k_qn_solve, &q);
@@ -1300,7 +1333,7 @@ int launch_qn_solve(Ctx& c, const SolverArgs& a, int grid_ctas) {
   cfg.gridDim = dim3((unsigned)g);
   cfg.blockDim = dim3(kThreads);
   static bool smem_set = false;
-  const int dyn = (int)(sizeof(double) * kWarps * 27 * kChunk);
+  const int dyn = (int)(sizeof(double) * kWarps * 27 * kSwStride);
   if (!smem_set) {
     MPMRB_CUDA_OK(cudaFuncSetAttribute(k_qn_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
     smem_set = true;
