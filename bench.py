@@ -57,43 +57,19 @@ def parse():
 
 def workload_scene(name: str, rank: int = 0) -> dict:
     from paper_2503_05046_b200 import scenes
+    from paper_2503_05046_b200.distributed import env_scene
     if name == "sand":
         sc = scenes.sand_pile_scene()
     elif name == "sand1m":
         sc = scenes.sand_pile_scene(half=(0.4, 0.4, 0.1))
     else:
         sc = scenes.elastic_cube_scene()
-    for v in sc["volumes"]:
-        v["seed"] = v["seed"] + 1000 * rank  # independent environment per rank
-    return sc
+    return env_scene(sc, rank)  # independent environment per rank
 
 
 def host_particles(scene: dict):
-    """Seed the scene's particles on the host (same lattice as seed_box)."""
-    from paper_2503_05046_b200.particles import _jittered_lattice
-    out = {k: [] for k in ("x", "v", "mass", "vol", "mid")}
-    h = scene["h"]
-    for v in scene["volumes"]:
-        m = scene["materials"][v["material"]]
-        c, half = np.asarray(v["center"], float), np.asarray(v["half"], float)
-        rng = np.random.default_rng(v["seed"])
-        lo = np.floor((c - half) / h).astype(np.int64)
-        hi = np.ceil((c + half) / h).astype(np.int64)
-        per_axis = max(1, round(v["ppc"] ** (1.0 / 3.0)))
-        pts = _jittered_lattice(lo, hi, h, per_axis, v["jitter"], rng)
-        pts = pts[np.all(np.abs(pts - c) <= half, axis=1)]
-        n = pts.shape[0]
-        vol = 8.0 * half.prod() / n
-        out["x"].append(pts)
-        out["v"].append(np.tile(np.asarray(v["velocity"], float), (n, 1)))
-        out["mass"].append(np.full(n, m["rho"] * vol))
-        out["vol"].append(np.full(n, vol))
-        out["mid"].append(np.full(n, v["material"], dtype=np.int64))
-    arr = {k: np.concatenate(val) for k, val in out.items()}
-    n = arr["x"].shape[0]
-    arr["f"] = np.tile(np.eye(3), (n, 1, 1))
-    arr["c"] = np.zeros((n, 3, 3))
-    return arr
+    from paper_2503_05046_b200.scenes import host_particles as hp
+    return hp(scene)
 
 
 def peaks():
@@ -235,13 +211,12 @@ def run_ours(args):
 
     import paper_2503_05046_b200 as mp
     from paper_2503_05046_b200 import _lib, scenes
+    from paper_2503_05046_b200 import distributed as D
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    info = D.rank_info()
+    world, rank, local = info.world, info.rank, info.local_rank
     torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    D.init("nccl")
     scene = workload_scene(args.workload, rank)
     state = scenes.build_state(scene)
     n = state.particles.n
@@ -271,10 +246,7 @@ def run_ours(args):
     stream = state._stream
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
+    barrier = D.barrier
 
     # ---- timed region: K steps, L2 flushed between steps (outside timing)
     clocks = ClockSampler(local)
@@ -299,12 +271,10 @@ def run_ours(args):
     barrier()
     clk = clocks.stop()
     launches = _lib.launch_count() - launches0
-    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.item())
+    total_ms = D.max_over_ranks(total_ms)  # device time of the job: slowest rank
     ms_per_step = total_ms / args.steps
-    value = world * n * N * args.steps / (total_ms * 1e-3)
+    n_all = int(D.sum_over_ranks(n))       # every rank runs its own environment
+    value = D.job_throughput(n_all * N * args.steps, total_ms * 1e-3)
 
     # ---- live per-stage timing (one profiled substep, direct launches), taken
     # in the middle of the timed window's regime: restore, advance half the
@@ -370,11 +340,9 @@ def run_ours(args):
             b.record(cur)
             b.synchronize()
             e_ms += a.elapsed_time(b)
-        te = torch.tensor([e_ms], dtype=torch.float64, device="cuda")
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e_ms = float(te.item())
-        e2e = dict(value=world * n * N * ke / (e_ms * 1e-3), unit=UNIT, h2d_bytes_per_step=h2d,
+        e_ms = D.max_over_ranks(e_ms)
+        e2e = dict(value=D.job_throughput(n_all * N * ke, e_ms * 1e-3), unit=UNIT,
+                   h2d_bytes_per_step=h2d,
                    d2h_bytes_per_step=d2h, steps=ke, ms_per_step=e_ms / ke)
 
     cpu = None
@@ -399,8 +367,7 @@ def run_ours(args):
             roofline=roofline, cpu_baseline=cpu, e2e=e2e, gpu_launches=int(launches),
             clocks=clk)
         print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    D.shutdown()
     return 0
 
 

@@ -150,6 +150,37 @@ def sand_pile_scene(half=(0.2, 0.2, 0.1), h=0.01, model="sand") -> dict:
                                          position=[0, 0, 0], quat=[1, 0, 0, 0], mu=0.5)])])
 
 
+def host_particles(scene: dict) -> dict:
+    """Seed the scene's particle volumes on the HOST as NumPy arrays (the same
+    jittered lattice as seed_box, particles.py:113-136): x, v, f, c, mass, vol,
+    mid.  Used by bench.py (pinned host buffers, CPU baseline) and the
+    multi-process tests; no device work."""
+    from .particles import _jittered_lattice
+    out = {k: [] for k in ("x", "v", "mass", "vol", "mid")}
+    h = scene["h"]
+    for v in scene["volumes"]:
+        m = scene["materials"][v["material"]]
+        c, half = np.asarray(v["center"], float), np.asarray(v["half"], float)
+        rng = np.random.default_rng(v["seed"])
+        lo = np.floor((c - half) / h).astype(np.int64)
+        hi = np.ceil((c + half) / h).astype(np.int64)
+        per_axis = max(1, round(v["ppc"] ** (1.0 / 3.0)))
+        pts = _jittered_lattice(lo, hi, h, per_axis, v["jitter"], rng)
+        pts = pts[np.all(np.abs(pts - c) <= half, axis=1)]
+        n = pts.shape[0]
+        vol = 8.0 * half.prod() / n
+        out["x"].append(pts)
+        out["v"].append(np.tile(np.asarray(v["velocity"], float), (n, 1)))
+        out["mass"].append(np.full(n, m["rho"] * vol))
+        out["vol"].append(np.full(n, vol))
+        out["mid"].append(np.full(n, v["material"], dtype=np.int64))
+    arr = {k: np.concatenate(val) for k, val in out.items()}
+    n = arr["x"].shape[0]
+    arr["f"] = np.tile(np.eye(3), (n, 1, 1))
+    arr["c"] = np.zeros((n, 3, 3))
+    return arr
+
+
 def scaled(scene: dict, **kw) -> dict:
     s = copy.deepcopy(scene)
     s.update(kw)
