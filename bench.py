@@ -49,7 +49,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["sand", "sand1m", "cube"], default="sand")
+    ap.add_argument("--workload", choices=["sand", "sand1m", "cube", "cloth", "tshirt"],
+                    default="sand")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -62,9 +63,26 @@ def workload_scene(name: str, rank: int = 0) -> dict:
         sc = scenes.sand_pile_scene()
     elif name == "sand1m":
         sc = scenes.sand_pile_scene(half=(0.4, 0.4, 0.1))
+    elif name == "cloth":
+        sc = scenes.cloth_sheet_scene()
+    elif name == "tshirt":
+        sc = scenes.tshirt_fold_scene()
     else:
         sc = scenes.elastic_cube_scene()
     return env_scene(sc, rank)  # independent environment per rank
+
+
+def workload_name(name: str, n: int, N: int) -> str:
+    return {
+        "sand": f"sand pile (configs[1]): {n} particles/GPU, Drucker-Prager sand, floor + "
+                f"kinematic pusher box, dt=2e-3, N={N} substeps",
+        "sand1m": f"sand pile 1M (north-star target scene): {n} particles/GPU, Drucker-Prager "
+                  f"sand, floor + kinematic pusher box, dt=2e-3, N={N} substeps",
+        "cube": f"elastic cube (configs[0]): {n} particles, dt=1e-3, N={N}",
+        "cloth": f"cloth sheet over a sphere (configs[2]): {n} particles (vertices + faces), "
+                 f"codimensional cloth, dt=2e-3, N={N}",
+        "tshirt": f"cloth fold with two grippers (configs[3]): {n} particles, dt=2e-3, N={N}",
+    }[name]
 
 
 def host_particles(scene: dict):
@@ -229,11 +247,14 @@ def run_ours(args):
     import copy
     p_keys = ("x", "v", "f", "c", "plastic")
     snap = {k: getattr(state.particles, k).clone() for k in p_keys}
+    d3_0 = state.cloth.d3.clone() if state.cloth is not None else None
     bodies0 = copy.deepcopy(state.bodies)
 
     def restore():
         for k in p_keys:
             getattr(state.particles, k).copy_(snap[k])
+        if d3_0 is not None:
+            state.cloth.d3.copy_(d3_0)
         state.bodies = copy.deepcopy(bodies0)
         state.time = 0.0
         state.step_index = 0
@@ -355,10 +376,7 @@ def run_ours(args):
             metric=METRIC, value=value, unit=UNIT, n_gpus=world, steps=args.steps,
             warmup=args.warmup, ms_per_step=ms_per_step, higher_is_better=True, scaling="weak",
             vs_baseline=None, dtype="f64", data="synthetic (seeded jittered lattice)",
-            config=dict(workload=(f"sand pile (configs[1]): {n} particles/GPU, Drucker-Prager "
-                                  "sand, floor + kinematic pusher box, dt=2e-3, N=10 substeps"
-                                  if args.workload.startswith("sand") else
-                                  f"elastic cube (configs[0]): {n} particles, dt=1e-3, N=10"),
+            config=dict(workload=workload_name(args.workload, n, N),
                         particles_per_gpu=n, substeps=N, envs=world,
                         parallelism=f"{world} independent envs (1/GPU)",
                         l2="flushed (256 MiB write) between timed steps",

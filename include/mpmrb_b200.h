@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define MPMRB_ABI_VERSION 1
+#define MPMRB_ABI_VERSION 2
 
 /* error codes -> reference exceptions */
 enum {
@@ -46,7 +46,11 @@ enum {
 
 /* material models */
 enum { MPMRB_MAT_ELASTIC = 0, /* fixed corotated, materials.py:113-122 */
-       MPMRB_MAT_SAND = 1 };  /* Drucker–Prager (new; parity unpinned)  */
+       MPMRB_MAT_SAND = 1,    /* Drucker–Prager (new; parity unpinned)  */
+       MPMRB_MAT_CLOTH = 2 }; /* codimensional cloth, Jiang et al. 2017 (new; parity unpinned) */
+
+/* per-particle cloth roles (mpmrb_sim_set_cloth) */
+enum { MPMRB_CLOTH_NONE = 0, MPMRB_CLOTH_VERTEX = 1, MPMRB_CLOTH_ELEMENT = 2 };
 
 /* geometry primitives (geometry.py) */
 enum { MPMRB_GEOM_HALFSPACE = 0, MPMRB_GEOM_SPHERE = 1, MPMRB_GEOM_BOX = 2,
@@ -60,6 +64,9 @@ typedef struct {
   int32_t pad_;
   double mu, lam;        /* Lame parameters (materials.py:40-46) */
   double dp_alpha;       /* Drucker–Prager alpha for sand, else 0 */
+  double k_normal;       /* cloth: transverse compression stiffness */
+  double gamma_shear;    /* cloth: transverse shear stiffness */
+  double friction;       /* cloth: cloth-cloth friction coefficient */
 } mpmrb_material;
 
 /* One rigid geometry in WORLD pose, flattened in (body, geom) order
@@ -280,6 +287,15 @@ int mpmrb_sim_set_geoms(mpmrb_sim* sim, const mpmrb_geom* geoms_host, int32_t n_
 int mpmrb_sim_set_params(mpmrb_sim* sim, double h, double dt_substep,
                          const double* gravity_host, double stiffness, double tau_d,
                          double eps_v, double margin, const mpmrb_solver_params* solver);
+/* Codimensional cloth (new): triangles with vertex particles
+ * and one element particle each.  All arrays are device arrays in the user's
+ * (reference) particle order: tri (ne,3) and epart (ne,) particle indices,
+ * dm_inv (ne,2,2) rest inverse, vol (ne,) rest volume, d3 (ne,3) transverse
+ * direction (state, updated in place every substep), role (n,) int8
+ * MPMRB_CLOTH_*.  Pass ne = 0 to remove the cloth. */
+int mpmrb_sim_set_cloth(mpmrb_sim* sim, int64_t n_elements, const int32_t* tri,
+                        const int32_t* epart, const double* dm_inv, const double* vol,
+                        double* d3, const int8_t* role);
 /* coupling.py:168-182: plan epoch, bias-cache reset, accumulator reset.
  * Sizes the grid/contact capacity for this step (synchronises once). */
 int mpmrb_sim_begin_step(mpmrb_sim* sim, int64_t epoch, int32_t n_substeps);

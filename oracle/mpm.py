@@ -79,6 +79,8 @@ def stresses(f: np.ndarray, material_id: np.ndarray, materials) -> np.ndarray:
         E, nu = (m if isinstance(m, tuple) else (m.youngs_modulus, m.poisson_ratio))[:2]
         mu, lam = lame(E, nu)
         sel = material_id == mid
+        if not isinstance(m, tuple) and getattr(m, "model", "elastic") == "cloth":
+            continue  # cloth: stresses come from the mesh (oracle/cloth.py)
         if not isinstance(m, tuple) and material_kind(m) == KIND_SAND:
             tau[sel] = hencky_stress(f[sel], mu, lam)
         else:
@@ -87,8 +89,12 @@ def stresses(f: np.ndarray, material_id: np.ndarray, materials) -> np.ndarray:
 
 
 def p2g(x, v, f, c, mass, vol0, material_id, materials, st: Stencil, dt: float,
-        n_nodes: int):
+        n_nodes: int, extra_tau=None, fext=None):
     """Scatter mass, APIC momentum and the MLS force impulse (mpm.py:66-99).
+
+    ``extra_tau`` (n,3,3) adds per-particle stresses (cloth element particles)
+    and ``fext`` (n,3) per-particle forces applied as dt f w in the force
+    channel (cloth vertex particles) — both NEW, oracle/cloth.py.
 
     Returns (mass (N,), mom_apic (N,3), mom_force (N,3)).
     """
@@ -96,6 +102,8 @@ def p2g(x, v, f, c, mass, vol0, material_id, materials, st: Stencil, dt: float,
     if n == 0:
         return np.zeros(n_nodes), np.zeros((n_nodes, 3)), np.zeros((n_nodes, 3))
     tau = stresses(f, material_id, materials)
+    if extra_tau is not None:
+        tau = tau + extra_tau
     w = st.weights
     dinv = 4.0 / (st.h * st.h)
     mv = mass[:, None] * v
@@ -105,6 +113,8 @@ def p2g(x, v, f, c, mass, vol0, material_id, materials, st: Stencil, dt: float,
     contrib[:, :, 0] = w * mass[:, None]
     contrib[:, :, 1:4] = w[:, :, None] * (mv[:, None, :] + st.dpos @ mc.transpose(0, 2, 1))
     contrib[:, :, 4:7] = w[:, :, None] * (st.dpos @ s.transpose(0, 2, 1))
+    if fext is not None:
+        contrib[:, :, 4:7] += w[:, :, None] * (dt * fext)[:, None, :]
     out = scatter_in_order(st.nodes, contrib, n_nodes)
     return out[:, 0].copy(), out[:, 1:4].copy(), out[:, 4:7].copy()
 
@@ -142,8 +152,9 @@ def clamp_inverted(f: np.ndarray) -> tuple[np.ndarray, int]:
     return out, k
 
 
-def g2p(x, f, st: Stencil, v_next: np.ndarray, dt: float):
+def g2p(x, f, st: Stencil, v_next: np.ndarray, dt: float, keep_f=None):
     """Gather v, C; advect x; F <- (I + dt C) F; clamp (mpm.py:118-138).
+    ``keep_f`` (n,) bool: particles whose F is left unchanged (cloth).
 
     Returns (x_new, v_new, c_new, f_new, n_clamped).
     """
@@ -155,5 +166,7 @@ def g2p(x, f, st: Stencil, v_next: np.ndarray, dt: float):
     c_new = dinv * (wv.transpose(0, 2, 1) @ st.dpos)
     x_new = x + dt * v_new
     f_new = (np.eye(3)[None] + dt * c_new) @ f
+    if keep_f is not None:
+        f_new[keep_f] = f[keep_f]
     f_new, k = clamp_inverted(f_new)
     return x_new, v_new, c_new, f_new, k

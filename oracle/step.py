@@ -23,6 +23,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
+from . import cloth as ocl
 from . import contact as cm
 from . import grid as og
 from . import mpm as om
@@ -58,6 +59,7 @@ class OracleState:
     time: float = 0.0
     step_index: int = 0
     plastic: np.ndarray | None = None   # per-particle DP hardening / log-volume state
+    cloth: object | None = None         # oracle.cloth.ClothMesh (codimensional cloth)
 
     def __post_init__(self):
         self.cache = cm.FirstSightBias()
@@ -86,8 +88,14 @@ def substep(s: OracleState, dt_s: float) -> dict:
     keys = og.allocate_blocks(s.x, s.h)
     n_nodes = keys.shape[0] * og.NODES_PER_BLOCK
     st = og.make_stencil(s.x, keys, s.h)
+    extra_tau = fext = keep_f = None
+    if s.cloth is not None:  # mesh forces before the transfer (oracle/cloth.py)
+        fext, tau_e, _ = ocl.forces(s.x, s.cloth)
+        extra_tau = np.zeros((s.x.shape[0], 3, 3))
+        extra_tau[s.cloth.epart] = tau_e
+        keep_f = s.cloth.roles(s.x.shape[0]) != ocl.ROLE_NONE
     mass, mom_apic, mom_force = om.p2g(s.x, s.v, s.f, s.c, s.mass, s.vol0, s.material_id,
-                                       s.materials, st, dt_s, n_nodes)
+                                       s.materials, st, dt_s, n_nodes, extra_tau, fext)
     active, v_k, v_star = om.grid_update(mass, mom_apic, mom_force, s.gravity, dt_s)
     con = cm.detect(s.x, s.bodies, s.det_margin, s.cache)
     gamma_world = np.zeros((0, 3))
@@ -112,8 +120,10 @@ def substep(s: OracleState, dt_s: float) -> dict:
             s.acc_lin[:, d] -= np.bincount(con.body, weights=gamma_world[:, d], minlength=nb)
             s.acc_ang[:, d] -= np.bincount(con.body, weights=moments[:, d], minlength=nb)
     x_old = s.x
-    s.x, s.v, s.c, f_new, clamped = om.g2p(s.x, s.f, st, v_next, dt_s)
+    s.x, s.v, s.c, f_new, clamped = om.g2p(s.x, s.f, st, v_next, dt_s, keep_f)
     s.f, s.plastic = opl.return_map(f_new, s.plastic, s.material_id, s.materials)
+    if s.cloth is not None:
+        s.x = ocl.post_g2p(s.x, s.c, s.cloth, dt_s)
     return dict(keys=keys, stencil=st, mass=mass, mom_apic=mom_apic, mom_force=mom_force,
                 active=active, v_k=v_k, v_star=v_star, v_next=v_next, contacts=con,
                 report=report, gamma_world=gamma_world, clamped=clamped, x_old=x_old)

@@ -31,6 +31,8 @@ E_CAPACITY = 8
 
 MAT_ELASTIC = 0
 MAT_SAND = 1
+MAT_CLOTH = 2
+CLOTH_NONE, CLOTH_VERTEX, CLOTH_ELEMENT = 0, 1, 2
 GEOM_HALFSPACE, GEOM_SPHERE, GEOM_BOX, GEOM_CAPSULE = 0, 1, 2, 3
 
 
@@ -48,7 +50,8 @@ class NativeError(RuntimeError):
 
 class Material(C.Structure):
     _fields_ = [("kind", C.c_int32), ("pad_", C.c_int32), ("mu", C.c_double),
-                ("lam", C.c_double), ("dp_alpha", C.c_double)]
+                ("lam", C.c_double), ("dp_alpha", C.c_double), ("k_normal", C.c_double),
+                ("gamma_shear", C.c_double), ("friction", C.c_double)]
 
 
 class Geom(C.Structure):
@@ -141,6 +144,7 @@ _SIGS = {
     "mpmrb_sim_set_geoms": ([_P, C.POINTER(Geom), C.c_int32, C.c_int32], C.c_int),
     "mpmrb_sim_set_params": ([_P, _D, _D, C.POINTER(_D), _D, _D, _D, _D,
                               C.POINTER(SolverParamsC)], C.c_int),
+    "mpmrb_sim_set_cloth": ([_P, _I64, _P, _P, _P, _P, _P, _P], C.c_int),
     "mpmrb_sim_begin_step": ([_P, _I64, C.c_int32], C.c_int),
     "mpmrb_sim_substep": ([_P], C.c_int),
     "mpmrb_sim_end_step": ([_P, C.POINTER(StepStats), C.POINTER(_D)], C.c_int),

@@ -102,6 +102,7 @@ class SimState:
     solver_params: SolverParams = field(default_factory=SolverParams)
     mode: str = "deterministic"
     workers: int | None = None
+    cloth: object | None = None  # cloth.ClothMesh (NEW: codimensional cloth)
     time: float = 0.0
     step_index: int = 0
     plan_builds: int = 0
@@ -174,6 +175,14 @@ def advance_step(state: SimState, profile: dict | None = None) -> StepSummary:
         _lib.check(L.mpmrb_sim_set_particles(sim, C.byref(pv)))
         tab, nm = material_table(state.materials)
         _lib.check(L.mpmrb_sim_set_materials(sim, tab, nm))
+        cl = state.cloth
+        if cl is not None and cl.n_elements > 0:
+            _lib.check(L.mpmrb_sim_set_cloth(sim, cl.n_elements, _lib.ptr(cl.tri),
+                                             _lib.ptr(cl.epart), _lib.ptr(cl.dm_inv),
+                                             _lib.ptr(cl.vol), _lib.ptr(cl.d3),
+                                             _lib.ptr(cl.role)))
+        else:
+            _lib.check(L.mpmrb_sim_set_cloth(sim, 0, None, None, None, None, None, None))
         gs = geom_structs(state.bodies)
         garr = (_lib.Geom * max(1, len(gs)))(*gs)
         _lib.check(L.mpmrb_sim_set_geoms(sim, garr, len(gs), nb))

@@ -602,6 +602,28 @@ int mpmrb_sim_set_particles(mpmrb_sim* s, const mpmrb_particles* p) {
   return MPMRB_OK;
 }
 
+int mpmrb_sim_set_cloth(mpmrb_sim* s, int64_t ne, const int32_t* tri, const int32_t* epart,
+                        const double* dm_inv, const double* vol, double* d3,
+                        const int8_t* role) {
+  if (!s) return set_error(MPMRB_E_INVALID, "null sim");
+  if (ne < 0) return set_error(MPMRB_E_INVALID, "negative element count");
+  if (ne > 0 && !(tri && epart && dm_inv && vol && d3 && role))
+    return set_error(MPMRB_E_INVALID, "cloth arrays must be non-null");
+  const bool changed = (ne > 0) != (s->cloth.ne > 0) || s->cloth.tri != tri ||
+                       s->cloth.epart != epart || s->cloth.dm_inv != dm_inv ||
+                       s->cloth.vol != vol || s->cloth.d3 != d3 || s->cloth.ne != ne ||
+                       s->cloth_role_user != (const signed char*)role;
+  s->cloth.ne = ne;
+  s->cloth.tri = tri;
+  s->cloth.epart = epart;
+  s->cloth.dm_inv = dm_inv;
+  s->cloth.vol = vol;
+  s->cloth.d3 = d3;
+  s->cloth_role_user = (const signed char*)role;
+  if (changed) s->invalidate();
+  return MPMRB_OK;
+}
+
 int mpmrb_sim_set_materials(mpmrb_sim* s, const mpmrb_material* mats, int32_t n) {
   if (!s) return set_error(MPMRB_E_INVALID, "null sim");
   if (s->b_mats.grow(sizeof(mpmrb_material) * (n > 0 ? n : 1))) return MPMRB_E_CUDA;

@@ -97,6 +97,20 @@ struct ParticlesDev {
   const long long* mid;
   double* plastic;
   long long n;
+  // codimensional cloth (NULL when absent): role per particle (MPMRB_CLOTH_*),
+  // element stresses written by the cloth kernel, vertex forces
+  const signed char* role = nullptr;
+  double* tau = nullptr;   // (n,9)
+  double* fext = nullptr;  // (n,3)
+};
+struct ClothDev {
+  long long ne = 0;
+  const int* tri = nullptr;
+  const int* epart = nullptr;
+  const double* dm_inv = nullptr;
+  const double* vol = nullptr;
+  double* d3 = nullptr;
+  const int* inv_perm = nullptr;
 };
 struct GridDev {
   const unsigned long long* hkeys;
@@ -113,6 +127,15 @@ int launch_grid_update(Ctx& c, long long n_nodes_cap, const int* nb_dev, const d
 int launch_g2p(Ctx& c, const GridDev& g, const ParticlesDev& p, const mpmrb_material* mats_dev,
                int nmat, const double* v_next, double dt, unsigned long long* clamped_dev,
                int* health_dev);
+
+// cloth.cu
+int launch_cloth_forces(Ctx& c, const ClothDev& cl, const ParticlesDev& p,
+                        const mpmrb_material* mats_dev, int nmat);
+int launch_cloth_post(Ctx& c, const ClothDev& cl, const ParticlesDev& p,
+                      const mpmrb_material* mats_dev, int nmat, double dt);
+int launch_inverse_perm(Ctx& c, const int* perm, long long n, int* inv);
+int launch_gather_i8(Ctx& c, const signed char* src, const int* perm, long long n,
+                     signed char* dst);
 
 int launch_clamp(Ctx& c, const double* f, long long n, double* out, unsigned long long* nbad);
 int launch_health(Ctx& c, const double* x, const double* v, long long n, double h, int* bad);

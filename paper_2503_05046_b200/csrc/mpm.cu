@@ -57,8 +57,9 @@ __global__ void k_stresses(const double* __restrict__ f, const long long* __rest
 __device__ __forceinline__ void p2g_scatter_one(const GridDev& g, const double* fx,
                                                 const double (*w1)[3], const StencilBlocks& sb,
                                                 const Stencil1& s, double m, const double* mv,
-                                                const M3& mC, const M3& S, double* gmass,
-                                                double* mom_apic, double* mom_force) {
+                                                const M3& mC, const M3& S, const double* fi,
+                                                double* gmass, double* mom_apic,
+                                                double* mom_force) {
   const double h = g.h;
 #pragma unroll 1
   for (int ox = 0; ox < 3; ++ox) {
@@ -76,7 +77,7 @@ __device__ __forceinline__ void p2g_scatter_one(const GridDev& g, const double* 
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
           double a = mv[d] + (mC(d, 0) * dx + mC(d, 1) * dy + mC(d, 2) * dz);
-          double b = S(d, 0) * dx + S(d, 1) * dy + S(d, 2) * dz;
+          double b = S(d, 0) * dx + S(d, 1) * dy + S(d, 2) * dz + fi[d];
           atomicAdd(&mom_apic[3 * node + d], w * a);
           atomicAdd(&mom_force[3 * node + d], w * b);
         }
@@ -100,10 +101,14 @@ __device__ __forceinline__ void p2g_scatter_one(const GridDev& g, const double* 
 constexpr int kP2GThreads = 128;
 constexpr int kWarpTile = 128;  // nodes per warp tile (e.g. 4 x 4 x 8)
 
+// Per-particle P2G payload: m, m v, m C, S = -dt D^-1 V0 tau and the external
+// impulse dt f of cloth vertex forces.  Cloth roles (cloth.cu): vertex
+// particles carry no stress (their in-plane forces arrive in fext), element
+// particles carry the transverse stress written by k_cloth_forces.
 __device__ __forceinline__ void particle_payload(const ParticlesDev& p, long long i, double h,
                                                  double dt, const mpmrb_material* mats, int nmat,
                                                  Stencil1& s, double& m, double* mv, M3& mC,
-                                                 M3& S, DevStatus* st) {
+                                                 M3& S, double* fi, DevStatus* st) {
   double xp[3] = {p.x[3 * i], p.x[3 * i + 1], p.x[3 * i + 2]};
   make_stencil1(xp, h, s);
   long long mid = p.mid[i];
@@ -112,7 +117,16 @@ __device__ __forceinline__ void particle_payload(const ParticlesDev& p, long lon
     mid = 0;
   }
   m = p.mass[i];
-  const M3 tau = particle_stress(m3_load(p.f + 9 * i), mats[mid]);
+  const int role = p.role ? p.role[i] : MPMRB_CLOTH_NONE;
+  M3 tau;
+  if (role == MPMRB_CLOTH_ELEMENT && p.tau) {
+    tau = m3_load(p.tau + 9 * i);
+  } else if (role != MPMRB_CLOTH_NONE || mats[mid].kind == MPMRB_MAT_CLOTH) {
+#pragma unroll
+    for (int k = 0; k < 9; ++k) tau.a[k] = 0.0;
+  } else {
+    tau = particle_stress(m3_load(p.f + 9 * i), mats[mid]);
+  }
   const double dinv = 4.0 / (h * h);
   const double coef = (-dt * dinv) * p.vol0[i];
   const M3 C = m3_load(p.c + 9 * i);
@@ -122,7 +136,10 @@ __device__ __forceinline__ void particle_payload(const ParticlesDev& p, long lon
     mC.a[k] = m * C.a[k];
   }
 #pragma unroll
-  for (int d = 0; d < 3; ++d) mv[d] = m * p.v[3 * i + d];
+  for (int d = 0; d < 3; ++d) {
+    mv[d] = m * p.v[3 * i + d];
+    fi[d] = (role == MPMRB_CLOTH_VERTEX && p.fext) ? dt * p.fext[3 * i + d] : 0.0;
+  }
 }
 
 __global__ void __launch_bounds__(kP2GThreads, 4) k_p2g(GridDev g, ParticlesDev p,
@@ -160,15 +177,15 @@ __global__ void __launch_bounds__(kP2GThreads, 4) k_p2g(GridDev g, ParticlesDev 
     // spread warp: per-particle scatter with global atomics
     if (live) {
       Stencil1 s;
-      double m, mv[3];
+      double m, mv[3], fi[3];
       M3 mC, S;
-      particle_payload(p, i, h, dt, mats, nmat, s, m, mv, mC, S, st);
+      particle_payload(p, i, h, dt, mats, nmat, s, m, mv, mC, S, fi, st);
       StencilBlocks sb;
       if (!resolve_blocks(s, g.hkeys, g.hvals, g.mask, sb)) {
         raise_status(st, MPMRB_E_ALLOCATION, 20, i);
         return;
       }
-      p2g_scatter_one(g, s.fx, s.w, sb, s, m, mv, mC, S, gmass, mom_apic, mom_force);
+      p2g_scatter_one(g, s.fx, s.w, sb, s, m, mv, mC, S, fi, gmass, mom_apic, mom_force);
     }
     return;
   }
@@ -209,7 +226,7 @@ __global__ void __launch_bounds__(kP2GThreads, 4) k_p2g(GridDev g, ParticlesDev 
     for (int ch = 0; ch < 7; ++ch) tile[ch][q] = 0.0;
   // 3. payload of this lane's (sorted) particle
   Stencil1 s;
-  double m = 0.0, mv[3] = {0.0, 0.0, 0.0};
+  double m = 0.0, mv[3] = {0.0, 0.0, 0.0}, fi[3] = {0.0, 0.0, 0.0};
   M3 mC, S;
 #pragma unroll
   for (int k = 0; k < 9; ++k) {
@@ -218,7 +235,7 @@ __global__ void __launch_bounds__(kP2GThreads, 4) k_p2g(GridDev g, ParticlesDev 
   }
   int cb[3] = {0, 0, 0};
   if (mlive) {
-    particle_payload(p, i, h, dt, mats, nmat, s, m, mv, mC, S, st);
+    particle_payload(p, i, h, dt, mats, nmat, s, m, mv, mC, S, fi, st);
 #pragma unroll
     for (int a = 0; a < 3; ++a) cb[a] = (int)s.base[a] - lo[a];
   } else {
@@ -251,7 +268,7 @@ __global__ void __launch_bounds__(kP2GThreads, 4) k_p2g(GridDev g, ParticlesDev 
       const double a = mv[d] + (mC(d, 0) * dx + mC(d, 1) * dy + mC(d, 2) * dz);
       const double bb = S(d, 0) * dx + S(d, 1) * dy + S(d, 2) * dz;
       v[1 + d] = w * a;
-      v[4 + d] = w * bb;
+      v[4 + d] = w * (bb + fi[d]);
     }
     for (int l = 0; l < levels; ++l) {
       const int o = 1 << l;
@@ -400,13 +417,17 @@ __global__ void __launch_bounds__(128) k_g2p(GridDev g, ParticlesDev p,
       M3 A = m3_identity();
 #pragma unroll
       for (int k = 0; k < 9; ++k) A.a[k] += dt * C.a[k];
-      M3 F = m3_mul(A, m3_load(p.f + 9 * i));
-      if (!(m3_det(F) > 0.0) || !m3_finite(F)) {
-        F = clamp_singular_values(F);
-        was_clamped = true;
+      const bool cloth = p.role && p.role[i] != MPMRB_CLOTH_NONE;
+      M3 F = m3_load(p.f + 9 * i);
+      if (!cloth) {  // cloth particles carry no F (cloth.cu: d3 per element)
+        F = m3_mul(A, F);
+        if (!(m3_det(F) > 0.0) || !m3_finite(F)) {
+          F = clamp_singular_values(F);
+          was_clamped = true;
+        }
       }
       long long mid = p.mid[i];
-      if (mid >= 0 && mid < nmat && mats[mid].kind == MPMRB_MAT_SAND) {
+      if (!cloth && mid >= 0 && mid < nmat && mats[mid].kind == MPMRB_MAT_SAND) {
         double dq = 0.0;
         F = dp_return_map(F, mats[mid].mu, mats[mid].lam, mats[mid].dp_alpha, &dq);
         if (p.plastic) p.plastic[i] += dq;

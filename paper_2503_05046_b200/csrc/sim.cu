@@ -314,6 +314,10 @@ int Sim::capture_or_launch() {
   MPMRB_CUDA_OK(cudaMemsetAsync(b_mom.p, 0, 8 * 6 * N, c.stream));
   double* mom_apic = b_mom.as<double>();
   double* mom_force = mom_apic + 3 * N;
+  if (cloth.ne > 0) {  // cloth forces before the transfer (cloth.cu)
+    rc = launch_cloth_forces(c, cloth, q, b_mats.as<mpmrb_material>(), nmat);
+    if (rc) return rc;
+  }
   rc = launch_p2g(c, g, q, b_mats.as<mpmrb_material>(), nmat, dt_s, b_mass.as<double>(), mom_apic,
                   mom_force);
   if (rc) return rc;
@@ -440,6 +444,10 @@ int Sim::capture_or_launch() {
   rc = launch_g2p(c, g, q, b_mats.as<mpmrb_material>(), nmat, b_vnext.as<double>(), dt_s,
                   b_misc.as<unsigned long long>(), b_misc.as<int>() + 2);
   if (rc) return rc;
+  if (cloth.ne > 0) {  // d3 advection, return map, element particles to centroids
+    rc = launch_cloth_post(c, cloth, q, b_mats.as<mpmrb_material>(), nmat, dt_s);
+    if (rc) return rc;
+  }
   mark(7);
   MPMRB_CUDA_OK(cudaGetLastError());
   return MPMRB_OK;
@@ -557,6 +565,31 @@ int Sim::begin_step(long long epoch, int n_substeps) {
       else MPMRB_CUDA_OK(cudaMemsetAsync(q.plastic, 0, 8 * p.n, c.stream));
     }
     if (rc) return rc;
+    if (cloth.ne > 0) {
+      if (b_invperm.grow(4 * p.n) || b_qrole.grow(p.n) || b_qtau.grow(8 * 9 * p.n) ||
+          b_qfext.grow(8 * 3 * p.n))
+        return MPMRB_E_CUDA;
+      if (q.role != b_qrole.as<signed char>() || q.tau != b_qtau.as<double>() ||
+          q.fext != b_qfext.as<double>()) {
+        q.role = b_qrole.as<signed char>();
+        q.tau = b_qtau.as<double>();
+        q.fext = b_qfext.as<double>();
+        invalidate();
+      }
+      if (cloth.inv_perm != b_invperm.as<int>()) {
+        cloth.inv_perm = b_invperm.as<int>();
+        invalidate();
+      }
+      rc = launch_inverse_perm(c, perm, p.n, b_invperm.as<int>());
+      if (!rc) rc = launch_gather_i8(c, cloth_role_user, perm, p.n, b_qrole.as<signed char>());
+      if (rc) return rc;
+      MPMRB_CUDA_OK(cudaMemsetAsync(q.tau, 0, 8 * 9 * p.n, c.stream));
+    } else if (q.role) {
+      q.role = nullptr;
+      q.tau = nullptr;
+      q.fext = nullptr;
+      invalidate();
+    }
   }
   if (max_substeps < n_substeps || !b_stats.p) {
     max_substeps = n_substeps > max_substeps ? n_substeps : max_substeps;

@@ -48,6 +48,10 @@ struct Sim {
   // sorted particle state: x, v (3n) f, c (9n) mass, vol0, plastic (n) doubles; mid (n) int64
   DevBuf b_qd, b_qmid, b_perm, b_skeys, b_svals, b_cpart_user;
   DevBuf b_react;  // per-CTA reaction partials
+  // codimensional cloth (cloth.cu): mesh in user order + per-step internal views
+  ClothDev cloth{};
+  const signed char* cloth_role_user = nullptr;
+  DevBuf b_invperm, b_qrole, b_qtau, b_qfext;
   bool slots_init = false;
   DevBuf b_bias_stamp, b_bias_store;
 

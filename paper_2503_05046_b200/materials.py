@@ -7,6 +7,11 @@
   SPEC.md:8,98,111): Hencky St.Venant–Kirchhoff stress plus a Drucker–Prager
   return map applied in the G2P kernel (Klár et al. 2016; oracle/plasticity.py
   restates it in NumPy).
+* cloth (NEW, parity unpinned): codimensional cloth of Jiang et al. 2017 as the
+  paper uses it — in-plane fixed corotated (mu, lambda),
+  transverse compression k_normal, transverse shear gamma_shear and cloth-cloth
+  friction (csrc/cloth.cu; oracle/cloth.py).  Defaults: k_normal = E,
+  gamma_shear = 0.1 E, friction 0.3 (proposed; the paper gives only E, nu, rho).
 """
 
 from __future__ import annotations
@@ -27,8 +32,11 @@ class Material:
     youngs_modulus: float
     poisson_ratio: float
     density: float
-    model: str = "elastic"          # "elastic" | "sand"
+    model: str = "elastic"          # "elastic" | "sand" | "cloth"
     friction_angle: float = 30.0    # degrees, sand only
+    cloth_normal_stiffness: float | None = None  # cloth: default E
+    cloth_shear_stiffness: float | None = None   # cloth: default 0.1 E
+    cloth_friction: float = 0.3                  # cloth-cloth friction
 
     def __post_init__(self):
         if not (self.youngs_modulus > 0.0):
@@ -37,7 +45,7 @@ class Material:
             raise ValueError(f"poisson_ratio must be in [0, 0.5), got {self.poisson_ratio}")
         if not (self.density > 0.0):
             raise ValueError(f"density must be > 0, got {self.density}")
-        if self.model not in ("elastic", "sand"):
+        if self.model not in ("elastic", "sand", "cloth"):
             raise ValueError(f"unknown material model {self.model!r}")
         if self.model == "sand" and not (0.0 < self.friction_angle < 90.0):
             raise ValueError("friction_angle must be in (0, 90) degrees")
@@ -53,11 +61,21 @@ class Material:
         s = np.sin(np.deg2rad(self.friction_angle))
         return float(np.sqrt(2.0 / 3.0) * 2.0 * s / (3.0 - s))
 
+    @property
+    def cloth_params(self) -> tuple[float, float, float]:
+        """(k_normal, gamma_shear, friction) of the cloth model."""
+        E = self.youngs_modulus
+        k = E if self.cloth_normal_stiffness is None else self.cloth_normal_stiffness
+        g = 0.1 * E if self.cloth_shear_stiffness is None else self.cloth_shear_stiffness
+        return float(k), float(g), float(self.cloth_friction)
+
     def to_struct(self) -> _lib.Material:
         m = _lib.Material()
-        m.kind = _lib.MAT_SAND if self.model == "sand" else _lib.MAT_ELASTIC
+        m.kind = {"sand": _lib.MAT_SAND, "cloth": _lib.MAT_CLOTH}.get(self.model, _lib.MAT_ELASTIC)
         m.mu, m.lam = self.lame
         m.dp_alpha = self.dp_alpha if self.model == "sand" else 0.0
+        if self.model == "cloth":
+            m.k_normal, m.gamma_shear, m.friction = self.cloth_params
         return m
 
 

@@ -60,30 +60,81 @@ def build_bodies(scene) -> list:
 
 
 def build_materials(scene) -> list:
-    return [Material(m["E"], m["nu"], m["rho"], model=m.get("model", "elastic"),
-                     friction_angle=m.get("friction_angle", 30.0)) for m in scene["materials"]]
+    out = []
+    for m in scene["materials"]:
+        kw = {}
+        if m.get("model") == "cloth":
+            kw = dict(cloth_normal_stiffness=m.get("k_normal"),
+                      cloth_shear_stiffness=m.get("gamma_shear"),
+                      cloth_friction=m.get("cloth_friction", 0.3))
+        out.append(Material(m["E"], m["nu"], m["rho"], model=m.get("model", "elastic"),
+                            friction_angle=m.get("friction_angle", 30.0), **kw))
+    return out
+
+
+def cloth_arrays(scene) -> list:
+    """Host arrays of the scene's cloth sheets (cloth.sheet_arrays), in scene
+    order, each with its material id and initial velocity."""
+    from .cloth import sheet_arrays
+    out = []
+    for c in scene.get("cloth", []):
+        a = sheet_arrays(c["center"], c["size"], c["n_side"], c["thickness"],
+                         scene["materials"][c["material"]]["rho"], c.get("normal_axis", 2))
+        a["mid"] = np.full(a["x"].shape[0], c["material"], dtype=np.int64)
+        a["v"] = np.tile(np.asarray(c.get("velocity", [0.0, 0.0, 0.0]), float),
+                         (a["x"].shape[0], 1))
+        out.append(a)
+    return out
 
 
 def build_particles(scene):
+    """Particles of the scene's volumes followed by its cloth sheets; returns
+    (ParticleSet, ClothMesh | None)."""
+    from .cloth import ClothMesh
+    from .particles import ParticleSet
     mats = build_materials(scene)
     sets = [seed_box(np.asarray(v["center"]), np.asarray(v["half"]), scene["h"],
                      mats[v["material"]], material_id=v["material"], particles_per_cell=v["ppc"],
                      jitter=v["jitter"], velocity=tuple(v["velocity"]), seed=v["seed"])
             for v in scene["volumes"]]
-    return concatenate(sets)
+    sheets = cloth_arrays(scene)
+    for a in sheets:
+        n = a["x"].shape[0]
+        sets.append(ParticleSet(a["x"], a["v"], np.tile(np.eye(3), (n, 1, 1)),
+                                np.zeros((n, 3, 3)), a["mass"], a["vol"], a["mid"]))
+    particles = concatenate(sets)
+    if not sheets:
+        return particles, None
+    n_total = particles.n
+    first = particles.n - sum(a["x"].shape[0] for a in sheets)
+    tri, ep, dmi, vol, d3 = [], [], [], [], []
+    role = np.zeros(n_total, dtype=np.int8)
+    for a in sheets:
+        tri.append(a["tri"] + first)
+        ep.append(a["epart"] + first)
+        dmi.append(a["dm_inv"])
+        vol.append(a["vol_e"])
+        d3.append(a["d3"])
+        role[first:first + a["x"].shape[0]] = a["role"]
+        first += a["x"].shape[0]
+    mesh = ClothMesh.from_arrays(np.concatenate(tri), np.concatenate(ep), np.concatenate(dmi),
+                                 np.concatenate(vol), np.concatenate(d3), role)
+    return particles, mesh
 
 
-def build_state(scene, particles=None) -> SimState:
+def build_state(scene, particles=None, cloth=None) -> SimState:
     c = scene["contact"]
     s = scene["solver"]
     sp = SolverParams(eps_r=s.get("eps_r", 5e-2), max_iters=s.get("max_iters", 500))
-    return SimState(particles=particles if particles is not None else build_particles(scene),
-                    materials=build_materials(scene), bodies=build_bodies(scene), h=scene["h"],
+    if particles is None:
+        particles, cloth = build_particles(scene)
+    return SimState(particles=particles, materials=build_materials(scene),
+                    bodies=build_bodies(scene), h=scene["h"],
                     step=StepConfig(dt=scene["dt"], substeps=scene["substeps"],
                                     gravity=tuple(scene["gravity"])),
                     contact_params=ContactParams(stiffness=c["stiffness"], tau_d=c["tau_d"],
                                                  eps_v=c["eps_v"], margin=c.get("margin")),
-                    solver_params=sp)
+                    solver_params=sp, cloth=cloth)
 
 
 # ------------------------------------------------------------------ configs
@@ -174,11 +225,72 @@ def host_particles(scene: dict) -> dict:
         out["mass"].append(np.full(n, m["rho"] * vol))
         out["vol"].append(np.full(n, vol))
         out["mid"].append(np.full(n, v["material"], dtype=np.int64))
+    for a in cloth_arrays(scene):  # cloth sheets follow the volumes
+        for k in ("x", "v", "mass", "vol", "mid"):
+            out[k].append(a[k])
+    out = {k: (val if val else [np.zeros((0, 3)) if k in ("x", "v") else np.zeros(0)])
+           for k, val in out.items()}
     arr = {k: np.concatenate(val) for k, val in out.items()}
+    arr["mid"] = arr["mid"].astype(np.int64)
     n = arr["x"].shape[0]
     arr["f"] = np.tile(np.eye(3), (n, 1, 1))
     arr["c"] = np.zeros((n, 3, 3))
     return arr
+
+
+def cloth_sheet_scene(n_side: int = 183, h: float = 1.0 / 128) -> dict:
+    """C3: a square cloth sheet (n_side^2 vertices + 2 (n_side-1)^2 face
+    particles; 183 -> 99,737 particles) draped over a rigid sphere r = 0.25,
+    E = 3.2e6, nu = 0.4, rho = 1.5e3, mu = 0.6, dt = 2 ms
+    (SURVEY.md §8d).  Vertex spacing h/2, thickness 1 mm (proposed).  N = 16
+    substeps: with E = 3.2e6 the membrane wave speed sqrt(E/rho) = 46 m/s and
+    the explicit transfer needs dt_s < spacing / c (N = 4 diverges in the
+    oracle as well)."""
+    dt = 2e-3
+    side = (n_side - 1) * 0.5 * h
+    return dict(h=h, dt=dt, substeps=16, gravity=[0, 0, -9.81],
+                contact=dict(stiffness=1e5, tau_d=dt, eps_v=1e-4, margin=None),
+                solver=dict(eps_r=5e-2),
+                materials=[dict(E=3.2e6, nu=0.4, rho=1.5e3, model="cloth")],
+                volumes=[],
+                cloth=[dict(material=0, center=[0.0, 0.0, 0.3], size=[side, side],
+                            n_side=n_side, thickness=1e-3)],
+                bodies=[dict(name="sphere", kinematic=True, position=[0, 0, 0],
+                             quat=[1, 0, 0, 0],
+                             geoms=[dict(shape="sphere", radius=0.25, position=[0, 0, 0],
+                                         quat=[1, 0, 0, 0], mu=0.6)])])
+
+
+def tshirt_fold_scene(n_side: int = 64, h: float = 1.0 / 128) -> dict:
+    """C4 (synthetic stand-in for the paper's T-shirt): a
+    sheet with the paper's particle count (64^2 vertices + 7,938 faces =
+    12,034 particles) on a table, its near edge gripped by two kinematic box
+    grippers that lift it and fold it over (keyframe trajectories), E = 1e5,
+    nu = 0.3, rho = 1e3, gripper friction 0.6, dt = 2 ms, N = 4."""
+    dt = 2e-3
+    side = (n_side - 1) * 0.5 * h
+    half = 0.5 * side
+    grip_half = [0.02, 0.02, 0.01]
+    z0 = 0.004 + grip_half[2] + 0.002
+    keys = [0.0, 0.3, 0.8, 1.3]
+
+    def gripper(name, y):
+        p0 = [-half + 0.01, y, z0]
+        return dict(name=name, kinematic=True, position=p0, quat=[1, 0, 0, 0],
+                    trajectory=dict(times=keys,
+                                    positions=[p0, [-half + 0.01, y, z0 - 0.004],
+                                               [0.0, y, 0.12], [half - 0.03, y, 0.03]]),
+                    geoms=[dict(shape="box", half_extents=grip_half, position=[0, 0, 0],
+                                quat=[1, 0, 0, 0], mu=0.6)])
+    return dict(h=h, dt=dt, substeps=4, gravity=[0, 0, -9.81],
+                contact=dict(stiffness=1e5, tau_d=dt, eps_v=1e-4, margin=None),
+                solver=dict(eps_r=5e-2),
+                materials=[dict(E=1e5, nu=0.3, rho=1e3, model="cloth")],
+                volumes=[],
+                cloth=[dict(material=0, center=[0.0, 0.0, 0.004], size=[side, side],
+                            n_side=n_side, thickness=1e-3)],
+                bodies=[_floor(0.5), gripper("gripper_a", -0.5 * half),
+                        gripper("gripper_b", 0.5 * half)])
 
 
 def scaled(scene: dict, **kw) -> dict:

@@ -67,6 +67,31 @@ def oracle_materials(scene) -> list:
             for m in scene["materials"]]
 
 
+def oracle_cloth(scene, n_total: int):
+    """oracle.cloth.ClothMesh of the scene's sheets, which follow the volume
+    particles at the end of the particle arrays (scenes.build_particles)."""
+    if not scene.get("cloth"):
+        return None
+    from oracle import cloth as oc
+    from paper_2503_05046_b200.scenes import cloth_arrays
+    sheets = cloth_arrays(scene)
+    first = n_total - sum(a["x"].shape[0] for a in sheets)
+    tri, ep, dmi, vol, d3 = [], [], [], [], []
+    for a in sheets:
+        tri.append(a["tri"] + first)
+        ep.append(a["epart"] + first)
+        dmi.append(a["dm_inv"])
+        vol.append(a["vol_e"])
+        d3.append(a["d3"])
+        first += a["x"].shape[0]
+    m = scene["materials"][scene["cloth"][0]["material"]]
+    params = oc.params_from(m["E"], m["nu"], m.get("k_normal"), m.get("gamma_shear"),
+                            m.get("cloth_friction", 0.3))
+    return oc.ClothMesh(tri=np.concatenate(tri), epart=np.concatenate(ep),
+                        dm_inv=np.concatenate(dmi), vol=np.concatenate(vol),
+                        d3=np.concatenate(d3), params=params)
+
+
 def oracle_state(scene, x, v, f, c, mass, vol, mid):
     from oracle.solver import Params
     from oracle.step import OracleState
@@ -80,4 +105,5 @@ def oracle_state(scene, x, v, f, c, mass, vol, mid):
                        materials=oracle_materials(scene), bodies=oracle_bodies(scene),
                        h=scene["h"], dt=scene["dt"], substeps=scene["substeps"],
                        gravity=tuple(scene["gravity"]), k=con["stiffness"], tau_d=con["tau_d"],
-                       eps_v=con["eps_v"], margin=con.get("margin"), solver=sp)
+                       eps_v=con["eps_v"], margin=con.get("margin"), solver=sp,
+                       cloth=oracle_cloth(scene, np.asarray(x).shape[0]))

@@ -409,3 +409,63 @@ def test_fused_matches_oracle_with_free_body_and_sand(mp):
     np.testing.assert_allclose(np_(st.particles.plastic), ref.plastic, rtol=0, atol=1e-8)
     np.testing.assert_allclose(np.array([b.position for b in st.bodies]),
                                np.array([b.position for b in ref.bodies]), rtol=0, atol=1e-10)
+
+
+# ------------------------------------------------------------------ codimensional cloth
+
+def _cloth_pair(mp, sc):
+    from paper_2503_05046_b200 import scenes
+    st = scenes.build_state(sc)
+    p0 = st.particles.numpy()
+    ref = oracle_state(sc, p0["x"], p0["v"], p0["f"], p0["c"], p0["mass"], p0["volume0"],
+                       p0["material_id"])
+    return st, ref
+
+
+def test_cloth_free_fall_stretched_matches_oracle(mp):
+    """A pre-stretched sheet in free fall (membrane + transverse terms, no
+    contact): positions and d3 match the cloth oracle (parity unpinned
+    against the reference, which has no cloth)."""
+    from paper_2503_05046_b200 import scenes
+    sc = scenes.cloth_sheet_scene(n_side=12)
+    sc["bodies"] = []
+    st, ref = _cloth_pair(mp, sc)
+    x = np_(st.particles.x)
+    x[:, 0] *= 1.05
+    st.particles.x.copy_(torch.as_tensor(x))
+    ref.x = x.copy()
+    for _ in range(4):
+        mp.advance_step(st)
+        ostep.step(ref)
+    np.testing.assert_allclose(np_(st.particles.x), ref.x, rtol=0, atol=1e-11)
+    np.testing.assert_allclose(np_(st.particles.v), ref.v, rtol=0, atol=1e-8)
+    np.testing.assert_allclose(np_(st.cloth.d3), ref.cloth.d3, rtol=0, atol=1e-10)
+
+
+@pytest.mark.parametrize("which", ["drape", "fold"])
+def test_cloth_contact_matches_oracle(mp, which):
+    """Cloth against rigid geometry (sheet dropping on the sphere of C3; the
+    gripper scene of C4): contact sets exact, positions / wrench to the
+    solver's tolerance-level reassociation."""
+    from paper_2503_05046_b200 import scenes
+    if which == "drape":
+        sc = scenes.cloth_sheet_scene(n_side=15)
+        sc["cloth"][0]["center"] = [0.0, 0.0, 0.2525]
+        sc["cloth"][0]["velocity"] = [0.0, 0.0, -0.3]
+        sc["contact"]["stiffness"] = 1e3
+        nsteps = 4
+    else:
+        sc = scenes.tshirt_fold_scene(n_side=16)
+        sc["cloth"][0]["center"] = [0.0, 0.0, 0.0012]
+        sc["cloth"][0]["velocity"] = [0.0, 0.0, -0.3]
+        sc["contact"]["stiffness"] = 1e3
+        nsteps = 4
+    st, ref = _cloth_pair(mp, sc)
+    for i in range(nsteps):
+        s = mp.advance_step(st)
+        r = ostep.step(ref)
+        assert s.n_contacts_mean == r["n_contacts_mean"], i
+        ws = np.abs(r["wrench"]).max()
+        assert np.abs(s.wrench - r["wrench"]).max() <= 1e-5 * ws + 1e-9, i
+    np.testing.assert_allclose(np_(st.particles.x), ref.x, rtol=0, atol=1e-9)
+    np.testing.assert_allclose(np_(st.cloth.d3), ref.cloth.d3, rtol=0, atol=1e-7)
