@@ -25,7 +25,7 @@ def test_library_loads_and_exports_every_header_symbol():
     assert not missing, missing
     # the ctypes table covers every declared entry point
     assert set(names) <= set(_lib.EXPORTED), set(names) - set(_lib.EXPORTED)
-    assert L.mpmrb_abi_version() == 1
+    assert L.mpmrb_abi_version() == 2  # v2: cloth material fields
 
 
 def test_library_is_sm100a():
