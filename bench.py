@@ -65,6 +65,9 @@ def workload_scene(name: str, rank: int = 0) -> dict:
         sc = scenes.sand_pile_scene(half=(0.4, 0.4, 0.1))
     elif name == "cloth":
         sc = scenes.cloth_sheet_scene()
+        # start the sheet 3.5 mm above the sphere so the timed window is in contact
+        sc["cloth"][0]["center"] = [0.0, 0.0, 0.2535]
+        sc["cloth"][0]["velocity"] = [0.0, 0.0, -0.2]
     elif name == "tshirt":
         sc = scenes.tshirt_fold_scene()
     else:

@@ -448,18 +448,20 @@ def test_cloth_contact_matches_oracle(mp, which):
     gripper scene of C4): contact sets exact, positions / wrench to the
     solver's tolerance-level reassociation."""
     from paper_2503_05046_b200 import scenes
+    # heavier cloth, softer contact and a tight solver tolerance: the contact
+    # problem converges in a few iterations, so both sides reach the same
+    # minimiser (light cloth with k = 1e5 needs thousands of iterations)
     if which == "drape":
         sc = scenes.cloth_sheet_scene(n_side=15)
         sc["cloth"][0]["center"] = [0.0, 0.0, 0.2525]
-        sc["cloth"][0]["velocity"] = [0.0, 0.0, -0.3]
-        sc["contact"]["stiffness"] = 1e3
-        nsteps = 4
     else:
         sc = scenes.tshirt_fold_scene(n_side=16)
         sc["cloth"][0]["center"] = [0.0, 0.0, 0.0012]
-        sc["cloth"][0]["velocity"] = [0.0, 0.0, -0.3]
-        sc["contact"]["stiffness"] = 1e3
-        nsteps = 4
+    sc["cloth"][0]["velocity"] = [0.0, 0.0, -0.3]
+    sc["cloth"][0]["thickness"] = 1e-2
+    sc["contact"]["stiffness"] = 1e2
+    sc["solver"]["eps_r"] = 1e-6
+    nsteps = 4
     st, ref = _cloth_pair(mp, sc)
     for i in range(nsteps):
         s = mp.advance_step(st)
