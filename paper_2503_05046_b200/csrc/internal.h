@@ -102,6 +102,10 @@ struct ParticlesDev {
   const signed char* role = nullptr;
   double* tau = nullptr;   // (n,9)
   double* fext = nullptr;  // (n,3)
+  // sand: Hencky stress of the post-return-map F written by G2P for the next
+  // substep's P2G (symmetric, 6 entries); valid when *tau_valid != 0
+  double* tau_cache = nullptr;  // (n,6)
+  int* tau_valid = nullptr;
 };
 struct ClothDev {
   long long ne = 0;

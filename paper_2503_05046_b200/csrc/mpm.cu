@@ -124,6 +124,14 @@ __device__ __forceinline__ void particle_payload(const ParticlesDev& p, long lon
   } else if (role != MPMRB_CLOTH_NONE || mats[mid].kind == MPMRB_MAT_CLOTH) {
 #pragma unroll
     for (int k = 0; k < 9; ++k) tau.a[k] = 0.0;
+  } else if (p.tau_cache && mats[mid].kind == MPMRB_MAT_SAND && *p.tau_valid) {
+    const double* t6 = p.tau_cache + 6 * i;  // xx yy zz xy xz yz
+    tau.a[0] = t6[0];
+    tau.a[4] = t6[1];
+    tau.a[8] = t6[2];
+    tau.a[1] = tau.a[3] = t6[3];
+    tau.a[2] = tau.a[6] = t6[4];
+    tau.a[5] = tau.a[7] = t6[5];
   } else {
     tau = particle_stress(m3_load(p.f + 9 * i), mats[mid]);
   }
@@ -371,21 +379,74 @@ __global__ void __launch_bounds__(128) k_g2p(GridDev g, ParticlesDev p,
                                              const double* __restrict__ v_next, double dt,
                                              unsigned long long* __restrict__ clamped,
                                              int* __restrict__ health, DevStatus* st) {
+  __shared__ double s_v[128 / 32][3][kWarpTile];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const bool live = i < p.n;
   bool was_clamped = false;
-  if (i < p.n) {
-    const double h = g.h;
+  const double h = g.h;
+  // Warp tile (as in k_p2g): the sorted particles of a warp gather from a
+  // shared-memory copy of the <= kWarpTile grid velocities their stencils
+  // cover, staged with one hash lookup per block; spread warps gather from
+  // global memory directly.
+  int b[3] = {0, 0, 0};
+  if (live)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) b[a] = (int)base_cell(p.x[3 * i + a], h);
+  int lo[3], hi[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    lo[a] = __reduce_min_sync(0xffffffffu, live ? b[a] : INT_MAX);
+    hi[a] = __reduce_max_sync(0xffffffffu, live ? b[a] : INT_MIN);
+  }
+  const int nx = hi[0] - lo[0] + 3, ny = hi[1] - lo[1] + 3, nz = hi[2] - lo[2] + 3;
+  const bool tiled = (long long)nx * ny * nz <= kWarpTile &&
+                     (((lo[0] + nx - 1) >> 2) - (lo[0] >> 2) <= 1) &&
+                     (((lo[1] + ny - 1) >> 2) - (lo[1] >> 2) <= 1) &&
+                     (((lo[2] + nz - 1) >> 2) - (lo[2] >> 2) <= 1);
+  double (*tv)[kWarpTile] = s_v[wid];
+  if (tiled) {
+    const int blo0 = lo[0] >> 2, blo1 = lo[1] >> 2, blo2 = lo[2] >> 2;
+    int myblk = -1;
+    if (lane < 8) {
+      int64_t bkey;
+      if (pack_block(blo0 + ((lane >> 2) & 1), blo1 + ((lane >> 1) & 1), blo2 + (lane & 1),
+                     &bkey))
+        myblk = hash_find(g.hkeys, g.hvals, g.mask, (uint64_t)bkey);
+    }
+    const int nnode = nx * ny * nz;
+    for (int q0 = 0; q0 < nnode; q0 += 32) {
+      const int q = q0 + lane;
+      const bool inb = q < nnode;
+      const int qz = inb ? q % nz : 0, qy = inb ? (q / nz) % ny : 0, qx = inb ? q / (nz * ny) : 0;
+      const int gx = lo[0] + qx, gy = lo[1] + qy, gz = lo[2] + qz;
+      const int bsel = (((gx >> 2) - blo0) << 2) | (((gy >> 2) - blo1) << 1) | ((gz >> 2) - blo2);
+      const int blk = __shfl_sync(0xffffffffu, myblk, bsel & 7);
+      if (!inb) continue;
+      // nodes outside the allocated blocks are never in a live stencil
+      const long long node =
+          (long long)(blk < 0 ? 0 : blk) * kNodesPerBlock + (((gx & 3) << 4) | ((gy & 3) << 2) | (gz & 3));
+#pragma unroll
+      for (int d = 0; d < 3; ++d) tv[d][q] = blk < 0 ? 0.0 : v_next[3 * node + d];
+    }
+    __syncwarp();
+  }
+  if (live) {
     double xp[3] = {p.x[3 * i], p.x[3 * i + 1], p.x[3 * i + 2]};
     Stencil1 s;
     make_stencil1(xp, h, s);
     StencilBlocks sb;
-    if (!resolve_blocks(s, g.hkeys, g.hvals, g.mask, sb)) {
+    bool ok = true;
+    if (!tiled) ok = resolve_blocks(s, g.hkeys, g.hvals, g.mask, sb);
+    if (!ok) {
       raise_status(st, MPMRB_E_ALLOCATION, 30, i);
     } else {
       double vn[3] = {0.0, 0.0, 0.0};
       M3 B;
 #pragma unroll
       for (int k = 0; k < 9; ++k) B.a[k] = 0.0;
+      const int cb0 = (int)s.base[0] - lo[0], cb1 = (int)s.base[1] - lo[1],
+                cb2 = (int)s.base[2] - lo[2];
 #pragma unroll 1
       for (int ox = 0; ox < 3; ++ox) {
         const double dx = (ox - s.fx[0]) * h;
@@ -397,11 +458,20 @@ __global__ void __launch_bounds__(128) k_g2p(GridDev g, ParticlesDev p,
           for (int oz = 0; oz < 3; ++oz) {
             const double dz = (oz - s.fx[2]) * h;
             const double w = wxy * s.w[2][oz];
-            const int node = stencil_node(s, sb, ox, oy, oz);
+            double vv[3];
+            if (tiled) {
+              const int q = ((cb0 + ox) * ny + (cb1 + oy)) * nz + (cb2 + oz);
+#pragma unroll
+              for (int d = 0; d < 3; ++d) vv[d] = tv[d][q];
+            } else {
+              const int node = stencil_node(s, sb, ox, oy, oz);
+#pragma unroll
+              for (int d = 0; d < 3; ++d) vv[d] = v_next[3 * node + d];
+            }
             double wv[3];
 #pragma unroll
             for (int d = 0; d < 3; ++d) {
-              wv[d] = w * v_next[3 * node + d];
+              wv[d] = w * vv[d];
               vn[d] += wv[d];
               B(d, 0) += wv[d] * dx;
               B(d, 1) += wv[d] * dy;
@@ -429,7 +499,19 @@ __global__ void __launch_bounds__(128) k_g2p(GridDev g, ParticlesDev p,
       long long mid = p.mid[i];
       if (!cloth && mid >= 0 && mid < nmat && mats[mid].kind == MPMRB_MAT_SAND) {
         double dq = 0.0;
-        F = dp_return_map(F, mats[mid].mu, mats[mid].lam, mats[mid].dp_alpha, &dq);
+        if (p.tau_cache) {
+          M3 t;
+          F = dp_return_map_tau(F, mats[mid].mu, mats[mid].lam, mats[mid].dp_alpha, &dq, &t);
+          double* t6 = p.tau_cache + 6 * i;
+          t6[0] = t.a[0];
+          t6[1] = t.a[4];
+          t6[2] = t.a[8];
+          t6[3] = t.a[1];
+          t6[4] = t.a[2];
+          t6[5] = t.a[5];
+        } else {
+          F = dp_return_map(F, mats[mid].mu, mats[mid].lam, mats[mid].dp_alpha, &dq);
+        }
         if (p.plastic) p.plastic[i] += dq;
       }
       double xn[3];
@@ -451,6 +533,7 @@ __global__ void __launch_bounds__(128) k_g2p(GridDev g, ParticlesDev p,
       }
     }
   }
+  if (p.tau_valid && blockIdx.x == 0 && threadIdx.x == 0) *p.tau_valid = 1;  // read by the next P2G
   if (clamped) {
     unsigned b = __ballot_sync(0xffffffffu, was_clamped);
     if ((threadIdx.x & 31) == 0 && b) atomicAdd(clamped, (unsigned long long)__popc(b));

@@ -238,6 +238,8 @@ int Sim::reserve(long long n, long long nb_needed) {
     rc |= b_skeys.grow(4 * 2 * nn);
     rc |= b_svals.grow(4 * 2 * nn);
     rc |= b_cpart_user.grow(4 * (long long)(ngeom > 0 ? ngeom : 1) * nn);
+    rc |= b_taucache.grow(8 * 6 * nn);
+    rc |= b_tauvalid.grow(64);
     if (rc) return MPMRB_E_CUDA;
     double* d = b_qd.as<double>();
     q.x = d;
@@ -249,6 +251,8 @@ int Sim::reserve(long long n, long long nb_needed) {
     q.plastic = d + 26 * nn;
     q.mid = b_qmid.as<long long>();
     q.n = n;
+    q.tau_cache = b_taucache.as<double>();
+    q.tau_valid = b_tauvalid.as<int>();
   }
   rc |= b_hkeys.grow(8 * hash_cap);
   rc |= b_hvals.grow(4 * hash_cap);
@@ -544,6 +548,7 @@ int Sim::begin_step(long long epoch, int n_substeps) {
     nb_probe = nb_host;
     break;
   }
+  if (b_tauvalid.p) MPMRB_CUDA_OK(cudaMemsetAsync(b_tauvalid.p, 0, sizeof(int), c.stream));
   // sim-internal particle order for this step: sorted by (block, cell) of the
   // step-start positions, gathered from the user's arrays (scattered back in
   // end_step)

@@ -52,6 +52,7 @@ struct Sim {
   ClothDev cloth{};
   const signed char* cloth_role_user = nullptr;
   DevBuf b_invperm, b_qrole, b_qtau, b_qfext;
+  DevBuf b_taucache, b_tauvalid;  // sand: Hencky stress cached by G2P for P2G
   bool slots_init = false;
   DevBuf b_bias_stamp, b_bias_store;
 

@@ -242,4 +242,55 @@ __device__ __forceinline__ M3 dp_return_map(const M3& f, double mu, double lam, 
   return svd_compose(d.u, sig, d.v);
 }
 
+// Drucker-Prager return map that also returns the Hencky Kirchhoff stress of
+// the projected F (same SVD: U diag(2 mu eps + lam tr eps) U^T), cached for
+// the next substep's P2G instead of a second SVD there.
+__device__ __forceinline__ M3 dp_return_map_tau(const M3& f, double mu, double lam,
+                                                double alpha, double* dq, M3* tau) {
+  SVD3 d = signed_svd(f);
+  double e[3], tr = 0.0;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    e[i] = log(fmax(d.s[i], 1e-12));
+    tr += e[i];
+  }
+  double eh[3], en2 = 0.0;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    eh[i] = e[i] - tr / 3.0;
+    en2 += eh[i] * eh[i];
+  }
+  double en = sqrt(en2);
+  double dgam = en + (3.0 * lam + 2.0 * mu) / (2.0 * mu) * tr * alpha;
+  double out[3];
+  if (tr > 0.0) {
+    out[0] = out[1] = out[2] = 0.0;  // tip (tension)
+  } else if (dgam > 0.0 && en > 0.0) {
+    double k = dgam / en;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) out[i] = e[i] - k * eh[i];
+  } else {
+    *dq = 0.0;
+    double tr_e = e[0] + e[1] + e[2], dd[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) dd[i] = 2.0 * mu * e[i] + lam * tr_e;
+    *tau = svd_compose(d.u, dd, d.u);
+    return f;
+  }
+  {
+    double tr_o = out[0] + out[1] + out[2], dd[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) dd[i] = 2.0 * mu * out[i] + lam * tr_o;
+    *tau = svd_compose(d.u, dd, d.u);
+  }
+  double q2 = 0.0, sig[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    q2 += (e[i] - out[i]) * (e[i] - out[i]);
+    sig[i] = exp(out[i]);
+  }
+  *dq = sqrt(q2);
+  return svd_compose(d.u, sig, d.v);
+}
+
 }  // namespace mpmrb
