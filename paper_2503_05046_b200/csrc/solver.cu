@@ -57,8 +57,8 @@ constexpr int kMaxRed = 8;        // reduction lanes per grid reduce
 constexpr int kLS = 6;            // contacts per line-search thread held in registers
 
 // slot areas (64-bit words), see kSolverSlotWords
-constexpr long long kSlotA = 0;                                  // [2][ctas][2]  gather (1 value)
-constexpr long long kSlotB = kSlotA + 2LL * kMaxSolverCtas * 2;  // [2][ctas][4]  group (2 values)
+constexpr long long kSlotA = 0;                                  // [2][ctas][6]  gather (3 values)
+constexpr long long kSlotB = kSlotA + 2LL * kMaxSolverCtas * 6;  // [2][ctas][4]  group (2 values)
 constexpr long long kSlotC = kSlotB + 2LL * kMaxSolverCtas * 4;  // [2][4]        broadcast (2)
 constexpr long long kSlotL = kSlotC + 2LL * 4;                     // [2][4]        group leader sum
 
@@ -874,8 +874,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
     }
     const double a1 = s[5], a2 = s[6];
 
-    // ---- D: dvc = R J dv and the phi'(0) contact term (solver.py:305-310, 269)
-    double r0 = 0.0;
+    // ---- D: dvc = R J dv, the phi'(0) contact term (solver.py:305-310, 269)
+    // and the first line-search evaluation, which is always at alpha = 1
+    // (solver.py:276): its contact sums travel with phi'(0) to the group
+    double r0 = 0.0, r1 = 0.0, r1dd = 0.0;
     cta_start();
     const bool dbg = a.debug && it == 5 && blockIdx.x == 0 && threadIdx.x == 0;
     unsigned long long td[6] = {0, 0, 0, 0, 0, 0};
@@ -898,7 +900,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
           vc[d] = a.vc[3 * c + d];
         }
         double dd2 = 0.0;
-        ls_terms(cm, inv_eps, vc, dvc, a.cvhat[c], a.cmug[c], 0.0, r0, dd2);
+        const double vh = a.cvhat[c], mg = a.cmug[c];
+        ls_terms(cm, inv_eps, vc, dvc, vh, mg, 0.0, r0, dd2);
+        ls_terms(cm, inv_eps, vc, dvc, vh, mg, 1.0, r1, r1dd);
         if (dbg) td[3] = gtime() + (r0 == 12345.0);
       }
     }
@@ -911,29 +915,37 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
       printf("D timeline (ns): frame %llu gather %llu ls %llu warp %llu cta %llu\n",
              td[1] - td[0], td[2] - td[1], td[3] - td[2], td[4] - td[3], td[5] - td[4]);
     }
-    // hand the contact data and the phi'(0) partials to the group
-    double d0s = 0.0;
+    // hand the contact data and the phi'(0) / alpha = 1 partials to the group
+    double d0s = 0.0, e1s = 0.0, e1dd = 0.0;
     if (nctas == 1) {
-      double rr[1] = {r0}, ss[1];
-      group_reduce<1>(1, a.slots, tagB, rr, ss, sm);
+      double rr[3] = {r0, r1, r1dd}, ss[3];
+      group_reduce<3>(1, a.slots, tagB, rr, ss, sm);
       d0s = ss[0];
+      e1s = ss[1];
+      e1dd = ss[2];
     } else {
-      double rr[1] = {r0}, bs[1];
-      block_reduce<1>(rr, sm, bs);
-      unsigned long long* base = a.slots + kSlotA + (long long)(tagA & 1u) * kMaxSolverCtas * 2;
+      double rr[3] = {r0, r1, r1dd}, bs[3];
+      block_reduce<3>(rr, sm, bs);
+      unsigned long long* base = a.slots + kSlotA + (long long)(tagA & 1u) * kMaxSolverCtas * 6;
       if (threadIdx.x == 0) {
         fence_acq_rel_gpu();  // release this CTA's dvc writes (bar.sync made them CTA-visible)
-        slot_publish<1>(base + 2LL * blockIdx.x, bs, tagA);
+        slot_publish<3>(base + 6LL * blockIdx.x, bs, tagA);
       }
       if (in_group && threadIdx.x < 32) {
-        double r[1];
-        slot_poll_sum<1, (kMaxSolverCtas + 31) / 32>(base, nctas, tagA, r);
+        double r[3];
+        slot_poll_sum<3, (kMaxSolverCtas + 31) / 32>(base, nctas, tagA, r);
         fence_acq_rel_gpu();  // acquire: the producers' dvc writes are visible below
-        if (threadIdx.x == 0) s_bc[0] = r[0];
+        if (threadIdx.x == 0) {
+          s_bc[0] = r[0];
+          s_bc[1] = r[1];
+          s_bc[2] = r[2];
+        }
       }
       ++tagA;
       __syncthreads();
       d0s = s_bc[0];
+      e1s = s_bc[1];
+      e1dd = s_bc[2];
       __syncthreads();
     }
     lap(2);
@@ -968,27 +980,32 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
         int evals = 0;
         for (int ev = 1; ev <= a.ls_max; ++ev) {
           unsigned long long tls0 = prof ? gtime() : 0ull;
-          double rr[2] = {0.0, 0.0};
-#pragma unroll
-          for (int j = 0; j < kLS; ++j) ls_terms_rec(cm, eps2, inv_eps, lv[j], alpha, rr[0], rr[1]);
-          for (long long c = gtid + kLS * gthr; c < nc; c += gthr) {
-            double vc[3], dvc[3];
-#pragma unroll
-            for (int d = 0; d < 3; ++d) {
-              vc[d] = __ldcg(&a.vc[3 * c + d]);
-              dvc[d] = __ldcg(&a.dvc[3 * c + d]);
-            }
-            ls_terms(cm, inv_eps, vc, dvc, __ldcg(&a.cvhat[c]), __ldcg(&a.cmug[c]), alpha, rr[0],
-                     rr[1]);
-          }
           double ss[2];
-          unsigned long long tls1 = prof ? gtime() : 0ull;
-          if (CL > 1) cluster_reduce<2>(CL, s_cl, cpar, rr, ss, sm);
-          else group_reduce<2>(G, a.slots, tagB, rr, ss, sm, a.ls_mode);
-          if (prof) {
-            unsigned long long tls2 = gtime();
-            pt[12] += tls1 - tls0;
-            pt[13] += tls2 - tls1;
+          if (ev == 1) {  // alpha = 1: summed in phase D
+            ss[0] = e1s;
+            ss[1] = e1dd;
+          } else {
+            double rr[2] = {0.0, 0.0};
+#pragma unroll
+            for (int j = 0; j < kLS; ++j) ls_terms_rec(cm, eps2, inv_eps, lv[j], alpha, rr[0], rr[1]);
+            for (long long c = gtid + kLS * gthr; c < nc; c += gthr) {
+              double vc[3], dvc[3];
+#pragma unroll
+              for (int d = 0; d < 3; ++d) {
+                vc[d] = __ldcg(&a.vc[3 * c + d]);
+                dvc[d] = __ldcg(&a.dvc[3 * c + d]);
+              }
+              ls_terms(cm, inv_eps, vc, dvc, __ldcg(&a.cvhat[c]), __ldcg(&a.cmug[c]), alpha, rr[0],
+                       rr[1]);
+            }
+            unsigned long long tls1 = prof ? gtime() : 0ull;
+            if (CL > 1) cluster_reduce<2>(CL, s_cl, cpar, rr, ss, sm);
+            else group_reduce<2>(G, a.slots, tagB, rr, ss, sm, a.ls_mode);
+            if (prof) {
+              unsigned long long tls2 = gtime();
+              pt[12] += tls1 - tls0;
+              pt[13] += tls2 - tls1;
+            }
           }
           evals = ev;
           const double d = a1 + a2 * alpha + ss[0];

@@ -102,7 +102,7 @@ struct SolverArgs {
 };
 
 // words of the self-validating slot area (solver.cu)
-constexpr long long kSolverSlotWords = 2LL * kMaxSolverCtas * 2 + 2LL * kMaxSolverCtas * 4 + 2 * 4 + 2 * 4;
+constexpr long long kSolverSlotWords = 2LL * kMaxSolverCtas * 6 + 2LL * kMaxSolverCtas * 4 + 2 * 4 + 2 * 4;
 // the slot buffer is followed by chan[4] (64 B) and the barrier words (256 B)
 constexpr long long kSolverSyncBytes = 8 * kSolverSlotWords + 64 + 256;
 
