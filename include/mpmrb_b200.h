@@ -196,6 +196,18 @@ int mpmrb_node_ids(mpmrb_ctx* ctx, const mpmrb_grid_view* grid, const int64_t* c
 int mpmrb_build_stencil(mpmrb_ctx* ctx, const mpmrb_grid_view* grid, const double* x,
                         int64_t n, double* weights, int64_t* nodes, double* dpos);
 
+/* particles.py:97-136 seed_box on the GPU: the jittered lattice of cells
+ * [lo, hi) with per_axis^3 points per cell, jitter drawn exactly as
+ * numpy.random.default_rng(seed).uniform (PCG64 jump-ahead; state4_host =
+ * bit_generator state hi, lo, inc hi, lo), kept where |x - center| <= half.
+ * Bit-identical to the reference's NumPy seeding.  x_out may be NULL to count;
+ * *n_host receives the count (synchronises); MPMRB_E_CAPACITY if cap is too
+ * small. */
+int mpmrb_seed_box(mpmrb_ctx* ctx, const int64_t* lo_host, const int64_t* hi_host,
+                   int32_t per_axis, double jitter, double h, const double* center_host,
+                   const double* half_host, const uint64_t* state4_host, double* x_out,
+                   int64_t cap, int64_t* n_host);
+
 /* ------------------------------------------------------------------ transfer */
 /* transfer.py:148-248 scatter_reduce: out (n_out, nch) = sum over (rows,k). */
 int mpmrb_scatter_reduce(mpmrb_ctx* ctx, const int64_t* node_ids, const double* values,

@@ -17,7 +17,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 OUT_DIR = PKG / "_native"
 LIB = OUT_DIR / "libmpmrb_b200.so"
-SOURCES = ["capi.cu", "binning.cu", "scan.cu", "mpm.cu", "contact.cu", "solver.cu", "sim.cu", "reorder.cu", "cloth.cu"]
+SOURCES = ["capi.cu", "binning.cu", "scan.cu", "mpm.cu", "contact.cu", "solver.cu", "sim.cu", "reorder.cu", "cloth.cu", "seed.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
          "--expt-relaxed-constexpr"]

@@ -406,6 +406,20 @@ int mpmrb_detect_contacts(mpmrb_ctx* c, const double* x, int64_t n, const mpmrb_
   return rc;
 }
 
+int mpmrb_seed_box(mpmrb_ctx* c, const int64_t* lo, const int64_t* hi, int32_t per_axis,
+                   double jitter, double h, const double* center, const double* half,
+                   const uint64_t* state4, double* x_out, int64_t cap, int64_t* n_host) {
+  CHECK_CTX(c);
+  if (per_axis < 1) return set_error(MPMRB_E_INVALID, "per_axis must be >= 1");
+  long long n = 0;
+  int rc = launch_seed_box(*c, (const long long*)lo, (const long long*)hi, per_axis, jitter, h,
+                           center, half, (const unsigned long long*)state4, x_out, cap, &n);
+  *n_host = n;
+  if (rc == MPMRB_E_CAPACITY) return set_error(rc, "seed_box: %lld points, capacity %lld", n, (long long)cap);
+  if (rc) return rc;
+  return c->check_status("seed_box");
+}
+
 int mpmrb_contact_velocities(mpmrb_ctx* c, const int64_t* nodes, const double* w,
                              const double* frames, const double* bias, int64_t nc,
                              const double* v_grid, double* vc) {

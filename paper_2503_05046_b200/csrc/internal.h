@@ -132,6 +132,12 @@ int launch_g2p(Ctx& c, const GridDev& g, const ParticlesDev& p, const mpmrb_mate
                int nmat, const double* v_next, double dt, unsigned long long* clamped_dev,
                int* health_dev);
 
+// seed.cu
+int launch_seed_box(Ctx& c, const long long* lo, const long long* hi, int per_axis,
+                    double jitter, double h, const double* center, const double* half,
+                    const unsigned long long* state4, double* x_out, long long cap,
+                    long long* n_host);
+
 // cloth.cu
 int launch_cloth_forces(Ctx& c, const ClothDev& cl, const ParticlesDev& p,
                         const mpmrb_material* mats_dev, int nmat);

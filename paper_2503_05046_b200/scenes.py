@@ -17,7 +17,7 @@ from .contact_model import ContactParams
 from .coupling import SimState, StepConfig
 from .geometry import Box, Capsule, HalfSpace, Sphere
 from .materials import Material
-from .particles import concatenate, seed_box
+from .particles import concatenate
 from .solver import SolverParams
 
 
@@ -91,11 +91,13 @@ def build_particles(scene):
     """Particles of the scene's volumes followed by its cloth sheets; returns
     (ParticleSet, ClothMesh | None)."""
     from .cloth import ClothMesh
-    from .particles import ParticleSet
+    from .particles import ParticleSet, seed_box_gpu
     mats = build_materials(scene)
-    sets = [seed_box(np.asarray(v["center"]), np.asarray(v["half"]), scene["h"],
-                     mats[v["material"]], material_id=v["material"], particles_per_cell=v["ppc"],
-                     jitter=v["jitter"], velocity=tuple(v["velocity"]), seed=v["seed"])
+    # seeded on the GPU, bit-identical to the reference's NumPy seeding
+    sets = [seed_box_gpu(np.asarray(v["center"]), np.asarray(v["half"]), scene["h"],
+                         mats[v["material"]], material_id=v["material"],
+                         particles_per_cell=v["ppc"], jitter=v["jitter"],
+                         velocity=tuple(v["velocity"]), seed=v["seed"])
             for v in scene["volumes"]]
     sheets = cloth_arrays(scene)
     for a in sheets:

@@ -471,3 +471,21 @@ def test_cloth_contact_matches_oracle(mp, which):
         assert np.abs(s.wrench - r["wrench"]).max() <= 1e-5 * ws + 1e-9, i
     np.testing.assert_allclose(np_(st.particles.x), ref.x, rtol=0, atol=1e-9)
     np.testing.assert_allclose(np_(st.cloth.d3), ref.cloth.d3, rtol=0, atol=1e-7)
+
+
+# ------------------------------------------------------------------ GPU seeding
+
+@pytest.mark.parametrize("case", [((0.0, 0.0, 0.102), (0.2, 0.2, 0.1), 0.01, 8, 1.0, 0),
+                                  ((0.013, -0.02, 0.05), (0.031, 0.027, 0.019), 0.007, 27, 0.7, 11),
+                                  ((0.0, 0.0, 0.0), (0.05, 0.05, 0.05), 0.01, 1, 0.0, 3)])
+def test_gpu_seeding_is_bit_identical_to_numpy(mp, case):
+    """seed_box_gpu reproduces the reference's NumPy jittered lattice bit for
+    bit (PCG64 jump-ahead), including the in-box filter order."""
+    from paper_2503_05046_b200.particles import seed_box, seed_box_gpu
+    center, half, h, ppc, jitter, seed = case
+    m = mp.Material(1e5, 0.3, 1000.0)
+    a = seed_box(center, half, h, m, particles_per_cell=ppc, jitter=jitter, seed=seed)
+    b = seed_box_gpu(center, half, h, m, particles_per_cell=ppc, jitter=jitter, seed=seed)
+    assert a.n == b.n
+    assert torch.equal(a.x, b.x)
+    assert torch.equal(a.mass, b.mass) and torch.equal(a.volume0, b.volume0)
