@@ -363,8 +363,34 @@ def gen_steps():
     save("steps", **out)
 
 
+def gen_outputs():
+    """Reference frame bytes (outputs.py:33-42), CSV frame and contact log
+    (outputs.py:61-105) for small seeded arrays."""
+    import tempfile
+    from mpmrb import outputs as ro
+    rng = np.random.default_rng(77)
+    x = rng.normal(size=(7, 3))
+    v = rng.normal(size=(7, 3))
+    wr = rng.normal(size=(2, 6))
+    out = dict(x=x, v=v, wrench=wr, time=np.array(0.123456789))
+    with tempfile.TemporaryDirectory() as d:
+        d = Path(d)
+        ro.write_frame(d / "a.bin", 0.123456789, x, v)
+        ro.write_frame(d / "b.bin", 0.5, x)
+        ro.write_frame_csv(d / "c.csv", 0.123456789, x, v)
+        log = ro.ContactLogWriter(d / "contacts.csv", ["ground", "pusher"])
+        log.log_step(0.002, {"ground": wr[0], "pusher": wr[1]})
+        log.log_step(0.004, {"ground": -wr[0], "pusher": 2 * wr[1]})
+        log.close()
+        out["frame_v"] = np.frombuffer((d / "a.bin").read_bytes(), dtype=np.uint8)
+        out["frame_nov"] = np.frombuffer((d / "b.bin").read_bytes(), dtype=np.uint8)
+        out["frame_csv"] = np.frombuffer((d / "c.csv").read_bytes(), dtype=np.uint8)
+        out["contact_log"] = np.frombuffer((d / "contacts.csv").read_bytes(), dtype=np.uint8)
+    save("outputs", **out)
+
+
 if __name__ == "__main__":
     _import_reference()
-    which = sys.argv[1:] or ["binning", "p2g_g2p", "sdf_contacts", "solver", "steps"]
+    which = sys.argv[1:] or ["binning", "p2g_g2p", "sdf_contacts", "solver", "steps", "outputs"]
     for w in which:
         globals()[f"gen_{w}"]()

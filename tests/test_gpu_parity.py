@@ -489,3 +489,33 @@ def test_gpu_seeding_is_bit_identical_to_numpy(mp, case):
     assert a.n == b.n
     assert torch.equal(a.x, b.x)
     assert torch.equal(a.mass, b.mass) and torch.equal(a.volume0, b.volume0)
+
+
+def test_async_frame_writer_from_device(mp, tmp_path):
+    """Frames of a running simulation (device tensors, side-stream D2H) are
+    byte-identical to synchronous writes of the same state."""
+    from paper_2503_05046_b200 import outputs as po
+    from paper_2503_05046_b200 import scenes
+    st = scenes.build_state(scenes.smoke_scene())
+    w = po.AsyncFrameWriter(depth=2)
+    ref = []
+    for k in range(3):
+        s = mp.advance_step(st)
+        w.submit(tmp_path / f"f{k}.bin", s.time, st.particles.x, st.particles.v,
+                 producer=st._stream)
+        ref.append(po.frame_bytes(s.time, np_(st.particles.x), np_(st.particles.v)))
+    w.close()
+    for k in range(3):
+        assert (tmp_path / f"f{k}.bin").read_bytes() == ref[k]
+
+
+def test_bench_transfer_harness(mp, capsys):
+    """GPU bench-transfer (cli.py:48-82 schema): every mode agrees with the
+    deterministic result to the reference's fast-mode bound (1e-12 * max)."""
+    from paper_2503_05046_b200 import bench_transfer
+    assert bench_transfer.main(["--particles", "5000", "--repeats", "2"]) == 0
+    lines = capsys.readouterr().out.strip().splitlines()
+    assert lines[0] == "mode,particles,workers,ms_per_scatter,rel_diff_vs_deterministic"
+    rows = [ln.split(",") for ln in lines[1:]]
+    assert [r[0] for r in rows] == ["deterministic", "fast", "naive"]
+    assert all(float(r[4]) <= 1e-12 for r in rows)
