@@ -559,7 +559,6 @@ extern "C" int mpmrb_qn_solve(mpmrb_ctx* c, const mpmrb_problem* pr,
   if (force) a.force_ctas = atoi(force);
   const char* force_ls = getenv("MPMRB_SOLVER_LS_CTAS");
   if (force_ls) a.force_ls_ctas = atoi(force_ls);
-  a.debug = getenv("MPMRB_SOLVER_DEBUG") ? 1 : 0;
   a.ls_mode = getenv("MPMRB_LS_MODE") ? atoi(getenv("MPMRB_LS_MODE")) : 0;
   rc = launch_qn_solve(*c, a, 0);
   if (rc) return rc;

@@ -415,7 +415,6 @@ int Sim::capture_or_launch() {
   a.skip_if_no_contacts = 1;
   a.force_ctas = force_ctas;
   a.force_ls_ctas = force_ls_ctas;
-  a.debug = getenv("MPMRB_SOLVER_DEBUG") ? 1 : 0;
   a.ls_mode = getenv("MPMRB_LS_MODE") ? atoi(getenv("MPMRB_LS_MODE")) : 0;
   a.v = b_sv.as<double>();
   a.dv = b_sdv.as<double>();

@@ -560,12 +560,9 @@ __device__ __forceinline__ void node_finish(const SolverArgs& a, long long i, co
 __device__ __forceinline__ void contact_update_chunk(const SolverArgs& a, const ContactModel& cm,
                                                      long long c0, int nc, bool init,
                                                      double alpha, double* s_gw,
-                                                     const double* s_w, double& e_acc,
-                                                     bool dbg = false) {
+                                                     const double* s_w, double& e_acc) {
   const int lane = threadIdx.x & 31;
   const long long c = c0 + lane;
-  unsigned long long tu[5] = {0, 0, 0, 0, 0};
-  if (dbg) tu[0] = gtime();
   if (c < nc) {
     double R[9], vc[3], gw[3], rgr[6], vhat, mug;
     load_frame(a.frames, c, R);
@@ -585,9 +582,7 @@ __device__ __forceinline__ void contact_update_chunk(const SolverArgs& a, const 
     }
 #pragma unroll
     for (int d = 0; d < 3; ++d) a.vc[3 * c + d] = vc[d];
-    if (dbg) tu[1] = gtime() + (vc[0] == 12345.0);
     e_acc += contact_terms(cm, vc, vhat, mug, R, gw, rgr);
-    if (dbg) tu[2] = gtime() + (gw[0] == 12345.0);
     double* sg = s_gw + 9 * lane;
 #pragma unroll
     for (int d = 0; d < 3; ++d) sg[d] = gw[d];
@@ -628,11 +623,6 @@ __device__ __forceinline__ void contact_update_chunk(const SolverArgs& a, const 
     out[4] = make_double2(acc[8], 0.0);
   }
   __syncwarp();
-  if (dbg) {
-    tu[3] = gtime();
-    printf("U timeline (ns): loads %llu terms %llu pairs %llu (pairs=%d)\n", tu[1] - tu[0],
-           tu[2] - tu[1], tu[3] - tu[2], pairs);
-  }
 }
 
 __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
@@ -767,7 +757,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
     double red[8] = {0, 0, 0, 0, e_acc, 0, 0, 0};
     int reg_count = 0;
     cta_start();
-    const unsigned long long cta_t0_n = (a.debug && it == 5 && threadIdx.x == 0) ? gtime() : 0ull;
     if (it > 0) P *= (1.0 - alpha_prev);
     {
       // 4 lanes per contact node (8 nodes per warp), warp-interleaved over CTAs
@@ -841,16 +830,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
       red[6] += p2s;
     }
     if (reg_count) atomicAdd(&a.out->regularized, reg_count);
-    unsigned long long tdbg0 = (a.debug && it == 5 && threadIdx.x == 0) ? gtime() : 0ull;
     cta_stop(0);
-    unsigned long long tdbg1 = (a.debug && it == 5 && threadIdx.x == 0) ? gtime() : 0ull;
     cta_start();
     double s[8];
     reduce_all<8>(sync, parity, red, s, sm);
     cta_stop(3);
-    if (a.debug && it == 5 && threadIdx.x == 0)
-      printf("NDBG cta %d nstart %llu warp0_end %llu cta_end %llu reduce_end %llu\n", blockIdx.x,
-             cta_t0_n, tdbg0, tdbg1, gtime());
     lap(1);
     const double residual = sqrt(s[0]);
     const double threshold = a.eps_a + a.eps_r * fmax(sqrt(s[1]), sqrt(s[2]));
@@ -879,21 +863,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
     // (solver.py:276): its contact sums travel with phi'(0) to the group
     double r0 = 0.0, r1 = 0.0, r1dd = 0.0;
     cta_start();
-    const bool dbg = a.debug && it == 5 && blockIdx.x == 0 && threadIdx.x == 0;
-    unsigned long long td[6] = {0, 0, 0, 0, 0, 0};
-    if (dbg) td[0] = gtime();
     for (long long c0 = chunk0; c0 < nc; c0 += chunk_step) {
       const long long c = c0 + lane;
       if (c < nc) {
         double R[9], dvc[3], vc[3];
         load_frame(a.frames, c, R);
-        if (dbg) {
-          double sR = R[0] + R[4];
-          td[1] = gtime() + (sR == 12345.0);
-        }
         if (resident) gather_contact_sw(a, c, a.dv, R, s_w_w, lane, dvc);
         else gather_contact(a, c, a.dv, R, dvc);
-        if (dbg) td[2] = gtime() + (dvc[0] == 12345.0);
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
           a.dvc[3 * c + d] = dvc[d];
@@ -903,18 +879,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
         const double vh = a.cvhat[c], mg = a.cmug[c];
         ls_terms(cm, inv_eps, vc, dvc, vh, mg, 0.0, r0, dd2);
         ls_terms(cm, inv_eps, vc, dvc, vh, mg, 1.0, r1, r1dd);
-        if (dbg) td[3] = gtime() + (r0 == 12345.0);
       }
     }
     __syncwarp();
-    if (dbg) td[4] = gtime();
     lap(7);
     cta_stop(1);
-    if (dbg) {
-      td[5] = gtime();
-      printf("D timeline (ns): frame %llu gather %llu ls %llu warp %llu cta %llu\n",
-             td[1] - td[0], td[2] - td[1], td[3] - td[2], td[4] - td[3], td[5] - td[4]);
-    }
     // hand the contact data and the phi'(0) / alpha = 1 partials to the group
     double d0s = 0.0, e1s = 0.0, e1dd = 0.0;
     if (nctas == 1) {
@@ -1058,8 +1027,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
     for (long long c0 = chunk0; c0 < nc; c0 += chunk_step)
     {
       if (!resident) stage_weights(a, c0, nc, s_w_w);
-      contact_update_chunk(a, cm, c0, nc, false, alpha_final, s_gw_w, s_w_w, e_acc,
-                           a.debug && it == 5 && blockIdx.x == 0 && threadIdx.x == 0);
+      contact_update_chunk(a, cm, c0, nc, false, alpha_final, s_gw_w, s_w_w, e_acc);
     }
     lap(8);
     cta_stop(2);

@@ -74,7 +74,6 @@ struct SolverArgs {
   int skip_if_no_contacts;
   int force_ctas;  // 0 = automatic
   int force_ls_ctas;  // 0 = automatic
-  int debug;          // MPMRB_SOLVER_DEBUG: printf a phase timeline of iteration 5
   int ls_mode;        // line-search group reduction: 0 all-to-all, 1 + backoff, 2 leader
   // work (device)
   double* v;         // (nd,3) solution (contact nodes during the solve, all at the end)
