@@ -2,7 +2,7 @@
 """Benchmark of the fused MPM + convex-contact coupling step on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload sand|sand1m|cube]
+                    [--workload sand|sand1m|cube|cloth|tshirt|multi4m]
 
 A "step" is one rigid coupling step (N substeps of P2G -> grid update ->
 contact detection -> device quasi-Newton solve -> G2P) of the configuration
@@ -49,7 +49,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["sand", "sand1m", "cube", "cloth", "tshirt"],
+    ap.add_argument("--workload", choices=["sand", "sand1m", "cube", "cloth", "tshirt", "multi4m"],
                     default="sand")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -70,6 +70,17 @@ def workload_scene(name: str, rank: int = 0) -> dict:
         sc["cloth"][0]["velocity"] = [0.0, 0.0, -0.2]
     elif name == "tshirt":
         sc = scenes.tshirt_fold_scene()
+    elif name == "multi4m":
+        sc = scenes.multi_material_scene()
+        # start the block on the floor and the pusher 1 mm clear (inside the
+        # contact margin) so the timed window is contact-loaded from t = 0
+        for vol in sc["volumes"]:
+            vol["center"][2] = vol["half"][2]
+        pusher = sc["bodies"][1]
+        x0 = -sc["volumes"][1]["center"][0] * 2 - 0.05 - 0.001
+        pusher["position"][0] = x0
+        pusher["trajectory"]["positions"] = [[x0, 0, pusher["position"][2]],
+                                             [x0 + 2.0, 0, pusher["position"][2]]]
     else:
         sc = scenes.elastic_cube_scene()
     return env_scene(sc, rank)  # independent environment per rank
@@ -85,6 +96,9 @@ def workload_name(name: str, n: int, N: int) -> str:
         "cloth": f"cloth sheet over a sphere (configs[2]): {n} particles (vertices + faces), "
                  f"codimensional cloth, dt=2e-3, N={N}",
         "tshirt": f"cloth fold with two grippers (configs[3]): {n} particles, dt=2e-3, N={N}",
+        "multi4m": f"multi-material block (configs[4], 1 GPU): {n} particles, elastic | "
+                   f"Drucker-Prager sand split at x=0, h=5 mm, floor + kinematic pusher box, "
+                   f"dt=2e-3, N={N} substeps",
     }[name]
 
 
@@ -135,7 +149,8 @@ def run_reference(args):
     os.environ["OMP_NUM_THREADS"] = "1"
     # one warm-up sample on a 1/64 subset keeps imports/allocators warm
     small = json.loads(json.dumps(scene))
-    small["volumes"][0]["half"] = [a / 4 for a in small["volumes"][0]["half"]]
+    for vol in small.get("volumes", []):
+        vol["half"] = [a / 4 for a in vol["half"]]
     cpu_oracle_sample(small)
     vals, secs = [], []
     budget = 150.0
@@ -153,8 +168,7 @@ def run_reference(args):
                 ms_per_step=float(np.mean(secs)) * 1e3 * scene["substeps"],
                 higher_is_better=True, scaling="weak", vs_baseline=None, dtype="f64",
                 data="synthetic",
-                config=dict(workload=f"sand pile (configs[1]), {n} particles, DP sand, "
-                                     "kinematic pusher, dt=2e-3, N=10",
+                config=dict(workload=workload_name(args.workload, n, scene["substeps"]),
                             substeps=scene["substeps"], samples_timed=len(vals)),
                 cpu_baseline=dict(value=value, unit=UNIT, cores=1, kind="port",
                                   sample=(f"{len(vals)} x one substep of the full workload "

@@ -170,7 +170,9 @@ def load_library(path: str | os.PathLike | None = None) -> C.CDLL:
     with _lock:
         if _lib is not None:
             return _lib
-        p = Path(path) if path else LIB_PATH
+        # MPMRB_LIB_PATH: an alternative build of the same library (A/B
+        # experiments, tools/build_variant.sh)
+        p = Path(path) if path else Path(os.environ.get("MPMRB_LIB_PATH", LIB_PATH))
         if not p.exists():
             raise NativeUnavailable(
                 f"{p} is missing; build it with `python -m paper_2503_05046_b200.build` "

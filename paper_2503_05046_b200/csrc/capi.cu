@@ -560,6 +560,8 @@ extern "C" int mpmrb_qn_solve(mpmrb_ctx* c, const mpmrb_problem* pr,
   const char* force_ls = getenv("MPMRB_SOLVER_LS_CTAS");
   if (force_ls) a.force_ls_ctas = atoi(force_ls);
   a.ls_mode = getenv("MPMRB_LS_MODE") ? atoi(getenv("MPMRB_LS_MODE")) : 0;
+  a.node_lanes = getenv("MPMRB_NODE_LANES") ? atoi(getenv("MPMRB_NODE_LANES")) : 0;
+  if (a.node_lanes != 2 && a.node_lanes != 4) a.node_lanes = 0;
   rc = launch_qn_solve(*c, a, 0);
   if (rc) return rc;
   SolveOut h{};

@@ -748,6 +748,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
   }
   lap(0);
 
+  // lanes per contact node in phase N: 4 (more entries in flight per node)
+  // while the nodes fit in <= 4 passes of the grid, else 2 (twice the nodes in
+  // flight per warp; tools/gpu_ab.sh: 16.4 -> 10.7 us of N work per iteration
+  // at 2M particles, no gain at 256k)
+  const int NL = a.node_lanes > 0 ? a.node_lanes
+                                  : (n_cn > (long long)nctas * kThreads ? 2 : 4);
   int iterations = 0, ls_evals_total = 0, status = 0;
   bool converged = false;
   double alpha_prev = 0.0;  // pending v += alpha dv, applied by each node's owner in N
@@ -759,10 +765,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
     cta_start();
     if (it > 0) P *= (1.0 - alpha_prev);
     {
-      // 4 lanes per contact node (8 nodes per warp), warp-interleaved over CTAs
-      const int grp = lane >> 2, gl = lane & 3;
+      // NL lanes per contact node (32 / NL nodes per warp), warp-interleaved
+      // over CTAs
+      const int kNPW = 32 / NL;
+      const int grp = lane / NL, gl = lane & (NL - 1);
       const long long vw = (long long)wid * nctas + blockIdx.x, nw = (long long)nctas * kWarps;
-      for (long long t0 = vw * 8; t0 < n_cn; t0 += nw * 8) {
+      for (long long t0 = vw * kNPW; t0 < n_cn; t0 += nw * kNPW) {
         const long long t = t0 + grp;
         const bool live = t < n_cn;
         const int4 rec = live ? a.su.cn_rec[t] : make_int4(0, 0, 0, 0);
@@ -785,10 +793,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
         }
         double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
         // up to 4 entries per lane per pass: all keys, then all records, in flight
-        for (int eb = rec.y + gl; eb < rec.z; eb += 16) {
+        for (int eb = rec.y + gl; eb < rec.z; eb += 4 * NL) {
           int key[4];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) key[j] = (eb + 4 * j < rec.z) ? __ldg(&a.su.ent[eb + 4 * j]) : -1;
+          for (int j = 0; j < 4; ++j)
+            key[j] = (eb + NL * j < rec.z) ? __ldg(&a.su.ent[eb + NL * j]) : -1;
           double2 q[4][5];
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
@@ -815,7 +824,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
 #pragma unroll
         for (int q = 0; q < 9; ++q)
 #pragma unroll
-          for (int o = 2; o > 0; o >>= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
+          for (int o = NL / 2; o > 0; o >>= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
         if (live && gl == 0) node_finish(a, i, nin, acc, acc + 3, red, reg_count);
       }
     }

@@ -75,6 +75,7 @@ struct SolverArgs {
   int force_ctas;  // 0 = automatic
   int force_ls_ctas;  // 0 = automatic
   int ls_mode;        // line-search group reduction: 0 all-to-all, 1 + backoff, 2 leader
+  int node_lanes;     // lanes per contact node in phase N (2 or 4; 0 = automatic)
   // work (device)
   double* v;         // (nd,3) solution (contact nodes during the solve, all at the end)
   double* dv;        // (nd,3)

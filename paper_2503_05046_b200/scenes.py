@@ -203,6 +203,36 @@ def sand_pile_scene(half=(0.2, 0.2, 0.1), h=0.01, model="sand") -> dict:
                                          position=[0, 0, 0], quat=[1, 0, 0, 0], mu=0.5)])])
 
 
+def multi_material_scene(half=(0.25, 0.25, 0.125), h=0.005, substeps=20) -> dict:
+    """C5: a block of two materials split at x = 0 (elastic on x < 0,
+    Drucker-Prager sand on x > 0), 4.0M particles at the default size
+    (100 x 100 x 50 cells x 8 ppc), on a floor and pushed from
+    -x by a kinematic box starting 5 mm clear at +0.2 m/s.  N = 20 substeps
+    keeps the sand's elastic wave CFL at h = 5 mm where C2 has it at 10 mm."""
+    dt = 2e-3
+    hx, hy, hz = half
+    push_half = (0.05, hy, 0.05)
+    x0 = -hx - 0.005 - push_half[0]
+    z0 = push_half[2] + 0.005
+    zc = hz + 0.002
+    return dict(h=h, dt=dt, substeps=substeps, gravity=[0, 0, -9.81],
+                contact=dict(stiffness=1e5, tau_d=dt, eps_v=1e-4, margin=None),
+                solver=dict(eps_r=5e-2),
+                materials=[dict(E=1e5, nu=0.3, rho=1000.0, model="elastic"),
+                           dict(E=3.5e5, nu=0.3, rho=1500.0, model="sand", friction_angle=30.0)],
+                volumes=[dict(center=[-hx / 2, 0, zc], half=[hx / 2, hy, hz], material=0, ppc=8,
+                              jitter=1.0, seed=0, velocity=[0, 0, 0]),
+                         dict(center=[hx / 2, 0, zc], half=[hx / 2, hy, hz], material=1, ppc=8,
+                              jitter=1.0, seed=1, velocity=[0, 0, 0])],
+                bodies=[_floor(0.5),
+                        dict(name="pusher", kinematic=True, position=[x0, 0, z0],
+                             quat=[1, 0, 0, 0],
+                             trajectory=dict(times=[0.0, 10.0],
+                                             positions=[[x0, 0, z0], [x0 + 2.0, 0, z0]]),
+                             geoms=[dict(shape="box", half_extents=list(push_half),
+                                         position=[0, 0, 0], quat=[1, 0, 0, 0], mu=0.5)])])
+
+
 def host_particles(scene: dict) -> dict:
     """Seed the scene's particle volumes on the HOST as NumPy arrays (the same
     jittered lattice as seed_box, particles.py:113-136): x, v, f, c, mass, vol,
