@@ -557,10 +557,27 @@ __device__ __forceinline__ void node_finish(const SolverArgs& a, long long i, co
 // contact velocity, contact gradient / Hessian / energy, then the per
 // (group, slot) sums (groups never cross a chunk).  Warp-synchronous; s_gw is
 // this warp's 32 x 9 scratch.
+// The groups of a chunk: first group, group count, and (one per lane) the
+// group bounds; constant over a solve, so resident warps load them once.
+struct ChunkGroups {
+  int g0, ngc, my_gs, gs_32;
+};
+__device__ __forceinline__ ChunkGroups chunk_groups(const SolverArgs& a, long long c0, int nc) {
+  const int lane = threadIdx.x & 31;
+  const long long c_last = (c0 + kChunk < nc ? c0 + kChunk : nc) - 1;
+  ChunkGroups cg;
+  cg.g0 = a.su.grp_of[c0];
+  cg.ngc = a.su.grp_of[c_last] - cg.g0 + 1;  // <= 32 groups in a chunk
+  cg.my_gs = (lane <= cg.ngc) ? a.su.grp_start[cg.g0 + lane] : 0;
+  cg.gs_32 = (cg.ngc == 32) ? a.su.grp_start[cg.g0 + 32] : 0;
+  return cg;
+}
+
 __device__ __forceinline__ void contact_update_chunk(const SolverArgs& a, const ContactModel& cm,
                                                      long long c0, int nc, bool init,
                                                      double alpha, double* s_gw,
-                                                     const double* s_w, double& e_acc) {
+                                                     const double* s_w, double& e_acc,
+                                                     const ChunkGroups& cg) {
   const int lane = threadIdx.x & 31;
   const long long c = c0 + lane;
   if (c < nc) {
@@ -590,13 +607,8 @@ __device__ __forceinline__ void contact_update_chunk(const SolverArgs& a, const 
     for (int q = 0; q < 6; ++q) sg[3 + q] = rgr[q];
   }
   __syncwarp();
-  const long long c_last = (c0 + kChunk < nc ? c0 + kChunk : nc) - 1;
-  const int g0 = a.su.grp_of[c0], g1 = a.su.grp_of[c_last];
-  const int ngc = g1 - g0 + 1;  // <= 32 groups in a chunk
+  const int g0 = cg.g0, ngc = cg.ngc, my_gs = cg.my_gs, gs_32 = cg.gs_32;
   const int pairs = ngc * 27;
-  // group bounds of the chunk, one group per lane (one load round trip)
-  const int my_gs = (lane <= ngc) ? a.su.grp_start[g0 + lane] : 0;
-  const int gs_32 = (ngc == 32) ? a.su.grp_start[g0 + 32] : 0;
   for (int p0 = 0; p0 < pairs; p0 += 32) {
     const int p = p0 + lane;
     const int gl = p < pairs ? p / 27 : 0, k = p - gl * 27;
@@ -713,6 +725,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
   // every warp owns at most one chunk: its weights stay staged for the solve
   const bool resident = (long long)nc <= (long long)nctas * kThreads;
 
+  ChunkGroups my_cg{0, 0, 0, 0};  // resident warps: the groups of their one chunk
   // ---- init: contact nodes v = v0; free-node sums; contacts
   for (long long t = vt; t < n_cn; t += nthr) {
     const long long i = a.su.cn[t];
@@ -737,8 +750,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
     }
     for (long long c0 = chunk0; c0 < nc; c0 += chunk_step)
     {
+      const ChunkGroups cgr = chunk_groups(a, c0, nc);
+      if (resident) my_cg = cgr;
       stage_weights(a, c0, nc, s_w_w);
-      contact_update_chunk(a, cm, c0, nc, true, 0.0, s_gw_w, s_w_w, e_acc);
+      contact_update_chunk(a, cm, c0, nc, true, 0.0, s_gw_w, s_w_w, e_acc, cgr);
     }
     double s3[3];
     reduce_all<3>(sync, parity, r3, s3, sm);  // also publishes vc / cellsum grid-wide
@@ -749,11 +764,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
   lap(0);
 
   // lanes per contact node in phase N: 4 (more entries in flight per node)
-  // while the nodes fit in <= 4 passes of the grid, else 2 (twice the nodes in
-  // flight per warp; tools/gpu_ab.sh: 16.4 -> 10.7 us of N work per iteration
-  // at 2M particles, no gain at 256k)
+  // while the contact nodes fit in one pass of the grid, else 2 (twice the
+  // nodes in flight per warp; tools/gpu_ab.sh: 16.4 -> 10.7 us of N work per
+  // iteration with 31k contact nodes, no change with 9k)
   const int NL = a.node_lanes > 0 ? a.node_lanes
-                                  : (n_cn > (long long)nctas * kThreads ? 2 : 4);
+                                  : (4LL * n_cn > (long long)nctas * kThreads ? 2 : 4);
   int iterations = 0, ls_evals_total = 0, status = 0;
   bool converged = false;
   double alpha_prev = 0.0;  // pending v += alpha dv, applied by each node's owner in N
@@ -1035,8 +1050,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
     cta_start();
     for (long long c0 = chunk0; c0 < nc; c0 += chunk_step)
     {
-      if (!resident) stage_weights(a, c0, nc, s_w_w);
-      contact_update_chunk(a, cm, c0, nc, false, alpha_final, s_gw_w, s_w_w, e_acc);
+      if (resident) {
+        contact_update_chunk(a, cm, c0, nc, false, alpha_final, s_gw_w, s_w_w, e_acc, my_cg);
+      } else {
+        const ChunkGroups cgr = chunk_groups(a, c0, nc);  // loads overlap the staging
+        stage_weights(a, c0, nc, s_w_w);
+        contact_update_chunk(a, cm, c0, nc, false, alpha_final, s_gw_w, s_w_w, e_acc, cgr);
+      }
     }
     lap(8);
     cta_stop(2);
