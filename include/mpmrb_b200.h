@@ -273,6 +273,19 @@ int mpmrb_qn_solve(mpmrb_ctx* ctx, const mpmrb_problem* prob_host,
                    const mpmrb_solver_params* params_host, const double* v0, double* v,
                    double* gamma, double* objective, double* residual, double* threshold,
                    double* alpha, mpmrb_solve_report* report_host);
+/* The same solve with free nodes held outside the problem (slab domain
+ * decomposition: the contact problem is gathered to one rank, every rank keeps
+ * its contact-free active nodes).  ext_free_host[3] = the external nodes'
+ * S0 = sum m |v0 - v*|^2, Q0 = sum m |v*|^2, Q1 = sum m v*.(v0 - v*); they
+ * enter every reduction in closed form (their g = m (v - v*), H = m I), and
+ * *p_host receives P = prod(1 - alpha) so that each rank finishes its free
+ * nodes as v = v* + P (v0 - v*).  No reference counterpart: the reference is
+ * single-process. */
+int mpmrb_qn_solve_ext(mpmrb_ctx* ctx, const mpmrb_problem* prob_host,
+                       const mpmrb_solver_params* params_host, const double* v0,
+                       const double* ext_free_host, double* v, double* gamma, double* objective,
+                       double* residual, double* threshold, double* alpha, double* p_host,
+                       mpmrb_solve_report* report_host);
 
 /* Solver phase timers (globaltimer ns, accumulated over solves since the last
  * reset) when the context was created with MPMRB_SOLVER_PROF=1, else zeros:

@@ -137,6 +137,9 @@ _SIGS = {
     "mpmrb_contact_velocities": ([_P, _P, _P, _P, _P, _I64, _P, _P], C.c_int),
     "mpmrb_qn_solve": ([_P, C.POINTER(Problem), C.POINTER(SolverParamsC), _P, _P, _P, _P, _P, _P,
                         _P, C.POINTER(SolveReportC)], C.c_int),
+    "mpmrb_qn_solve_ext": ([_P, C.POINTER(Problem), C.POINTER(SolverParamsC), _P,
+                            C.POINTER(C.c_double), _P, _P, _P, _P, _P, _P,
+                            C.POINTER(C.c_double), C.POINTER(SolveReportC)], C.c_int),
     "mpmrb_solver_profile": ([_P, C.POINTER(C.c_uint64), C.c_int32], C.c_int),
     "mpmrb_solver_profile_cta": ([_P, C.POINTER(C.c_uint64)], C.c_int),
     "mpmrb_sim_create":([_P, C.POINTER(C.c_void_p)], C.c_int),

@@ -447,10 +447,32 @@ __global__ void k_problem_layout(const long long* __restrict__ nodes, const doub
 }  // namespace
 }  // namespace mpmrb
 
+static int qn_solve_impl(mpmrb_ctx* c, const mpmrb_problem* pr, const mpmrb_solver_params* sp,
+                         const double* v0, const double* ext_free, double* v, double* gamma,
+                         double* objective, double* residual, double* threshold, double* alpha,
+                         double* p_host, mpmrb_solve_report* rep);
+
 extern "C" int mpmrb_qn_solve(mpmrb_ctx* c, const mpmrb_problem* pr,
                               const mpmrb_solver_params* sp, const double* v0, double* v,
                               double* gamma, double* objective, double* residual,
                               double* threshold, double* alpha, mpmrb_solve_report* rep) {
+  return qn_solve_impl(c, pr, sp, v0, nullptr, v, gamma, objective, residual, threshold, alpha,
+                       nullptr, rep);
+}
+
+extern "C" int mpmrb_qn_solve_ext(mpmrb_ctx* c, const mpmrb_problem* pr,
+                                  const mpmrb_solver_params* sp, const double* v0,
+                                  const double* ext_free_host, double* v, double* gamma,
+                                  double* objective, double* residual, double* threshold,
+                                  double* alpha, double* p_host, mpmrb_solve_report* rep) {
+  return qn_solve_impl(c, pr, sp, v0, ext_free_host, v, gamma, objective, residual, threshold,
+                       alpha, p_host, rep);
+}
+
+static int qn_solve_impl(mpmrb_ctx* c, const mpmrb_problem* pr, const mpmrb_solver_params* sp,
+                         const double* v0, const double* ext_free, double* v, double* gamma,
+                         double* objective, double* residual, double* threshold, double* alpha,
+                         double* p_host, mpmrb_solve_report* rep) {
   CHECK_CTX(c);
   long long nd = pr->n_nodes, nc = pr->n_contacts;
   long long ncc = nc > 0 ? nc : 1, ndd = nd > 0 ? nd : 1;
@@ -562,10 +584,15 @@ extern "C" int mpmrb_qn_solve(mpmrb_ctx* c, const mpmrb_problem* pr,
   a.ls_mode = getenv("MPMRB_LS_MODE") ? atoi(getenv("MPMRB_LS_MODE")) : 0;
   a.node_lanes = getenv("MPMRB_NODE_LANES") ? atoi(getenv("MPMRB_NODE_LANES")) : 0;
   if (a.node_lanes != 2 && a.node_lanes != 4) a.node_lanes = 0;
+  for (int k = 0; k < 3; ++k) a.ext_free[k] = ext_free ? ext_free[k] : 0.0;
+  double* p_dev = reinterpret_cast<double*>(misc + 2304 + 256);  // after SolveOut
+  a.p_out = p_dev;
   rc = launch_qn_solve(*c, a, 0);
   if (rc) return rc;
   SolveOut h{};
   MPMRB_CUDA_OK(cudaMemcpyAsync(&h, so, sizeof(SolveOut), cudaMemcpyDeviceToHost, c->stream));
+  if (p_host)
+    MPMRB_CUDA_OK(cudaMemcpyAsync(p_host, p_dev, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   rc = c->check_status("quasi_newton_solve");
   if (rc) return rc;
   rep->converged = h.converged;

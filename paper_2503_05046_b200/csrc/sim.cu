@@ -418,6 +418,8 @@ int Sim::capture_or_launch() {
   a.ls_mode = getenv("MPMRB_LS_MODE") ? atoi(getenv("MPMRB_LS_MODE")) : 0;
   a.node_lanes = getenv("MPMRB_NODE_LANES") ? atoi(getenv("MPMRB_NODE_LANES")) : 0;
   if (a.node_lanes != 2 && a.node_lanes != 4) a.node_lanes = 0;
+  a.ext_free[0] = a.ext_free[1] = a.ext_free[2] = 0.0;
+  a.p_out = nullptr;
   a.v = b_sv.as<double>();
   a.dv = b_sdv.as<double>();
   a.vc = b_svc.as<double>();

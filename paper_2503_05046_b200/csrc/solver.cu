@@ -654,6 +654,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
       a.out->status = 0;
       a.out->n_contacts = 0;
       a.out->n_dofs = 3 * nd;
+      if (a.p_out) *a.p_out = 1.0;
     }
     return;
   }
@@ -757,9 +758,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
     }
     double s3[3];
     reduce_all<3>(sync, parity, r3, s3, sm);  // also publishes vc / cellsum grid-wide
-    S0 = s3[0];
-    Q0 = s3[1];
-    Q1 = s3[2];
+    S0 = s3[0] + a.ext_free[0];
+    Q0 = s3[1] + a.ext_free[1];
+    Q1 = s3[2] + a.ext_free[2];
   }
   lap(0);
 
@@ -1114,6 +1115,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
     a.out->status = status;
     a.out->n_contacts = nc;
     a.out->n_dofs = 3 * nd;
+    if (a.p_out) *a.p_out = P;
     a.chan[0] = tagA;
     a.chan[1] = tagB;
     a.chan[2] = tagC;

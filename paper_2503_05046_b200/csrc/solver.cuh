@@ -76,6 +76,11 @@ struct SolverArgs {
   int force_ls_ctas;  // 0 = automatic
   int ls_mode;        // line-search group reduction: 0 all-to-all, 1 + backoff, 2 leader
   int node_lanes;     // lanes per contact node in phase N (2 or 4; 0 = automatic)
+  // free nodes held outside this problem (slab decomposition, slab.py): their
+  // sums S0 = sum m |v0 - v*|^2, Q0 = sum m |v*|^2, Q1 = sum m v*.(v0 - v*),
+  // added to the problem's own; the final P = prod(1 - alpha) goes to p_out
+  double ext_free[3];
+  double* p_out;      // device, optional
   // work (device)
   double* v;         // (nd,3) solution (contact nodes during the solve, all at the end)
   double* dv;        // (nd,3)

@@ -7,8 +7,8 @@ device time reduced as the MAX over ranks.  One process per GPU, launched by
 ``torch.distributed.run``; NCCL for the timing/statistics reductions on the
 GPU box, gloo for the CPU tests (tests/test_distributed.py).
 
-Slab decomposition of one large scene (P2G halo exchange + line-search scalar
-all-reduce) is not built yet; see DESIGN.md §7.
+Slab decomposition of one large scene (P2G halo exchange, the contact problem
+gathered to one rank) is ``slab.py``; see DESIGN.md §7.
 """
 
 from __future__ import annotations

@@ -1,0 +1,486 @@
+"""Slab domain decomposition of ONE scene over ranks (second
+bullet): the north-star's "slab domain decomposition of large scenes with P2G
+halo exchange".  No reference counterpart: the reference is single-process.
+
+Layout.  Rank r owns the particles whose x (``axis``) lies in the slab
+[X_r, X_{r+1}); the interior bounds are equal-count quantiles of the initial
+positions snapped to grid-block boundaries (multiples of 4h).  Particles
+migrate once per rigid step, at its start (the reference builds its sort plan
+once per step too, ``coupling.py:168-219``).  Each substep (``coupling.py:
+115-150``) then runs the same fine-grained device operators as
+``coupling.advance_step_ops`` on the rank's particles, with three exchanges:
+
+1. **P2G halo reduce.**  After P2G, every rank sends the 7 node channels of its
+   blocks within two blocks of a slab boundary (particles drift at most that
+   far within a step; checked) and adds the channels of every block it shares
+   with a neighbour.  A block is shared by at most two ranks and IEEE addition
+   commutes, so both copies of a shared node hold bitwise-identical sums and
+   the grid update agrees on both sides.
+2. **Contact problem gather.**  The contact solve is latency-bound (DESIGN.md
+   §3): splitting its line search across GPUs would put a cross-GPU scalar
+   all-reduce in each of its ~500 reductions per substep.  Instead the contact
+   problem — contacts with their stencils keyed by global node coordinates,
+   the contact nodes' (m, v*, v_k), and three scalars per rank summarising its
+   contact-free active nodes — is gathered to rank 0 once per substep and
+   solved by ``quasi_newton_solve_ext``.  Contact-free nodes enter every
+   reduction of the solve in closed form (g = m (v - v*), H = m I), so the
+   global problem is exactly the single-scene one.
+3. **Solution scatter.**  Rank 0 broadcasts the contact-node velocities,
+   P = prod(1 - alpha) (free nodes finish at v* + P (v_k - v*)), the impulses
+   and the solve report.  Reactions accumulate per rank; the step wrench is
+   all-reduced, so every rank advances the (replicated) rigid bodies alike.
+
+Node ownership (each active node counted once in the free-node sums and the
+statistics): a node of a block shared with a neighbour belongs to the rank
+whose slab contains the node's coordinate; a node of an unshared block belongs
+to the only rank that has it.
+
+The communication layer works on CPU tensors under gloo (tests, and several
+ranks sharing one GPU) and on device tensors under NCCL.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from .collision import BiasCache, contact_velocities, detect_contacts
+from .contact_model import normal_impulse
+from .coupling import ImpulseAccumulator, SimState, StepSummary, _rigid_update
+from .grid import BLOCK_NODES, COORD_BIAS, SparseGrid
+from .mpm import build_stencil, grid_to_particle, grid_update, particle_to_grid
+from .particles import ParticleSet
+from .solver import ContactProblem, SolveReport, quasi_newton_solve_ext
+from .transfer import build_sort_plan, plan_staleness
+
+BLOCK_EDGE = 4
+HALO_BLOCKS = 2       # blocks on each side of a slab bound that may be shared
+MIN_SLAB_BLOCKS = 2 * HALO_BLOCKS  # halo bands of adjacent bounds never overlap
+PARTICLE_FIELDS = ("x", "v", "f", "c", "mass", "volume0", "material_id", "plastic")
+
+
+# ------------------------------------------------------------------ pure logic
+
+def slab_bounds(x_axis: np.ndarray, world: int, h: float) -> np.ndarray:
+    """Interior slab bounds: equal-count quantiles of the positions snapped to
+    block boundaries; returns [-inf, X_1, ..., X_{W-1}, +inf]."""
+    if world == 1:
+        return np.array([-np.inf, np.inf])
+    width = BLOCK_EDGE * h
+    qs = np.quantile(np.asarray(x_axis, float), np.arange(1, world) / world)
+    blocks = np.round(qs / width).astype(np.int64)
+    for k in range(1, len(blocks)):
+        blocks[k] = max(blocks[k], blocks[k - 1] + MIN_SLAB_BLOCKS)
+    bounds = np.concatenate([[-np.inf], blocks * width, [np.inf]])
+    counts = np.bincount(np.searchsorted(bounds[1:-1], x_axis, side="right"), minlength=world)
+    if counts.min() == 0:
+        raise ValueError(f"scene too narrow for {world} slabs of >= {MIN_SLAB_BLOCKS} blocks")
+    return bounds
+
+
+def slab_of(x_axis: torch.Tensor, bounds: np.ndarray) -> torch.Tensor:
+    """Owning rank of each position (slab [X_r, X_{r+1}))."""
+    inner = torch.as_tensor(bounds[1:-1], dtype=x_axis.dtype, device=x_axis.device)
+    return torch.searchsorted(inner, x_axis.contiguous(), right=True)
+
+
+def pack_coords(c: torch.Tensor) -> torch.Tensor:
+    """(k,3) int64 node coordinates -> global 63-bit keys (grid.py:26-31 packing)."""
+    c = c.to(torch.int64) + COORD_BIAS
+    return (c[:, 0] << 42) | (c[:, 1] << 21) | c[:, 2]
+
+
+def node_coords(block_coords: torch.Tensor, node_ids: torch.Tensor) -> torch.Tensor:
+    """Global coordinates of local node ids (node = block * 64 + (lx*4+ly)*4+lz)."""
+    b = node_ids // BLOCK_NODES
+    lid = node_ids % BLOCK_NODES
+    off = torch.stack([lid >> 4, (lid >> 2) & 3, lid & 3], dim=1)
+    return block_coords[b] * BLOCK_EDGE + off
+
+
+def halo_band(block_axis: torch.Tensor, bounds: np.ndarray, rank: int, h: float) -> torch.Tensor:
+    """Blocks within HALO_BLOCKS of this rank's interior slab bounds."""
+    band = torch.zeros_like(block_axis, dtype=torch.bool)
+    width = BLOCK_EDGE * h
+    for k in (rank, rank + 1):
+        if 0 < k < len(bounds) - 1:
+            bX = int(round(bounds[k] / width))
+            band |= (block_axis >= bX - HALO_BLOCKS) & (block_axis < bX + HALO_BLOCKS)
+    return band
+
+
+def match_keys(mine_sorted: torch.Tensor, theirs: torch.Tensor):
+    """Positions of ``theirs`` in the sorted ``mine_sorted`` (or -1)."""
+    if mine_sorted.numel() == 0 or theirs.numel() == 0:
+        return torch.full_like(theirs, -1)
+    pos = torch.searchsorted(mine_sorted, theirs).clamp(max=mine_sorted.numel() - 1)
+    return torch.where(mine_sorted[pos] == theirs, pos, torch.full_like(pos, -1))
+
+
+def node_owned(coords_axis: torch.Tensor, block_shared: torch.Tensor, bounds: np.ndarray,
+               rank: int, h: float) -> torch.Tensor:
+    """Ownership of active nodes: by coordinate in shared blocks, else mine."""
+    slab = slab_of(coords_axis.to(torch.float64) * h, bounds)
+    return (~block_shared) | (slab == rank)
+
+
+def free_sums(m, v_star, v0) -> torch.Tensor:
+    """(S0, Q0, Q1) of contact-free nodes (solver.cu closed form)."""
+    e = v0 - v_star
+    return torch.stack([(m[:, None] * e * e).sum(), (m[:, None] * v_star * v_star).sum(),
+                        (m[:, None] * v_star * e).sum()])
+
+
+# ------------------------------------------------------------------ communication
+
+class Comm:
+    """torch.distributed wrapper: variable-size all-gathers / broadcasts on the
+    backend's device (CPU under gloo, the rank's GPU under NCCL)."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        nccl = dist.is_initialized() and dist.get_backend(group) == "nccl"
+        self.dev = torch.device("cuda", torch.cuda.current_device()) if nccl else torch.device("cpu")
+
+    def allgather(self, t: torch.Tensor) -> list[torch.Tensor]:
+        """All ranks' tensors (same trailing shape and dtype; any row count)."""
+        if self.world == 1:
+            return [t]
+        src = t.to(self.dev).contiguous()
+        n = torch.tensor([src.shape[0]], dtype=torch.int64, device=self.dev)
+        ns = [torch.zeros_like(n) for _ in range(self.world)]
+        dist.all_gather(ns, n, group=self.group)
+        ns = [int(k.item()) for k in ns]
+        cap = max(max(ns), 1)
+        pad = torch.zeros((cap,) + tuple(src.shape[1:]), dtype=src.dtype, device=self.dev)
+        pad[: src.shape[0]] = src
+        outs = [torch.empty_like(pad) for _ in range(self.world)]
+        dist.all_gather(outs, pad, group=self.group)
+        return [o[:k].to(t.device) for o, k in zip(outs, ns)]
+
+    def sum(self, t: torch.Tensor) -> torch.Tensor:
+        if self.world == 1:
+            return t
+        x = t.to(self.dev).clone()
+        dist.all_reduce(x, group=self.group)
+        return x.to(t.device)
+
+    def bcast(self, t: torch.Tensor | None, shape_dtype=None, src: int = 0) -> torch.Tensor:
+        """Broadcast from ``src``; other ranks pass None and receive any shape."""
+        if self.world == 1:
+            return t
+        if self.rank == src:
+            x = t.to(self.dev).contiguous()
+            meta = torch.tensor([x.dim()] + list(x.shape) + [0] * (4 - x.dim()),
+                                dtype=torch.int64, device=self.dev)
+        else:
+            meta = torch.zeros(5, dtype=torch.int64, device=self.dev)
+        dist.broadcast(meta, src, group=self.group)
+        shape = tuple(int(s) for s in meta[1: 1 + int(meta[0])].tolist())
+        dtype = shape_dtype if shape_dtype is not None else (t.dtype if t is not None else torch.float64)
+        if self.rank != src:
+            x = torch.empty(shape, dtype=dtype, device=self.dev)
+        dist.broadcast(x, src, group=self.group)
+        return x
+
+
+# ------------------------------------------------------------------ state
+
+@dataclass
+class SlabState:
+    """A rank's share of one scene: the replicated scene constants and bodies
+    (``state``, whose particle set is this rank's) plus the global ids."""
+
+    state: SimState
+    gid: torch.Tensor          # (n_local,) global particle ids
+    bounds: np.ndarray
+    axis: int
+    comm: Comm
+
+    @staticmethod
+    def from_state(state: SimState, comm: Comm | None = None, axis: int = 0) -> "SlabState":
+        """Split a fully built (replicated) scene: every rank calls this with the
+        same ``state`` and keeps its slab's particles."""
+        comm = comm or Comm()
+        p = state.particles
+        x_axis = p.x[:, axis]
+        bounds = slab_bounds(x_axis.detach().cpu().numpy(), comm.world, state.h)
+        mine = slab_of(x_axis, bounds) == comm.rank
+        idx = torch.nonzero(mine, as_tuple=False).reshape(-1)
+        local = ParticleSet(*(getattr(p, k)[idx].clone() for k in PARTICLE_FIELDS),
+                            validate=False)
+        st = SimState(particles=local, materials=state.materials, bodies=state.bodies,
+                      h=state.h, step=state.step, contact_params=state.contact_params,
+                      solver_params=state.solver_params, mode=state.mode, workers=state.workers)
+        st.time, st.step_index = state.time, state.step_index
+        return SlabState(st, idx.clone(), bounds, axis, comm)
+
+    # -------------------------------------------------------------- migration
+    def migrate(self) -> None:
+        """Send particles that left the slab to their new owner (once per step)."""
+        c, p = self.comm, self.state.particles
+        dest = slab_of(p.x[:, self.axis], self.bounds)
+        if c.world > 1:
+            moving = dest != c.rank
+            n_moving = int(c.sum(torch.tensor([int(moving.sum())], dtype=torch.int64)).item())
+            if n_moving == 0:
+                return
+            out = torch.nonzero(moving, as_tuple=False).reshape(-1)
+            keep = torch.nonzero(~moving, as_tuple=False).reshape(-1)
+            pay = _pack_particles(p, self.gid, out, dest[out])
+            recv = [r for r in c.allgather(pay)]
+            got = torch.cat(recv)
+            got = got[got[:, 0].to(torch.int64) == c.rank] if got.numel() else got
+            arrays = {k: getattr(p, k)[keep] for k in PARTICLE_FIELDS}
+            gid = self.gid[keep]
+            if got.shape[0]:
+                g_gid, g_arr = _unpack_particles(got, p.x.device)
+                for k in PARTICLE_FIELDS:
+                    arrays[k] = torch.cat([arrays[k], g_arr[k]])
+                gid = torch.cat([gid, g_gid])
+            order = torch.argsort(gid)  # canonical local order: ascending global id
+            self.state.particles = ParticleSet(*(arrays[k][order].contiguous()
+                                                 for k in PARTICLE_FIELDS), validate=False)
+            self.gid = gid[order].contiguous()
+
+    def drift_check(self) -> None:
+        """Particles must stay within the halo band of their slab during a step."""
+        lo, hi = self.bounds[self.comm.rank], self.bounds[self.comm.rank + 1]
+        x = self.state.particles.x[:, self.axis]
+        slack = (HALO_BLOCKS - 1) * BLOCK_EDGE * self.state.h
+        if x.numel() and (float(x.min()) < lo - slack or float(x.max()) >= hi + slack):
+            raise RuntimeError("slab decomposition: particles drifted beyond the halo band "
+                               "within one step (reduce dt or widen HALO_BLOCKS)")
+
+
+def _pack_particles(p: ParticleSet, gid, idx, dest) -> torch.Tensor:
+    cols = [dest.to(torch.float64)[:, None], gid[idx].to(torch.float64)[:, None],
+            p.x[idx], p.v[idx], p.f[idx].reshape(-1, 9), p.c[idx].reshape(-1, 9),
+            p.mass[idx][:, None], p.volume0[idx][:, None],
+            p.material_id[idx].to(torch.float64)[:, None], p.plastic[idx][:, None]]
+    return torch.cat(cols, dim=1)
+
+
+def _unpack_particles(t: torch.Tensor, device):
+    t = t.to(device)
+    gid = t[:, 1].to(torch.int64)
+    arr = dict(x=t[:, 2:5].contiguous(), v=t[:, 5:8].contiguous(),
+               f=t[:, 8:17].reshape(-1, 3, 3).contiguous(),
+               c=t[:, 17:26].reshape(-1, 3, 3).contiguous(), mass=t[:, 26].contiguous(),
+               volume0=t[:, 27].contiguous(), material_id=t[:, 28].to(torch.int64),
+               plastic=t[:, 29].contiguous())
+    return gid, arr
+
+
+# ------------------------------------------------------------------ substep
+
+def _halo_reduce(ss: SlabState, grid: SparseGrid) -> torch.Tensor:
+    """Sum the node channels of blocks shared with neighbours; returns the
+    per-block "shared" mask."""
+    c = ss.comm
+    shared = torch.zeros(grid.n_blocks, dtype=torch.bool, device=grid.block_keys.device)
+    if c.world == 1 or grid.n_blocks == 0:
+        return shared
+    bc = grid.block_coords
+    band = torch.nonzero(halo_band(bc[:, ss.axis], ss.bounds, c.rank, ss.state.h),
+                         as_tuple=False).reshape(-1)
+    ch = torch.cat([grid.mass.view(-1, BLOCK_NODES, 1), grid.mom_apic.view(-1, BLOCK_NODES, 3),
+                    grid.mom_force.view(-1, BLOCK_NODES, 3)], dim=2)  # (nb, 64, 7)
+    keys = c.allgather(grid.block_keys[band])
+    vals = c.allgather(ch[band].reshape(-1, BLOCK_NODES * 7))
+    add = torch.zeros_like(ch)
+    for q in range(c.world):
+        if q == c.rank or keys[q].numel() == 0:
+            continue
+        pos = match_keys(grid.block_keys, keys[q])
+        hit = pos >= 0
+        if bool(hit.any()):
+            add[pos[hit]] += vals[q][hit].view(-1, BLOCK_NODES, 7)
+            shared[pos[hit]] = True
+    ch = ch + add
+    grid.mass.copy_(ch[:, :, 0].reshape(-1))
+    grid.mom_apic.copy_(ch[:, :, 1:4].reshape(-1, 3))
+    grid.mom_force.copy_(ch[:, :, 4:7].reshape(-1, 3))
+    return shared
+
+
+def _distributed_solve(ss: SlabState, grid, stencil, contacts, dt_s, block_shared):
+    """Gather the contact problem to rank 0, solve, scatter the solution.
+    Returns (v_next, gamma (local contacts, contact frame), report, owned)."""
+    st, c = ss.state, ss.comm
+    dev = grid.mass.device
+    act = torch.nonzero(grid.active, as_tuple=False).reshape(-1)
+    coords = node_coords(grid.block_coords, act)
+    keys_act = pack_coords(coords)
+    owned = node_owned(coords[:, ss.axis], block_shared[act // BLOCK_NODES], ss.bounds, c.rank,
+                       st.h)
+    remap = torch.full((grid.n_nodes,), -1, dtype=torch.int64, device=dev)
+    remap[act] = torch.arange(act.shape[0], device=dev)
+    if contacts.n:
+        vcs = contact_velocities(contacts, stencil, grid.v_k)
+        contacts.gamma_lag = normal_impulse(vcs[:, 2], contacts.phi, st.contact_params, dt_s)
+        loc = remap[stencil.nodes[contacts.particle]]          # (nc,27) active index or -1
+        w = stencil.weights[contacts.particle].clone()
+        dead = loc < 0
+        w[dead] = 0.0
+        skeys = torch.where(dead, torch.full_like(loc, -1), keys_act[loc.clamp(min=0)])
+        cn = torch.unique(loc[~dead])
+    else:
+        skeys = torch.zeros((0, 27), dtype=torch.int64, device=dev)
+        w = _lib.zeros((0, 27))
+        cn = torch.zeros(0, dtype=torch.int64, device=dev)
+    # global contact-node set
+    all_cn = c.allgather(keys_act[cn])
+    C = torch.unique(torch.cat([k.to(dev) for k in all_cn]))     # sorted
+    in_C = match_keys(C, keys_act) >= 0
+    fm = owned & ~in_C
+    fs = free_sums(grid.mass[act][fm], grid.v_star[act][fm], grid.v_k[act][fm])
+    ext = c.sum(fs)
+    # contact records and contact-node records to rank 0
+    crec = torch.cat([contacts.frames.reshape(-1, 9), contacts.bias, contacts.phi[:, None],
+                      contacts.mu[:, None], contacts.gamma_lag[:, None], w], dim=1) \
+        if contacts.n else _lib.zeros((0, 9 + 3 + 3 + 27))
+    nrec = torch.cat([grid.mass[act][cn][:, None], grid.v_star[act][cn], grid.v_k[act][cn]], dim=1)
+    g_ck = c.allgather(skeys)
+    g_cr = c.allgather(crec)
+    g_nk = all_cn
+    g_nr = c.allgather(nrec)
+    counts = [int(k.shape[0]) for k in g_ck]
+    if c.rank == 0:
+        ck = torch.cat([k.to(dev) for k in g_ck])
+        cr = torch.cat([r.to(dev) for r in g_cr])
+        nk = torch.cat([k.to(dev) for k in g_nk])
+        nr = torch.cat([r.to(dev) for r in g_nr])
+        first = match_keys(C, nk)                               # every record maps into C
+        m = torch.empty(C.shape[0], dtype=torch.float64, device=dev)
+        vs = torch.empty((C.shape[0], 3), dtype=torch.float64, device=dev)
+        v0 = torch.empty((C.shape[0], 3), dtype=torch.float64, device=dev)
+        m[first] = nr[:, 0]                                      # shared copies are identical
+        vs[first] = nr[:, 1:4]
+        v0[first] = nr[:, 4:7]
+        nodes = match_keys(C, ck.reshape(-1)).reshape(-1, 27).clamp(min=0)
+        prob = ContactProblem(m=m, v_star=vs, v_init=v0, nodes=nodes, w=cr[:, 15:42].contiguous(),
+                              frames=cr[:, 0:9].reshape(-1, 3, 3).contiguous(),
+                              bias=cr[:, 9:12].contiguous(), phi=cr[:, 12].contiguous(),
+                              mu=cr[:, 13].contiguous(), gamma_lag=cr[:, 14].contiguous(),
+                              contact_params=st.contact_params, dt=dt_s)
+        v_sol, gamma_all, report, P = quasi_newton_solve_ext(prob, st.solver_params,
+                                                             ext.tolist())
+        meta = torch.tensor([P, float(report.converged), float(report.iterations),
+                             float(report.ls_evals), float(report.regularized)],
+                            dtype=torch.float64, device=dev)
+    else:
+        v_sol = gamma_all = meta = None
+    meta = c.bcast(meta)
+    v_sol = c.bcast(v_sol).to(dev)
+    gamma_all = c.bcast(gamma_all).to(dev)
+    P = float(meta[0])
+    start = sum(counts[: c.rank])
+    gamma = gamma_all[start: start + contacts.n]
+    report = SolveReport(converged=bool(meta[1] > 0.5), iterations=int(meta[2]),
+                         n_contacts=int(sum(counts)), n_dofs=3 * int(C.shape[0]),
+                         ls_evals=int(meta[3]), regularized=int(meta[4]))
+    # v_next on the local grid
+    v_next = _lib.zeros((grid.n_nodes, 3))
+    va = grid.v_star[act] + P * (grid.v_k[act] - grid.v_star[act])
+    pos = match_keys(C, keys_act)
+    hit = pos >= 0
+    va[hit] = v_sol[pos[hit]]
+    v_next[act] = va
+    return v_next, gamma, report, owned
+
+
+def slab_substep(ss: SlabState, dt_s: float, plan, epoch: int) -> dict:
+    """coupling.py:115-150 on this rank's slab (the three exchanges above)."""
+    st, c = ss.state, ss.comm
+    p = st.particles
+    grid = SparseGrid.allocate(p.x, st.h)
+    stencil = build_stencil(p.x, grid)
+    particle_to_grid(p, grid, stencil, st.materials, dt_s, plan, epoch, mode=st.mode,
+                     workers=st.workers)
+    shared = _halo_reduce(ss, grid)
+    grid_update(grid, st.step.gravity, dt_s)
+    contacts = detect_contacts(p, st.bodies, st.margin, st._bias_cache)
+    n_glob = int(c.sum(torch.tensor([contacts.n], dtype=torch.int64)).item())
+    if n_glob == 0:
+        grid.v_next = grid.v_star
+        act = torch.nonzero(grid.active, as_tuple=False).reshape(-1)
+        coords = node_coords(grid.block_coords, act)
+        owned = node_owned(coords[:, ss.axis], shared[act // BLOCK_NODES], ss.bounds, c.rank,
+                           st.h)
+        report = SolveReport(converged=True, n_contacts=0,
+                             n_dofs=3 * int(c.sum(torch.tensor([int(owned.sum())])).item()))
+    else:
+        grid.v_next, gamma, report, owned = _distributed_solve(ss, grid, stencil, contacts, dt_s,
+                                                               shared)
+        if contacts.n:
+            gamma_world = torch.einsum("ci,cij->cj", gamma, contacts.frames)
+            bpos = torch.as_tensor(np.stack([np.asarray(b.position) for b in st.bodies]),
+                                   dtype=torch.float64, device=gamma.device)
+            st._accum.add_reactions(contacts.body, gamma_world, contacts.witness - bpos[contacts.body])
+    clamped = grid_to_particle(p, grid, stencil, dt_s, st.materials)
+    n_active = int(c.sum(torch.tensor([int(owned.sum())], dtype=torch.int64)).item())
+    return dict(n_contacts=n_glob, report=report, clamped=clamped, n_active=n_active)
+
+
+def slab_advance_step(ss: SlabState) -> StepSummary:
+    """advance_step (coupling.py:168-219) of the whole scene; every rank returns
+    the same summary."""
+    st, c = ss.state, ss.comm
+    ss.migrate()
+    p = st.particles
+    epoch = st.step_index
+    plan = build_sort_plan(p.x, st.h, epoch)
+    st._bias_cache = BiasCache()
+    st._accum = ImpulseAccumulator(len(st.bodies))
+    n = st.step.substeps
+    dt_s = st.step.dt / n
+    ncs, its, acts, clamped, conv = [], [], [], 0, True
+    for _ in range(n):
+        info = slab_substep(ss, dt_s, plan, epoch)
+        ss.drift_check()
+        ncs.append(info["n_contacts"])
+        its.append(info["report"].iterations)
+        acts.append(info["n_active"])
+        conv &= info["report"].converged
+        clamped += info["clamped"]
+    dt = st.step.dt
+    acc = torch.as_tensor(np.concatenate([st._accum.linear, st._accum.angular], axis=1))
+    acc = c.sum(acc).numpy()
+    nb = len(st.bodies)
+    st._accum.linear[:] = acc[:, :3]
+    st._accum.angular[:] = acc[:, 3:]
+    wrench = acc / dt
+    new_time = st.time + dt
+    _rigid_update(st, new_time)
+    stale = torch.tensor([plan_staleness(plan, p.x, st.h) * p.n, float(p.n)], dtype=torch.float64)
+    stale = c.sum(stale)
+    n_tot = int(stale[1].item())
+    clamped = int(c.sum(torch.tensor([int(clamped)], dtype=torch.int64)).item())
+    summary = StepSummary(step_index=st.step_index, time=new_time, n_particles=n_tot,
+                          n_active_nodes=float(np.mean(acts)),
+                          n_contacts_mean=float(np.mean(ncs)), n_contacts_max=int(np.max(ncs)),
+                          iterations_mean=float(np.mean(its)), iterations_max=int(np.max(its)),
+                          all_converged=conv,
+                          staleness=float(stale[0].item()) / max(n_tot, 1),
+                          clamped_gradients=clamped, wrench=wrench[:nb])
+    st.time = new_time
+    st.step_index += 1
+    return summary
+
+
+def gather_particles(ss: SlabState) -> dict:
+    """The whole scene's particle arrays in global-id order (on every rank)."""
+    p = ss.state.particles
+    pay = _pack_particles(p, ss.gid, torch.arange(p.n, device=p.x.device),
+                          torch.zeros(p.n, dtype=torch.int64, device=p.x.device))
+    allp = torch.cat([t.to(p.x.device) for t in ss.comm.allgather(pay)])
+    gid, arr = _unpack_particles(allp, p.x.device)
+    order = torch.argsort(gid)
+    return {k: v[order] for k, v in arr.items()}

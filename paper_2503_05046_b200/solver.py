@@ -186,6 +186,19 @@ def line_search(deriv, max_iters: int = 50, tol: float = 1e-8) -> LineSearchResu
 
 def quasi_newton_solve(problem: ContactProblem, params: SolverParams, v0=None):
     """Block-preconditioned solve on the device; returns (v, gamma, report)."""
+    v, gamma, report, _ = _solve(problem, params, v0, None)
+    return v, gamma, report
+
+
+def quasi_newton_solve_ext(problem: ContactProblem, params: SolverParams, ext_free, v0=None):
+    """The solve with contact-free nodes held elsewhere (slab decomposition,
+    slab.py): ext_free = (S0, Q0, Q1) of those nodes (S0 = sum m|v0 - v*|^2,
+    Q0 = sum m|v*|^2, Q1 = sum m v*.(v0 - v*)).  Returns (v, gamma, report, P)
+    with P = prod(1 - alpha): the external nodes end at v* + P (v0 - v*)."""
+    return _solve(problem, params, v0, ext_free)
+
+
+def _solve(problem: ContactProblem, params: SolverParams, v0, ext_free):
     nd, nc = int(problem.m.shape[0]), problem.n_contacts
     v = _lib.empty((nd, 3))
     gamma = _lib.empty((nc, 3))
@@ -195,10 +208,18 @@ def quasi_newton_solve(problem: ContactProblem, params: SolverParams, v0=None):
     pr = problem.to_struct()
     sp = params.to_struct()
     v0d = _lib.as_dev(v0) if v0 is not None else None
-    _lib.check(_lib.lib().mpmrb_qn_solve(_lib.ctx(), C.byref(pr), C.byref(sp), _lib.ptr(v0d),
-                                         _lib.ptr(v), _lib.ptr(gamma), _lib.ptr(tr[0]),
-                                         _lib.ptr(tr[1]), _lib.ptr(tr[2]), _lib.ptr(tr[3]),
-                                         C.byref(rep)))
+    P = C.c_double(1.0)
+    if ext_free is None:
+        _lib.check(_lib.lib().mpmrb_qn_solve(_lib.ctx(), C.byref(pr), C.byref(sp), _lib.ptr(v0d),
+                                             _lib.ptr(v), _lib.ptr(gamma), _lib.ptr(tr[0]),
+                                             _lib.ptr(tr[1]), _lib.ptr(tr[2]), _lib.ptr(tr[3]),
+                                             C.byref(rep)))
+    else:
+        ext = (C.c_double * 3)(*[float(e) for e in ext_free])
+        _lib.check(_lib.lib().mpmrb_qn_solve_ext(
+            _lib.ctx(), C.byref(pr), C.byref(sp), _lib.ptr(v0d), ext, _lib.ptr(v),
+            _lib.ptr(gamma), _lib.ptr(tr[0]), _lib.ptr(tr[1]), _lib.ptr(tr[2]), _lib.ptr(tr[3]),
+            C.byref(P), C.byref(rep)))
     it = int(rep.iterations)
     trh = _lib.to_numpy(tr)
     report = SolveReport(converged=bool(rep.converged), iterations=it, n_contacts=nc,
@@ -212,4 +233,4 @@ def quasi_newton_solve(problem: ContactProblem, params: SolverParams, v0=None):
     if not report.converged:
         log.warning("contact solve hit max_iters=%d (residual %.3e, threshold %.3e)",
                     params.max_iters, report.residual_trace[-1], report.threshold_trace[-1])
-    return v, gamma, report
+    return v, gamma, report, float(P.value)

@@ -2,6 +2,8 @@
 vectors and the CPU oracle.  Bit-exact for integer/index work; float64
 tolerances (stated per test) for reassociated sums."""
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -553,3 +555,77 @@ def test_bench_transfer_harness(mp, capsys):
     rows = [ln.split(",") for ln in lines[1:]]
     assert [r[0] for r in rows] == ["deterministic", "fast", "naive"]
     assert all(float(r[4]) <= 1e-12 for r in rows)
+
+
+# ------------------------------------------------------------------ slab decomposition
+
+def _slab_scene():
+    from paper_2503_05046_b200 import scenes
+    sc = scenes.multi_material_scene(half=(0.06, 0.03, 0.02), h=0.01, substeps=4)
+    sc["bodies"] = sc["bodies"][:1]
+    sc["bodies"].append(dict(name="ball", kinematic=False, mass=0.05,
+                             inertia=(np.eye(3) * 2e-6).tolist(), position=[0.0, 0.0, 0.06],
+                             quat=[1, 0, 0, 0], v=[0, 0, -0.5], omega=[0, 1.0, 0],
+                             geoms=[dict(shape="sphere", radius=0.015, position=[0, 0, 0],
+                                         quat=[1, 0, 0, 0], mu=0.5)]))
+    return sc
+
+
+def _slab_worker(rank, world, port, out, steps):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2503_05046_b200 import scenes, slab
+    st = scenes.build_state(_slab_scene())
+    ss = slab.SlabState.from_state(st)
+    n_local0 = ss.state.particles.n
+    sums = [slab.slab_advance_step(ss) for _ in range(steps)]
+    allp = slab.gather_particles(ss)
+    if rank == 0:
+        np.savez(out, **{k: v.cpu().numpy() for k, v in allp.items()},
+                 wrench=np.stack([s.wrench for s in sums]),
+                 ncont=np.array([s.n_contacts_mean for s in sums]),
+                 nact=np.array([s.n_active_nodes for s in sums]),
+                 iters=np.array([s.iterations_mean for s in sums]),
+                 bodies=np.array([b.position for b in ss.state.bodies]),
+                 n_local0=n_local0, n_part=sums[-1].n_particles)
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_slab_decomposition_matches_single_scene(mp, tmp_path):
+    """Two slab ranks (gloo, sharing cuda:0) advance one scene: P2G halo reduce
+    across the slab bound, the contact problem gathered to rank 0 and solved
+    with the ranks' contact-free nodes in closed form, impulses scattered back.
+    The result must match the single-scene run of the same operators
+    (advance_step_ops) up to reduction-order roundoff."""
+    import socket
+
+    import torch.multiprocessing as tmp
+    from paper_2503_05046_b200 import coupling, scenes
+    steps = 5
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    out = str(tmp_path / "slab.npz")
+    tmp.spawn(_slab_worker, args=(2, port, out, steps), nprocs=2, join=True)
+    r = np.load(out)
+    st = scenes.build_state(_slab_scene())
+    n = st.particles.n
+    assert 0 < int(r["n_local0"]) < n and int(r["n_part"]) == n
+    ref = [coupling.advance_step_ops(st) for _ in range(steps)]
+    for i, sref in enumerate(ref):
+        assert r["ncont"][i] == sref.n_contacts_mean, i
+        assert r["nact"][i] == sref.n_active_nodes, i
+        ws = np.abs(sref.wrench).max()
+        assert np.abs(r["wrench"][i] - sref.wrench).max() <= 1e-6 * ws + 1e-9, i
+    assert np.abs(ref[-1].wrench[1]).max() > 0  # the ball is in contact across the bound
+    p = st.particles
+    np.testing.assert_allclose(r["x"], np_(p.x), rtol=0, atol=1e-10)
+    np.testing.assert_allclose(r["v"], np_(p.v), rtol=0, atol=1e-7)
+    np.testing.assert_allclose(r["f"], np_(p.f), rtol=0, atol=1e-8)
+    np.testing.assert_allclose(r["plastic"], np_(p.plastic), rtol=0, atol=1e-8)
+    np.testing.assert_allclose(r["bodies"], np.array([b.position for b in st.bodies]), rtol=0,
+                               atol=1e-10)
