@@ -227,16 +227,22 @@ class ClockSampler:
 
 # ------------------------------------------------------------------ ours
 
-def algorithmic_bytes(stage: str, n: int, n_act: int, sand: bool) -> float:
+def algorithmic_bytes(stage: str, n: int, n_act: int, sand: bool, prof: dict | None = None
+                      ) -> float:
     """Algorithmic HBM bytes per launch (float64):
     P2G reads x,v (24+24), C,F (72+72), m, V0, material id (8 each) = 216 B
     per particle and writes 7 channels x 8 B = 56 B per active node; G2P reads
     x, F (96) and writes x, v, C, F (192) = 288 B per particle (+16 B plastic
-    read+write for sand) and reads v_next (24 B) per active node."""
+    read+write for sand) and reads v_next (24 B) per active node; the contact
+    solve moves 80 B per active node + 128 B per contact per iteration and
+    48 B per contact per line-search evaluation."""
     if stage == "p2g":
         return 216.0 * n + 56.0 * n_act
     if stage == "g2p":
         return (288.0 + (16.0 if sand else 0.0)) * n + 24.0 * n_act
+    if stage == "solve":
+        nc = prof["n_contacts"]
+        return (80.0 * n_act + 128.0 * nc) * prof["iterations"] + 48.0 * nc * prof["ls_evals"]
     raise ValueError(stage)
 
 
@@ -325,27 +331,36 @@ def run_ours(args):
     st = prof["stage_ms"]
     substep_ms = sum(st.values())
     hbm, peak_src = peaks()
-    cand = {k: st[k] for k in ("p2g", "g2p")}
-    dom = max(cand, key=cand.get)
-    abytes = algorithmic_bytes(dom, n, prof["n_active"], sand)
-    achieved = abytes / (st[dom] * 1e-3) / 1e9
-    traffic = None
     tf = ROOT / "profiles" / "ncu_traffic.json"
-    if tf.exists():
-        try:
-            traffic = json.loads(tf.read_text()).get(args.workload, {}).get(dom)
-        except Exception:
-            traffic = None
-    roofline = dict(bound="hbm", kernel=dom, achieved=achieved, peak=hbm, unit="GB/s",
-                    frac=achieved / hbm, traffic=traffic, peak_source=peak_src,
-                    algorithmic_bytes=abytes, launch_ms=st[dom],
-                    share_of_substep=st[dom] / substep_ms,
-                    stages_ms=st, solver=dict(iterations=prof["iterations"],
-                                              ls_evals=prof["ls_evals"],
-                                              contacts=prof["n_contacts"],
-                                              ms=st["solve"],
-                                              us_per_iter=(1e3 * st["solve"] / prof["iterations"]
-                                                           if prof["iterations"] else None)))
+    try:
+        traffic_all = json.loads(tf.read_text()).get(args.workload, {}) if tf.exists() else {}
+    except Exception:
+        traffic_all = {}
+
+    def kernel_roof(stage: str) -> dict:
+        abytes = algorithmic_bytes(stage, n, prof["n_active"], sand, prof)
+        achieved = abytes / (st[stage] * 1e-3) / 1e9
+        kname = "k_qn_solve" if stage == "solve" else stage
+        return dict(bound="hbm", kernel=kname, achieved=achieved, peak=hbm, unit="GB/s",
+                    frac=achieved / hbm, traffic=traffic_all.get(kname),
+                    algorithmic_bytes=abytes, launch_ms=st[stage],
+                    share_of_substep=st[stage] / substep_ms)
+
+    # the dominant kernel of the profiled substep (the contact solve whenever
+    # contacts are present); P2G / G2P ride along as the transfer kernels
+    dom = max(("solve", "p2g", "g2p"), key=lambda k: st[k])
+    roofline = kernel_roof(dom)
+    roofline["peak_source"] = peak_src
+    if dom == "solve":
+        roofline["note"] = ("latency-bound: per iteration two grid barriers and ~12 "
+                            "line-search group reductions (DESIGN.md section 3) leave HBM "
+                            "mostly idle")
+    roofline["secondary"] = {k: kernel_roof(k) for k in ("p2g", "g2p") if k != dom}
+    roofline["stages_ms"] = st
+    roofline["solver"] = dict(iterations=prof["iterations"], ls_evals=prof["ls_evals"],
+                              contacts=prof["n_contacts"], ms=st["solve"],
+                              us_per_iter=(1e3 * st["solve"] / prof["iterations"]
+                                           if prof["iterations"] else None))
 
     # ---- end to end through the public API with pinned host buffers
     e2e = None
