@@ -262,9 +262,13 @@ __device__ void reduce_all(const Sync& sync, int& parity, double (&v)[K], double
 
 // All-reduce of K values over the line-search group (CTAs 0..G-1) through
 // channel B slots; G == 1 is a plain block reduction.
+// The result goes through one of two shared-memory buffers (alternating per
+// call, `rpar`), so no trailing barrier is needed before the next call.
 template <int K>
 __device__ void group_reduce(int G, unsigned long long* slots, unsigned& tag, double (&v)[K],
-                             double (&out)[K], double* sm, int mode = 0) {
+                             double (&out)[K], double* sm, unsigned& rpar, int mode = 0) {
+  double* res = sm + 32 * kMaxRed + 4 * (rpar & 1u);
+  ++rpar;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double bs[K];
   block_reduce<K>(v, sm, bs);
@@ -272,7 +276,7 @@ __device__ void group_reduce(int G, unsigned long long* slots, unsigned& tag, do
     if (G == 1) {
       if (lane == 0)
 #pragma unroll
-        for (int k = 0; k < K; ++k) sm[32 * kMaxRed + k] = bs[k];
+        for (int k = 0; k < K; ++k) res[k] = bs[k];
     } else {
       unsigned long long* base = slots + kSlotB + (long long)(tag & 1u) * kMaxSolverCtas * 4;
       if (lane == 0) slot_publish<K>(base + (long long)blockIdx.x * 2 * K, bs, tag);
@@ -293,14 +297,13 @@ __device__ void group_reduce(int G, unsigned long long* slots, unsigned& tag, do
       }
       if (lane == 0)
 #pragma unroll
-        for (int k = 0; k < K; ++k) sm[32 * kMaxRed + k] = r[k];
+        for (int k = 0; k < K; ++k) res[k] = r[k];
     }
   }
   if (G > 1) ++tag;
   __syncthreads();
 #pragma unroll
-  for (int k = 0; k < K; ++k) out[k] = sm[32 * kMaxRed + k];
-  __syncthreads();
+  for (int k = 0; k < K; ++k) out[k] = res[k];
 }
 
 // All-reduce of K values over the line-search group when it is cluster 0:
@@ -690,6 +693,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
             (a.prof && blockIdx.x == 0 && threadIdx.x == 0) ? a.prof : nullptr,
             (a.prof && threadIdx.x == 0) ? &in_sync_acc : nullptr, a.bar, &bar_gen};
   int parity = 0;
+  unsigned grp_par = 0;  // group_reduce result buffer parity
   const long long tid = (long long)blockIdx.x * kThreads + threadIdx.x;
   const long long nthr = (long long)nctas * kThreads;
   const ContactModel cm{a.K, a.den, a.eps_v};
@@ -913,7 +917,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
     double d0s = 0.0, e1s = 0.0, e1dd = 0.0;
     if (nctas == 1) {
       double rr[3] = {r0, r1, r1dd}, ss[3];
-      group_reduce<3>(1, a.slots, tagB, rr, ss, sm);
+      group_reduce<3>(1, a.slots, tagB, rr, ss, sm, grp_par);
       d0s = ss[0];
       e1s = ss[1];
       e1dd = ss[2];
@@ -994,7 +998,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
             }
             unsigned long long tls1 = prof ? gtime() : 0ull;
             if (CL > 1) cluster_reduce<2>(CL, s_cl, cpar, rr, ss, sm);
-            else group_reduce<2>(G, a.slots, tagB, rr, ss, sm, a.ls_mode);
+            else group_reduce<2>(G, a.slots, tagB, rr, ss, sm, grp_par, a.ls_mode);
             if (prof) {
               unsigned long long tls2 = gtime();
               pt[12] += tls1 - tls0;
@@ -1029,7 +1033,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
         a.tr_alpha[it] = alpha_final;
     } else if (threadIdx.x < 32) {
       double r[2];
-      slot_poll_sum<2, 1, 256>(a.slots + kSlotC + (long long)(tagC & 1u) * 4, 1, tagC, r);
+      slot_poll_sum<2, 1, 128>(a.slots + kSlotC + (long long)(tagC & 1u) * 4, 1, tagC, r);
       if (threadIdx.x == 0) {
         s_bc[0] = r[0];
         s_bc[1] = r[1];

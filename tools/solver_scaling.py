@@ -108,7 +108,7 @@ def main():
         print(f"ctas={spec:>7}: {dt * 1e3:8.2f} ms, iters={rep.iterations}, "
               f"ls_evals={rep.ls_evals}, us/iter={dt * 1e6 * reps / it:7.1f} | per-iter us: "
               f"N={ph[1]:.1f} (work {nw:.1f}) D={ph[2]:.1f} (work {dw:.1f}) LS={ph[3]:.1f} U={ph[4]:.1f} (work {uw:.1f}) "
-              f"in-sync={prof[10] / 1e3 / it:.1f} "
+              f"in-sync={prof[10] / 1e3 / it:.1f} kernel={sum(ph):.1f} (init {ph[0]:.1f} epi {ph[5]:.1f}) "
               f"(LS/eval={prof[3] / 1e3 / max(1, rep.ls_evals * reps):.2f}) "
               f"ctas={prof[8] & 0xffffffff} ls_group={prof[8] >> 32} "
               f"contact_nodes={prof[11] & 0xffffffff} groups={prof[11] >> 32} "
