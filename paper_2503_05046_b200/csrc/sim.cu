@@ -152,10 +152,12 @@ __global__ void k_substep_end(const int* __restrict__ counters, const SolveOut* 
                               const double* __restrict__ partial, int nbody,
                               double* __restrict__ accum, int* __restrict__ substep_idx,
                               SubstepStat* __restrict__ stats, int max_substeps, DevStatus* st) {
-  const int lane = threadIdx.x;
+  // one warp per wrench component (all components' partial loads in flight
+  // at once), each summing the kReactCtas partials in a fixed order
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int nb = nbody < kMaxBodies ? nbody : kMaxBodies;
   const bool any = counters[2] > 0;
-  for (int q = 0; q < nb * 6; ++q) {
+  for (int q = wid; q < nb * 6; q += nw) {
     double x = 0.0;
     if (any)
       for (int k = lane; k < kReactCtas; k += 32) x += partial[(long long)q * kReactCtas + k];
@@ -163,7 +165,7 @@ __global__ void k_substep_end(const int* __restrict__ counters, const SolveOut* 
     for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
     if (lane == 0) accum[q] -= x;
   }
-  if (lane == 0) {
+  if (threadIdx.x == 0) {
     int k = *substep_idx;
     if (k < max_substeps) {
       SubstepStat r;
@@ -441,7 +443,7 @@ int Sim::capture_or_launch() {
   k_reactions<<<kReactCtas, kReactThreads, 0, c.stream>>>(
       counters, b_gamma.as<double>(), ca.frames, ca.witness, ca.body, b_geoms.as<mpmrb_geom>(),
       ngeom, nbody, nc_cap, b_gworld.as<double>(), b_react.as<double>());
-  k_substep_end<<<1, 32, 0, c.stream>>>(counters, b_solveout.as<SolveOut>(),
+  k_substep_end<<<1, 256, 0, c.stream>>>(counters, b_solveout.as<SolveOut>(),
                                        b_react.as<double>(), nbody, b_accum.as<double>(),
                                        counters + 3, b_stats.as<SubstepStat>(), max_substeps,
                                        c.status);

@@ -14,7 +14,9 @@ timeout 900 python bench.py --workload multi4m --steps 5 --no-cpu-baseline > gpu
 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 20000 --csv \
    --log-file gpurun_out/launches.csv python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-e2e \
    > gpurun_out/launches_bench.log 2>&1
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:'k_p2g|k_g2p|k_qn_solve' -s 100 -c 3 \
-   -o gpurun_out/prof_sand python bench.py --steps 4 --warmup 3 --no-cpu-baseline --no-e2e \
+# skip into the contact-loaded window (the pusher reaches the pile after ~12 steps)
+timeout 1500 ncu --set full --clock-control none --import-source on -k regex:'k_p2g|k_g2p|k_qn_solve' -s 450 -c 3 \
+   -o gpurun_out/prof_sand python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-e2e \
    > gpurun_out/prof_sand.log 2>&1
+python tools/summarize_evidence.py gpurun_out/launches.csv gpurun_out/prof_sand.ncu-rep sand_final > gpurun_out/summarize.log 2>&1
 ls -la gpurun_out
