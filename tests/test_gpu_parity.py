@@ -559,12 +559,14 @@ def test_bench_transfer_harness(mp, capsys):
 
 # ------------------------------------------------------------------ slab decomposition
 
-def _slab_scene():
+def _slab_scene(world=2):
     from paper_2503_05046_b200 import scenes
-    sc = scenes.multi_material_scene(half=(0.06, 0.03, 0.02), h=0.01, substeps=4)
+    hx = 0.06 if world == 2 else 0.1 * world  # >= 4 blocks per slab
+    sc = scenes.multi_material_scene(half=(hx, 0.03, 0.02), h=0.01, substeps=4)
     sc["bodies"] = sc["bodies"][:1]
+    bx = 0.0 if world == 2 else -0.08  # on a slab bound (quantile bounds: 0 / -0.08, 0.12)
     sc["bodies"].append(dict(name="ball", kinematic=False, mass=0.05,
-                             inertia=(np.eye(3) * 2e-6).tolist(), position=[0.0, 0.0, 0.06],
+                             inertia=(np.eye(3) * 2e-6).tolist(), position=[bx, 0.0, 0.06],
                              quat=[1, 0, 0, 0], v=[0, 0, -0.5], omega=[0, 1.0, 0],
                              geoms=[dict(shape="sphere", radius=0.015, position=[0, 0, 0],
                                          quat=[1, 0, 0, 0], mu=0.5)]))
@@ -577,7 +579,7 @@ def _slab_worker(rank, world, port, out, steps):
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2503_05046_b200 import scenes, slab
-    st = scenes.build_state(_slab_scene())
+    st = scenes.build_state(_slab_scene(world))
     ss = slab.SlabState.from_state(st)
     n_local0 = ss.state.particles.n
     sums = [slab.slab_advance_step(ss) for _ in range(steps)]
@@ -594,7 +596,8 @@ def _slab_worker(rank, world, port, out, steps):
 
 
 @pytest.mark.gpu
-def test_slab_decomposition_matches_single_scene(mp, tmp_path):
+@pytest.mark.parametrize("world", [2, 3])
+def test_slab_decomposition_matches_single_scene(mp, tmp_path, world):
     """Two slab ranks (gloo, sharing cuda:0) advance one scene: P2G halo reduce
     across the slab bound, the contact problem gathered to rank 0 and solved
     with the ranks' contact-free nodes in closed form, impulses scattered back.
@@ -610,9 +613,9 @@ def test_slab_decomposition_matches_single_scene(mp, tmp_path):
     port = s.getsockname()[1]
     s.close()
     out = str(tmp_path / "slab.npz")
-    tmp.spawn(_slab_worker, args=(2, port, out, steps), nprocs=2, join=True)
+    tmp.spawn(_slab_worker, args=(world, port, out, steps), nprocs=world, join=True)
     r = np.load(out)
-    st = scenes.build_state(_slab_scene())
+    st = scenes.build_state(_slab_scene(world))
     n = st.particles.n
     assert 0 < int(r["n_local0"]) < n and int(r["n_part"]) == n
     ref = [coupling.advance_step_ops(st) for _ in range(steps)]
