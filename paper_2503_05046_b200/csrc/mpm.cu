@@ -150,7 +150,13 @@ __device__ __forceinline__ void particle_payload(const ParticlesDev& p, long lon
   }
 }
 
-__global__ void __launch_bounds__(kP2GThreads, 4) k_p2g(GridDev g, ParticlesDev p,
+#ifndef MPMRB_P2G_MINB
+#define MPMRB_P2G_MINB 4  // resident CTAs per SM the register budget is sized for
+#endif
+#ifndef MPMRB_G2P_MINB
+#define MPMRB_G2P_MINB 1
+#endif
+__global__ void __launch_bounds__(kP2GThreads, MPMRB_P2G_MINB) k_p2g(GridDev g, ParticlesDev p,
                                                      const mpmrb_material* __restrict__ mats,
                                                      int nmat, double dt,
                                                      double* __restrict__ gmass,
@@ -374,7 +380,7 @@ __global__ void k_grid_update(long long n_cap, const int* __restrict__ nb_dev,
   }
 }
 
-__global__ void __launch_bounds__(128) k_g2p(GridDev g, ParticlesDev p,
+__global__ void __launch_bounds__(128, MPMRB_G2P_MINB) k_g2p(GridDev g, ParticlesDev p,
                                              const mpmrb_material* __restrict__ mats, int nmat,
                                              const double* __restrict__ v_next, double dt,
                                              unsigned long long* __restrict__ clamped,
