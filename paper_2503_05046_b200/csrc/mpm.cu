@@ -101,6 +101,14 @@ __device__ __forceinline__ void p2g_scatter_one(const GridDev& g, const double* 
 constexpr int kP2GThreads = 128;
 constexpr int kWarpTile = 128;  // nodes per warp tile (e.g. 4 x 4 x 8)
 
+// two ints packed in one shared-memory double slot (payload staging)
+__device__ __forceinline__ double pack2i(int lo, int hi) {
+  return __hiloint2double(hi, lo);
+}
+__device__ __forceinline__ int2 double_as_int2(double d) {
+  return make_int2(__double2loint(d), __double2hiint(d));
+}
+
 // Per-particle P2G payload: m, m v, m C, S = -dt D^-1 V0 tau and the external
 // impulse dt f of cloth vertex forces.  Cloth roles (cloth.cu): vertex
 // particles carry no stress (their in-plane forces arrive in fext), element
@@ -164,6 +172,7 @@ __global__ void __launch_bounds__(kP2GThreads, MPMRB_P2G_MINB) k_p2g(GridDev g, 
                                                      double* __restrict__ mom_force,
                                                      DevStatus* st) {
   __shared__ double s_tile[kP2GThreads / 32][7][kWarpTile];
+  __shared__ double s_pay[kP2GThreads / 32][39][16];  // 16 particles' payloads
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const long long w0 = ((long long)blockIdx.x * kP2GThreads) + wid * 32;
   if (w0 >= p.n) return;
@@ -203,102 +212,100 @@ __global__ void __launch_bounds__(kP2GThreads, MPMRB_P2G_MINB) k_p2g(GridDev g, 
     }
     return;
   }
-  // 2. sort lanes by cell (bitonic over (cell, lane) keys); dead lanes last
-  const int cell = live ? ((b[0] - lo[0]) * cy + (b[1] - lo[1])) * cz + (b[2] - lo[2]) : 0x3fffff;
-  unsigned key = ((unsigned)cell << 5) | (unsigned)lane;
-#pragma unroll
-  for (int k = 2; k <= 32; k <<= 1) {
-#pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      const unsigned other = __shfl_xor_sync(0xffffffffu, key, j);
-      const bool up = ((lane & k) == 0);
-      const bool lower = (lane & j) == 0;
-      const unsigned mn = min(key, other), mx = max(key, other);
-      key = (lower == up) ? mn : mx;
-    }
-  }
-  const int src = key & 31;
-  const int mycell = (int)(key >> 5);
-  i = w0 + src;
-  const bool mlive = i < p.n;
-  // run boundaries: a lane starts a run if its cell differs from lane-1's
-  const int prev = __shfl_up_sync(0xffffffffu, mycell, 1);
-  const bool head = (lane == 0) || (prev != mycell);
-  const unsigned heads = __ballot_sync(0xffffffffu, head);
-  const unsigned after = heads & ~((2u << lane) - 1u);  // heads strictly above this lane
-  const int run_end = after ? (__ffs(after) - 1) : 32;  // first lane of the next run
-  // longest run -> number of reduction levels
-  const int run_len = head ? (run_end - lane) : 0;
-  const int max_run = __reduce_max_sync(0xffffffffu, run_len);
-  int levels = 0;
-  while ((1 << levels) < max_run) ++levels;
-  // zero the tile
+  // 2. zero the warp's node tile
   double (*tile)[kWarpTile] = s_tile[wid];
   const int nnode = nx * ny * nz;
   for (int q = lane; q < nnode; q += 32)
 #pragma unroll
     for (int ch = 0; ch < 7; ++ch) tile[ch][q] = 0.0;
-  // 3. payload of this lane's (sorted) particle
+  // 3. payload of this lane's particle (registers)
   Stencil1 s;
   double m = 0.0, mv[3] = {0.0, 0.0, 0.0}, fi[3] = {0.0, 0.0, 0.0};
   M3 mC, S;
-#pragma unroll
-  for (int k = 0; k < 9; ++k) {
-    mC.a[k] = 0.0;
-    S.a[k] = 0.0;
-  }
   int cb[3] = {0, 0, 0};
-  if (mlive) {
+  if (live) {
     particle_payload(p, i, h, dt, mats, nmat, s, m, mv, mC, S, fi, st);
 #pragma unroll
     for (int a = 0; a < 3; ++a) cb[a] = (int)s.base[a] - lo[a];
-  } else {
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      s.fx[a] = 1.0;
-      s.w[a][0] = s.w[a][1] = s.w[a][2] = 0.0;
-    }
   }
-  __syncwarp();
-  // 4. per slot: segmented reduction over the run, leader adds to the tile.
-  // Loops are not unrolled (instruction-cache footprint); per-slot weights
-  // and offsets are picked with selects so they stay in registers.
-  const double fx0 = s.fx[0], fx1 = s.fx[1], fx2 = s.fx[2];
-  const double wx0 = s.w[0][0], wx1 = s.w[0][1], wx2 = s.w[0][2];
-  const double wy0 = s.w[1][0], wy1 = s.w[1][1], wy2 = s.w[1][2];
-  const double wz0 = s.w[2][0], wz1 = s.w[2][1], wz2 = s.w[2][2];
+  // 4. slot-parallel accumulation: lane k < 27 owns stencil slot k and walks
+  // the warp's particles in lane order, adding particle p's 7 contributions
+  // to node (cell_p + offset_k).  One particle's 27 slots are 27 distinct
+  // nodes, so the tile updates need neither atomics nor a reduction, and each
+  // node's sum runs in particle order (deterministic).  The payloads travel
+  // through shared memory in two halves of 16 particles.
+  const int ox = lane / 9, oy = (lane / 3) % 3, oz = lane % 3;
+  const bool slot_lane = lane < 27;
+  double (*pay)[16] = s_pay[wid];
+  const int n_live = (int)min((long long)32, p.n - w0);
+  double acc[7];
+  int q_run = -1;  // node of the particle run being summed in acc
 #pragma unroll 1
-  for (int k = 0; k < 27; ++k) {
-    const int ox = k / 9, oy = (k / 3) % 3, oz = k % 3;
-    const double dx = (ox - fx0) * h, dy = (oy - fx1) * h, dz = (oz - fx2) * h;
-    const double wx = ox == 0 ? wx0 : (ox == 1 ? wx1 : wx2);
-    const double wy = oy == 0 ? wy0 : (oy == 1 ? wy1 : wy2);
-    const double wz = oz == 0 ? wz0 : (oz == 1 ? wz1 : wz2);
-    const double w = (wx * wy) * wz;
-    double v[7];
-    v[0] = w * m;
+  for (int half = 0; half < 2; ++half) {
+    const int p0 = 16 * half;
+    if (p0 >= n_live) break;
+    __syncwarp();
+    if ((lane >> 4) == half) {
+      const int r = lane & 15;
+      pay[0][r] = m;
 #pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      const double a = mv[d] + (mC(d, 0) * dx + mC(d, 1) * dy + mC(d, 2) * dz);
-      const double bb = S(d, 0) * dx + S(d, 1) * dy + S(d, 2) * dz;
-      v[1 + d] = w * a;
-      v[4 + d] = w * (bb + fi[d]);
-    }
-    for (int l = 0; l < levels; ++l) {
-      const int o = 1 << l;
-#pragma unroll
-      for (int ch = 0; ch < 7; ++ch) {
-        const double other = __shfl_down_sync(0xffffffffu, v[ch], o);
-        if (lane + o < run_end) v[ch] += other;
+      for (int d = 0; d < 3; ++d) {
+        pay[1 + d][r] = mv[d];
+        pay[4 + d][r] = fi[d];
+        pay[7 + d][r] = s.fx[d];
       }
-    }
-    if (head && mlive) {
-      const int q = ((cb[0] + ox) * ny + (cb[1] + oy)) * nz + (cb[2] + oz);
 #pragma unroll
-      for (int ch = 0; ch < 7; ++ch) tile[ch][q] += v[ch];
+      for (int k = 0; k < 9; ++k) {
+        pay[10 + k][r] = mC.a[k];
+        pay[19 + k][r] = S.a[k];
+        pay[28 + k][r] = s.w[k / 3][k % 3];
+      }
+      pay[37][r] = pack2i(cb[0], cb[1]);
+      pay[38][r] = pack2i(cb[2], 0);
     }
     __syncwarp();
+    if (slot_lane) {
+      // consecutive particles of one cell (sorted order) hit the same node:
+      // their contributions are summed in registers and added to the tile
+      // when the cell changes (warp-uniform, so one flush writes 27 distinct
+      // nodes), which also keeps the tile's read-modify-write chains short
+      const int pend = min(16, n_live - p0);
+#pragma unroll 1
+      for (int r = 0; r < pend; ++r) {
+        const double pm = pay[0][r];
+        const double dx = (ox - pay[7][r]) * h, dy = (oy - pay[8][r]) * h, dz = (oz - pay[9][r]) * h;
+        const double w = (pay[28 + ox][r] * pay[31 + oy][r]) * pay[34 + oz][r];
+        double v[7];
+        v[0] = w * pm;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          const double aa = pay[1 + d][r] +
+                            (pay[10 + 3 * d][r] * dx + pay[11 + 3 * d][r] * dy + pay[12 + 3 * d][r] * dz);
+          const double bb = pay[19 + 3 * d][r] * dx + pay[20 + 3 * d][r] * dy + pay[21 + 3 * d][r] * dz;
+          v[1 + d] = w * aa;
+          v[4 + d] = w * (bb + pay[4 + d][r]);
+        }
+        const int2 c01 = double_as_int2(pay[37][r]);
+        const int c2 = double_as_int2(pay[38][r]).x;
+        const int q = ((c01.x + ox) * ny + (c01.y + oy)) * nz + (c2 + oz);
+        if (q != q_run) {
+          if (q_run >= 0)
+#pragma unroll
+            for (int ch = 0; ch < 7; ++ch) tile[ch][q_run] += acc[ch];
+#pragma unroll
+          for (int ch = 0; ch < 7; ++ch) acc[ch] = v[ch];
+          q_run = q;
+        } else {
+#pragma unroll
+          for (int ch = 0; ch < 7; ++ch) acc[ch] += v[ch];
+        }
+      }
+    }
   }
+  if (slot_lane && q_run >= 0)
+#pragma unroll
+    for (int ch = 0; ch < 7; ++ch) tile[ch][q_run] += acc[ch];
+  __syncwarp();
   // 5. flush: one atomic per (node, channel).  The tile spans at most 2
   // blocks per axis (<= 8 blocks, nodes <= 10 per axis): lanes 0-7 resolve
   // one block each through the hash table, the others read them by shuffle.
