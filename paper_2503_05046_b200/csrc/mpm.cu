@@ -89,12 +89,12 @@ __device__ __forceinline__ void p2g_scatter_one(const GridDev& g, const double* 
 // P2G (mpm.py:66-99 with the stress of materials.py:113-122), warp-level.
 // Each warp takes 32 consecutive particles (the fused path sorts particles by
 // (block, cell) once per step, so a warp covers a few neighbouring cells):
-//   1. warp bounding box of the base cells; if the stencils fit a private
-//      shared-memory node tile of <= kWarpTile nodes the warp sorts its lanes
-//      by cell (bitonic, shuffles) so equal cells are contiguous lane runs;
-//   2. per stencil slot, the 7 contributions of the lanes of one cell are
-//      summed by a segmented shuffle reduction and the run leader adds them to
-//      the tile (leaders of one slot write distinct nodes: no atomics);
+//   1. warp bounding box of the base cells; the stencils must fit a private
+//      shared-memory node tile of <= kWarpTile nodes;
+//   2. slot-parallel accumulation (step 4 below): lane k < 27 owns stencil
+//      slot k and walks the warp's particles in order, summing runs of
+//      same-cell particles in registers and adding them to the tile (one
+//      particle's 27 slots are 27 distinct nodes: no atomics, no reduction);
 //   3. the tile is flushed with one float64 atomic per node and channel.
 // ~18x fewer global atomics than the per-particle scatter (27 x 7 per
 // particle), which remains the fallback for warps whose particles are spread.
