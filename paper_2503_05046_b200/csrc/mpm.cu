@@ -162,7 +162,7 @@ __device__ __forceinline__ void particle_payload(const ParticlesDev& p, long lon
 #define MPMRB_P2G_MINB 4  // resident CTAs per SM the register budget is sized for
 #endif
 #ifndef MPMRB_G2P_MINB
-#define MPMRB_G2P_MINB 1
+#define MPMRB_G2P_MINB 4
 #endif
 __global__ void __launch_bounds__(kP2GThreads, MPMRB_P2G_MINB) k_p2g(GridDev g, ParticlesDev p,
                                                      const mpmrb_material* __restrict__ mats,
