@@ -152,6 +152,12 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+#ifndef MPMRB_BAR_MONO
+#define MPMRB_BAR_MONO 1
+#endif
+__device__ __forceinline__ void red_release_add_u32(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -171,6 +177,15 @@ struct Sync {
     unsigned long long t0 = (prof || cta_in_sync) ? gtime() : 0ull;
     __syncthreads();
     if (threadIdx.x == 0) {
+#if MPMRB_BAR_MONO
+      // monotonic arrival counter: *gen holds its value at this barrier's
+      // start; every CTA adds 1 (release) and waits until all nctas arrivals
+      // have landed (acquire).  No reset and no release hop by a last arriver.
+      const unsigned target = *gen + (unsigned)nctas;
+      red_release_add_u32(bar, 1u);
+      while ((int)(ld_acquire_u32(bar) - target) < 0) __nanosleep(32);
+      *gen = target;
+#else
       const unsigned target = *gen + 1u;
       const unsigned old = atom_add_acq_rel(bar, 1u);
       if (old == (unsigned)nctas - 1u) {
@@ -180,6 +195,7 @@ struct Sync {
         while (ld_acquire_u32(bar + 32) != target) __nanosleep(64);
       }
       *gen = target;
+#endif
     }
     __syncthreads();
     if (prof) atomicAdd(prof + 10, gtime() - t0);
