@@ -290,6 +290,62 @@ def test_qn_solve_matches_reference(mp, golden, seed, ctas, monkeypatch):
         assert rep.residual_trace[-1] < rep.threshold_trace[-1] or not rep.converged
 
 
+@pytest.mark.parametrize("ctas", [0, 3])
+def test_qn_solve_is_bitwise_reproducible(mp, golden, ctas, monkeypatch):
+    """Fixed summation orders and no atomics in the solve: two runs of the same
+    problem give bit-identical velocities, impulses and traces."""
+    if ctas:
+        monkeypatch.setenv("MPMRB_SOLVER_CTAS", str(ctas))
+    g = golden("solver")
+    prob = _problem(mp, g, 1)
+    par = mp.SolverParams(eps_r=1e-8, max_iters=400)
+    v1, g1, r1 = mp.quasi_newton_solve(prob, par)
+    v2, g2, r2 = mp.quasi_newton_solve(prob, par)
+    assert np.array_equal(np_(v1), np_(v2)) and np.array_equal(np_(g1), np_(g2))
+    assert r1.iterations == r2.iterations and r1.ls_evals == r2.ls_evals
+    assert r1.residual_trace == r2.residual_trace and r1.alpha_trace == r2.alpha_trace
+
+
+@pytest.mark.parametrize("seed", [0, 1, 3])  # golden problems with contact-free nodes
+def test_qn_solve_ext_matches_full_problem(mp, golden, seed):
+    """mpmrb_qn_solve_ext (slab decomposition): the contact-free nodes held
+    outside the problem as (S0, Q0, Q1) give the same solve as the full
+    problem, and P = prod(1 - alpha) reproduces their final velocities."""
+    from paper_2503_05046_b200.solver import quasi_newton_solve_ext
+    g = golden("solver")
+    full = _problem(mp, g, seed)
+    par = mp.SolverParams(eps_r=1e-10, max_iters=3000)
+    v_full, gam_full, rep_full = mp.quasi_newton_solve(full, par)
+    m, vs, v0 = g[f"s{seed}_m"], g[f"s{seed}_v_star"], g[f"s{seed}_v_init"]
+    nodes, w = g[f"s{seed}_nodes"], g[f"s{seed}_w"]
+    used = np.unique(nodes[w != 0.0])
+    free = np.setdiff1d(np.arange(m.shape[0]), used)
+    assert free.size > 0 and used.size > 0
+    remap = -np.ones(m.shape[0], dtype=np.int64)
+    remap[used] = np.arange(used.size)
+    red_nodes = np.where(w != 0.0, remap[nodes], 0)
+    e = v0[free] - vs[free]
+    mf = m[free][:, None]
+    ext = [float((mf * e * e).sum()), float((mf * vs[free] ** 2).sum()),
+           float((mf * vs[free] * e).sum())]
+    pre = f"s{seed}_"
+    k, tau_d, eps_v, dt = g[pre + "cparams"]
+    red = mp.ContactProblem(m=m[used], v_star=vs[used], v_init=v0[used], nodes=red_nodes, w=w,
+                            frames=g[pre + "frames"], bias=g[pre + "bias"], phi=g[pre + "phi"],
+                            mu=g[pre + "mu"], gamma_lag=g[pre + "gamma_lag"],
+                            contact_params=mp.ContactParams(stiffness=k, tau_d=tau_d, eps_v=eps_v),
+                            dt=dt)
+    v_red, gam_red, rep_red, P = quasi_newton_solve_ext(red, par, ext)
+    assert abs(rep_red.iterations - rep_full.iterations) <= max(1, rep_full.iterations // 50)
+    vf = np_(v_full)
+    scale = max(1.0, _mnorm(vf, m))
+    assert _mnorm(np_(v_red) - vf[used], m[used]) <= 1e-9 * scale
+    free_v = vs[free] + P * e
+    assert _mnorm(free_v - vf[free], m[free]) <= 1e-9 * scale
+    gs = np.abs(np_(gam_full)).max()
+    assert np.abs(np_(gam_red) - np_(gam_full)).max() <= 1e-7 * gs
+
+
 def test_zero_contact_solve_returns_v_star(mp):
     rng = np.random.default_rng(2)
     m = rng.uniform(0.5, 2.0, size=6)
