@@ -97,13 +97,14 @@ __global__ void k_contact_prepare(GridDev g, const double* __restrict__ x,
 // -arm x gamma_world per body (grid-stride over the device contact count).
 constexpr int kReactCtas = 148;
 constexpr int kReactThreads = 256;
+constexpr int kReactBodies = 4;  // bodies accumulated per pass over the contacts
 
 __global__ void __launch_bounds__(kReactThreads) k_reactions(
     const int* __restrict__ counters /*nb, n_act, nc*/, const double* __restrict__ gamma,
     const double* __restrict__ frames, const double* __restrict__ witness,
     const int* __restrict__ cbody, const mpmrb_geom* __restrict__ geoms, int ngeom, int nbody,
     long long nc_cap, double* __restrict__ gamma_world, double* __restrict__ partial) {
-  __shared__ double red[32];
+  __shared__ double wsum[kReactThreads / 32][kReactBodies * 6];
   __shared__ double body_pos[kMaxBodies][3];
   const long long nc = min((long long)counters[2], nc_cap);
   for (int gi = threadIdx.x; gi < ngeom; gi += blockDim.x) {
@@ -113,8 +114,15 @@ __global__ void __launch_bounds__(kReactThreads) k_reactions(
   }
   __syncthreads();
   const int nb = nbody < kMaxBodies ? nbody : kMaxBodies;
-  for (int b = 0; b < nb; ++b) {
-    double acc[6] = {0, 0, 0, 0, 0, 0};
+  // bodies in passes of kReactBodies: each pass reads every contact once and
+  // accumulates the 6 wrench components of those bodies in registers, then
+  // reduces them all with one shared-memory exchange
+  for (int b0 = 0; b0 < nb; b0 += kReactBodies) {
+    double acc[kReactBodies][6];
+#pragma unroll
+    for (int j = 0; j < kReactBodies; ++j)
+#pragma unroll
+      for (int e = 0; e < 6; ++e) acc[j][e] = 0.0;
     for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < nc;
          c += (long long)gridDim.x * blockDim.x) {
       const double* R = frames + 9 * c;
@@ -122,23 +130,41 @@ __global__ void __launch_bounds__(kReactThreads) k_reactions(
       double gw[3];
 #pragma unroll
       for (int j = 0; j < 3; ++j) gw[j] = gm[0] * R[j] + gm[1] * R[3 + j] + gm[2] * R[6 + j];
-      if (b == 0)
+      if (b0 == 0)
 #pragma unroll
         for (int j = 0; j < 3; ++j) gamma_world[3 * c + j] = gw[j];
-      if (cbody[c] != b) continue;
-      const double arm[3] = {witness[3 * c] - body_pos[b][0], witness[3 * c + 1] - body_pos[b][1],
-                             witness[3 * c + 2] - body_pos[b][2]};
-      acc[0] += gw[0];
-      acc[1] += gw[1];
-      acc[2] += gw[2];
-      acc[3] += arm[1] * gw[2] - arm[2] * gw[1];
-      acc[4] += arm[2] * gw[0] - arm[0] * gw[2];
-      acc[5] += arm[0] * gw[1] - arm[1] * gw[0];
+      const int bj = cbody[c] - b0;
+      if (bj < 0 || bj >= kReactBodies) continue;
+      const double arm[3] = {witness[3 * c] - body_pos[cbody[c]][0],
+                             witness[3 * c + 1] - body_pos[cbody[c]][1],
+                             witness[3 * c + 2] - body_pos[cbody[c]][2]};
+      const double v6[6] = {gw[0], gw[1], gw[2], arm[1] * gw[2] - arm[2] * gw[1],
+                            arm[2] * gw[0] - arm[0] * gw[2], arm[0] * gw[1] - arm[1] * gw[0]};
+#pragma unroll
+      for (int j = 0; j < kReactBodies; ++j)
+        if (j == bj)
+#pragma unroll
+          for (int e = 0; e < 6; ++e) acc[j][e] += v6[e];
     }
-    for (int e = 0; e < 6; ++e) {
-      const double s = block_sum<kReactThreads>(acc[e], red);
-      if (threadIdx.x == 0) partial[((long long)b * 6 + e) * kReactCtas + blockIdx.x] = s;
+    // warp sums, then warp 0 adds the warps' sums in warp order
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int j = 0; j < kReactBodies; ++j)
+#pragma unroll
+      for (int e = 0; e < 6; ++e) {
+        double x = acc[j][e];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+        if (lane == 0) wsum[wid][j * 6 + e] = x;
+      }
+    __syncthreads();
+    if (threadIdx.x < kReactBodies * 6) {
+      const int j = threadIdx.x / 6, e = threadIdx.x % 6;
+      double x = 0.0;
+      for (int w = 0; w < kReactThreads / 32; ++w) x += wsum[w][threadIdx.x];
+      if (b0 + j < nb) partial[((long long)(b0 + j) * 6 + e) * kReactCtas + blockIdx.x] = x;
     }
+    __syncthreads();
   }
 }
 
