@@ -234,8 +234,7 @@ class SlabState:
             out = torch.nonzero(moving, as_tuple=False).reshape(-1)
             keep = torch.nonzero(~moving, as_tuple=False).reshape(-1)
             pay = _pack_particles(p, self.gid, out, dest[out])
-            recv = [r for r in c.allgather(pay)]
-            got = torch.cat(recv)
+            got = torch.cat(c.allgather(pay))
             got = got[got[:, 0].to(torch.int64) == c.rank] if got.numel() else got
             arrays = {k: getattr(p, k)[keep] for k in PARTICLE_FIELDS}
             gid = self.gid[keep]
