@@ -237,10 +237,38 @@ def ctx() -> C.c_void_p:
     return h
 
 
+_own_ctx: list = []  # contexts owned by simulation states (coupling.SimState)
+
+
+def new_ctx() -> C.c_void_p:
+    """A library context of its own (stream, scratch, status), for a
+    simulation state that may step concurrently with others on the device."""
+    out = C.c_void_p()
+    check(lib().mpmrb_create(device().index, C.byref(out)))
+    with _lock:
+        _own_ctx.append(out.value)
+    return out
+
+
+def free_ctx(h) -> None:
+    with _lock:
+        if h.value in _own_ctx:
+            _own_ctx.remove(h.value)
+    lib().mpmrb_destroy(h)
+
+
+def bind_stream(h, stream: torch.cuda.Stream) -> None:
+    check(lib().mpmrb_set_stream(h, C.c_void_p(stream.cuda_stream)))
+
+
 def launch_count() -> int:
+    """Kernels launched so far by every context on this device."""
     dev = device()
     h = _ctx.get(dev.index)
-    return int(lib().mpmrb_launch_count(h)) if h is not None else 0
+    n = int(lib().mpmrb_launch_count(h)) if h is not None else 0
+    with _lock:
+        own = list(_own_ctx)
+    return n + sum(int(lib().mpmrb_launch_count(C.c_void_p(v))) for v in own)
 
 
 # ----------------------------------------------------------------- tensors

@@ -114,6 +114,7 @@ class SimState:
         if not self.h > 0:
             raise ValueError("grid spacing h must be positive")
         self._sim = None
+        self._ctx = None  # the state's own library context (stream, scratch, status)
         self._stream = None
 
     @property
@@ -123,21 +124,28 @@ class SimState:
 
     def __del__(self):
         sim = getattr(self, "_sim", None)
-        if sim is not None:
-            try:
+        ctx = getattr(self, "_ctx", None)
+        try:
+            if sim is not None:
                 _lib.lib().mpmrb_sim_destroy(sim)
-            except Exception:  # pragma: no cover - interpreter shutdown
-                pass
+            if ctx is not None:
+                _lib.free_ctx(ctx)
+        except Exception:  # pragma: no cover - interpreter shutdown
+            pass
 
 
 # ------------------------------------------------------------------ fused path
 
 def _ensure_sim(state: SimState):
+    """The state's fused simulator, on a library context of its own, so that
+    several states (batched environments) can step concurrently from
+    different host threads, each on its own stream."""
     if state._sim is None:
         L = _lib.lib()
+        state._ctx = _lib.new_ctx()
+        _lib.bind_stream(state._ctx, _stream_of(state))
         h = C.c_void_p()
-        with torch.cuda.stream(_stream_of(state)):
-            _lib.check(L.mpmrb_sim_create(_lib.ctx(), C.byref(h)))
+        _lib.check(L.mpmrb_sim_create(state._ctx, C.byref(h)))
         state._sim = h
     return state._sim
 
@@ -170,7 +178,7 @@ def advance_step(state: SimState, profile: dict | None = None) -> StepSummary:
     nb = len(state.bodies)
     imp = (C.c_double * (6 * max(nb, 1)))()
     with torch.cuda.stream(stream):
-        _lib.ctx()  # bind the library context to this stream
+        _lib.bind_stream(state._ctx, stream)
         pv = p.view()
         _lib.check(L.mpmrb_sim_set_particles(sim, C.byref(pv)))
         tab, nm = material_table(state.materials)
