@@ -688,3 +688,44 @@ def test_slab_decomposition_matches_single_scene(mp, tmp_path, world):
     np.testing.assert_allclose(r["plastic"], np_(p.plastic), rtol=0, atol=1e-8)
     np.testing.assert_allclose(r["bodies"], np.array([b.position for b in st.bodies]), rtol=0,
                                atol=1e-10)
+
+
+@pytest.mark.gpu
+def test_concurrent_environments_match_sequential(mp):
+    """Each simulation state owns its library context and stream: two
+    environments stepped concurrently from two host threads give the results
+    of stepping them one after the other."""
+    import threading
+
+    from paper_2503_05046_b200 import scenes
+    from paper_2503_05046_b200.distributed import env_scene
+
+    def make(e):
+        sc = env_scene(scenes.sand_pile_scene(half=(0.03, 0.03, 0.02)), e)
+        sc["substeps"] = 4
+        return scenes.build_state(sc)
+
+    seq = [make(e) for e in range(2)]
+    for s in seq:
+        for _ in range(3):
+            mp.advance_step(s)
+    par = [make(e) for e in range(2)]
+    errs = []
+
+    def run(s):
+        try:
+            for _ in range(3):
+                mp.advance_step(s)
+        except BaseException as ex:  # pragma: no cover - surfaced below
+            errs.append(ex)
+
+    th = [threading.Thread(target=run, args=(s,)) for s in par]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for a, b in zip(seq, par):
+        np.testing.assert_allclose(np_(b.particles.x), np_(a.particles.x), rtol=0, atol=1e-12)
+        np.testing.assert_allclose(np_(b.particles.v), np_(a.particles.v), rtol=0, atol=1e-9)
+        assert b.step_index == a.step_index == 3
