@@ -1,4 +1,6 @@
 #!/bin/bash
+# NOTE: the dataflow variant this script A/B-tested was measured slower and removed;
+# the results are in profiles/r01_solver_flow_ab_*.txt and DESIGN.md section 2.
 # A/B of the dataflow solver iteration (MPMRB_SOLVER_FLOW=1, default) against
 # the barrier iteration (=0): parity tests, solver timing, bench lines.
 mkdir -p gpurun_out
