@@ -54,7 +54,10 @@ constexpr int kChunk = 32;        // contacts per ownership chunk: one warp, one
 constexpr int kWarps = kThreads / 32;
 constexpr int kSwStride = 33;  // staged weights sw[k * 33 + lane]: rows padded (bank conflicts)
 constexpr int kMaxRed = 8;        // reduction lanes per grid reduce
-constexpr int kLS = 6;            // contacts per line-search thread held in registers
+#ifndef MPMRB_KLS
+#define MPMRB_KLS 4  // = the contacts per thread the group is sized for (no dead slots)
+#endif
+constexpr int kLS = MPMRB_KLS;    // contacts per line-search thread held in registers
 
 // slot areas (64-bit words), see kSolverSlotWords
 constexpr long long kSlotA = 0;                                  // [2][ctas][6]  gather (3 values)
