@@ -693,9 +693,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
   if (nctas > 1 && CL > 1) {
     G = CL;  // the line-search group is cluster 0 (DSMEM reductions)
   } else if (nctas > 1) {
-    // ~4 contacts per thread (measured optimum between per-evaluation compute
+    // kLS contacts per thread, all in registers (4: measured optimum between
+    // per-evaluation compute
     // and the all-to-all reduction latency, which grows with the group)
-    G = (a.force_ls_ctas > 0) ? a.force_ls_ctas : (nc + kThreads * 4 - 1) / (kThreads * 4);
+    G = (a.force_ls_ctas > 0) ? a.force_ls_ctas : (nc + kThreads * kLS - 1) / (kThreads * kLS);
     if (G < 1) G = 1;
     if (G > nctas) G = nctas;
     if (G > 64) G = 64;  // slot_poll_sum<.., 2> polls at most 64 slots
