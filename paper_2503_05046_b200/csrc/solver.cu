@@ -54,6 +54,9 @@ constexpr int kChunk = 32;        // contacts per ownership chunk: one warp, one
 constexpr int kWarps = kThreads / 32;
 constexpr int kSwStride = 33;  // staged weights sw[k * 33 + lane]: rows padded (bank conflicts)
 constexpr int kMaxRed = 8;        // reduction lanes per grid reduce
+#ifndef MPMRB_HAND_SLEEP
+#define MPMRB_HAND_SLEEP 0  // ns between the group's polls of the handoff slots
+#endif
 #ifndef MPMRB_KLS
 #define MPMRB_KLS 4  // = the contacts per thread the group is sized for (no dead slots)
 #endif
@@ -951,7 +954,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
       }
       if (in_group && threadIdx.x < 32) {
         double r[3];
-        slot_poll_sum<3, (kMaxSolverCtas + 31) / 32>(base, nctas, tagA, r);
+        slot_poll_sum<3, (kMaxSolverCtas + 31) / 32, MPMRB_HAND_SLEEP>(base, nctas, tagA, r);
         fence_acq_rel_gpu();  // acquire: the producers' dvc writes are visible below
         if (threadIdx.x == 0) {
           s_bc[0] = r[0];
