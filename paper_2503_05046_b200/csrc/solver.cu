@@ -480,8 +480,15 @@ __device__ __forceinline__ void ls_terms(const ContactModel& cm, double inv_eps,
 
 // The same with the per-line-search constants of a contact precomputed
 // (LsRec): gap0 = vhat - vc_n, dvn, K dvn^2, |dvt|^2, mu gamma_lag.
+#ifndef MPMRB_LSREC7
+#define MPMRB_LSREC7 0
+#endif
 struct LsRec {
+#if MPMRB_LSREC7
+  double t0, t1, d0, d1, gap0, dvn, mug;  // K dvn^2, |dvt|^2 recomputed per evaluation
+#else
   double t0, t1, d0, d1, gap0, dvn, kdvn2, dd, mug;
+#endif
 };
 __device__ __forceinline__ LsRec ls_rec(const ContactModel& cm, const double* vc,
                                         const double* dvc, double vhat, double mug) {
@@ -492,17 +499,25 @@ __device__ __forceinline__ LsRec ls_rec(const ContactModel& cm, const double* vc
   r.d1 = dvc[1];
   r.gap0 = vhat - vc[2];
   r.dvn = dvc[2];
+#if !MPMRB_LSREC7
   r.kdvn2 = cm.K * (dvc[2] * dvc[2]);
   r.dd = dvc[0] * dvc[0] + dvc[1] * dvc[1];
+#endif
   r.mug = mug;
   return r;
 }
 __device__ __forceinline__ void ls_terms_rec(const ContactModel& cm, double eps2, double inv_eps,
                                              const LsRec& c, double alpha, double& d1,
                                              double& d2) {
+#if MPMRB_LSREC7
+  const double kdvn2 = cm.K * (c.dvn * c.dvn);
+  const double cdd = c.d0 * c.d0 + c.d1 * c.d1;
+#else
+  const double kdvn2 = c.kdvn2, cdd = c.dd;
+#endif
   const double gap = c.gap0 - alpha * c.dvn;
   if (gap > 0.0) d1 -= (cm.K * gap) * c.dvn;
-  if (gap >= 0.0) d2 += c.kdvn2;
+  if (gap >= 0.0) d2 += kdvn2;
   const double t0 = c.t0 + alpha * c.d0, t1 = c.t1 + alpha * c.d1;
   const double s2 = t0 * t0 + t1 * t1;
   const double td = t0 * c.d0 + t1 * c.d1;
@@ -510,11 +525,11 @@ __device__ __forceinline__ void ls_terms_rec(const ContactModel& cm, double eps2
     const double r = rsqrt(s2);
     const double av = c.mug * r;
     d1 += av * td;
-    d2 += av * (c.dd - (r * r) * (td * td));
+    d2 += av * (cdd - (r * r) * (td * td));
   } else {
     const double av = c.mug * inv_eps;
     d1 += av * td;
-    d2 += av * c.dd;
+    d2 += av * cdd;
   }
 }
 
