@@ -157,6 +157,12 @@ typedef struct {
   int32_t status;           /* first error of the step (MPMRB_E_*) */
   int32_t status_detail;
   int64_t status_aux;
+  /* contact solves of the step that stopped at max_iters without meeting the
+   * residual test (solver.py:358-362) and the iterations they spent */
+  int32_t substeps_unconverged;
+  int32_t reserved;
+  int64_t iterations_total;
+  int64_t iterations_unconverged;
 } mpmrb_step_stats;
 
 /* ------------------------------------------------------------------ lifecycle */

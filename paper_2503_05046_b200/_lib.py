@@ -98,7 +98,9 @@ class StepStats(C.Structure):
                 ("iterations_mean", C.c_double), ("n_contacts_mean", C.c_double),
                 ("n_active_mean", C.c_double), ("clamped", C.c_int64), ("ls_evals", C.c_int64),
                 ("regularized", C.c_int64), ("status", C.c_int32), ("status_detail", C.c_int32),
-                ("status_aux", C.c_int64)]
+                ("status_aux", C.c_int64), ("substeps_unconverged", C.c_int32),
+                ("reserved", C.c_int32), ("iterations_total", C.c_int64),
+                ("iterations_unconverged", C.c_int64)]
 
 
 _P = C.c_void_p

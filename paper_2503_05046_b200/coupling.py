@@ -89,6 +89,9 @@ class StepSummary:
     wrench: np.ndarray = None
     wall_ms: float | None = None
     ls_evals: int = 0
+    # solves that stopped at max_iters (solver.py:358-362) and their iterations
+    substeps_unconverged: int = 0
+    iterations_unconverged: int = 0
 
 
 @dataclass
@@ -226,7 +229,8 @@ def advance_step(state: SimState, profile: dict | None = None) -> StepSummary:
     if stats.regularized:
         log.warning("regularized %d near-singular Hessian blocks this step", stats.regularized)
     if not stats.all_converged:
-        log.warning("contact solve hit max_iters=%d in step %d", state.solver_params.max_iters,
+        log.warning("contact solve hit max_iters=%d in %d of %d substeps of step %d",
+                    state.solver_params.max_iters, stats.substeps_unconverged, n,
                     state.step_index)
     if stats.clamped:
         log.warning("clamped %d inverted deformation gradients (singular value floor %.2f)",
@@ -240,7 +244,8 @@ def advance_step(state: SimState, profile: dict | None = None) -> StepSummary:
         n_contacts_max=int(stats.n_contacts_max), iterations_mean=float(stats.iterations_mean),
         iterations_max=int(stats.iterations_max), all_converged=bool(stats.all_converged),
         staleness=_last_staleness(state), clamped_gradients=int(stats.clamped), wrench=wrench,
-        ls_evals=int(stats.ls_evals))
+        ls_evals=int(stats.ls_evals), substeps_unconverged=int(stats.substeps_unconverged),
+        iterations_unconverged=int(stats.iterations_unconverged))
     state.last_report = SolveReport(converged=bool(stats.all_converged),
                                     iterations=int(stats.iterations_max),
                                     n_contacts=int(stats.n_contacts_max),

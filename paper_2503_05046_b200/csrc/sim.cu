@@ -736,6 +736,10 @@ int Sim::end_step(mpmrb_step_stats* out, double* impulses_host) {
     const SubstepStat& s = st[k];
     int conv = (s.nc == 0) ? 1 : s.converged;
     out->all_converged &= conv ? 1 : 0;
+    if (!conv) {
+      out->substeps_unconverged += 1;
+      out->iterations_unconverged += s.iters;
+    }
     it_sum += s.iters;
     nc_sum += s.nc;
     act_sum += s.n_act;
@@ -744,6 +748,7 @@ int Sim::end_step(mpmrb_step_stats* out, double* impulses_host) {
     out->ls_evals += s.ls_evals;
     out->regularized += s.regularized;
   }
+  out->iterations_total = it_sum;
   if (steps_substeps > 0) {
     out->iterations_mean = (double)it_sum / steps_substeps;
     out->n_contacts_mean = (double)nc_sum / steps_substeps;
