@@ -2,23 +2,31 @@
 """Benchmark of the fused MPM + convex-contact coupling step on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload sand|sand1m|cube|cloth|tshirt|multi4m]
+                    [--workload sand1m|sand|cube|cloth|tshirt|multi4m]
 
 A "step" is one rigid coupling step (N substeps of P2G -> grid update ->
-contact detection -> device quasi-Newton solve -> G2P) of the configuration
-BASELINE.json's metric is quoted on, configs[1]: a Drucker–Prager sand block of
-~256k particles on a floor, pushed by a kinematic box.
-Inputs are synthetic (seeded jittered lattice), float64 throughout.
+contact detection -> device quasi-Newton solve -> G2P).  The default workload
+is the scene BASELINE.json's north_star quotes its steps/s target on: a
+1M-particle Drucker-Prager sand block on a floor, pushed by a kinematic box
+whose face starts at the sand's face, so every timed step is contact-loaded
+(SURVEY.md §8d C2 geometry at 0.8 x 0.8 x 0.2 m).  configs[1] (256k) is
+``--workload sand``.  Inputs are synthetic (seeded jittered lattice), float64.
+
+The timed window is the first K rigid steps of the scene from t = 0 (warm-up
+steps run first and are rolled back), with L2 flushed between steps.
 
 Metric: MPM particle-substeps/s including the convex contact solve (whole job,
-all ranks), with ms per rigid step.  Multi-GPU runs (torchrun) are batched
-independent environments, one per GPU (weak scaling, no data-path collective);
-timing is device time (CUDA events) reduced as the MAX over ranks.
+all ranks), with ms per rigid step and rigid steps/s.  ``--gpus N`` without
+torchrun re-launches itself under torch.distributed.run: N batched independent
+environments, one per GPU (weak scaling, no data-path collective); timing is
+device time (CUDA events) reduced as the MAX over ranks.
 
 The cpu_baseline leg and ``--impl reference`` time the CPU oracle port
 (oracle/, a float64 NumPy restatement of the reference, which is itself pure
-NumPy) on this host's cores on a bounded sample (one substep) of the same
-workload.
+NumPy and single-threaded) on this host on the contiguous prefix of the SAME
+window: substeps 0, 1, 2, ... of the same scene from t = 0, until a time
+budget is spent.  ``--impl reference --gpus N`` runs P = min(nproc, N)
+environments as concurrent CPU processes and sums their throughput.
 """
 
 from __future__ import annotations
@@ -26,6 +34,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -41,28 +50,33 @@ METRIC = "MPM particle-substeps/sec incl. convex contact solve; ms per rigid ste
 UNIT = "particle-substeps/s"
 PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
 FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
+WORKLOADS = ["sand1m", "sand", "cube", "cloth", "tshirt", "multi4m"]
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["sand", "sand1m", "cube", "cloth", "tshirt", "multi4m"],
-                    default="sand")
+    ap.add_argument("--workload", choices=WORKLOADS, default="sand1m")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    return ap.parse_args()
+    ap.add_argument("--ref-budget", type=float, default=90.0,
+                    help="seconds of timed CPU work per reference environment")
+    ap.add_argument("--ncu-window", action="store_true",
+                    help="only run to the profiled substep and bracket it with "
+                         "cudaProfilerStart/Stop (ncu --profile-from-start off)")
+    return ap.parse_args(argv)
 
 
 def workload_scene(name: str, rank: int = 0) -> dict:
     from paper_2503_05046_b200 import scenes
     from paper_2503_05046_b200.distributed import env_scene
     if name == "sand":
-        sc = scenes.sand_pile_scene()
+        sc = scenes.sand_pile_scene(gap=0.0)
     elif name == "sand1m":
-        sc = scenes.sand_pile_scene(half=(0.4, 0.4, 0.1))
+        sc = scenes.sand_pile_scene(half=(0.4, 0.4, 0.1), gap=0.0)
     elif name == "cloth":
         sc = scenes.cloth_sheet_scene()
         # start the sheet 3.5 mm above the sphere so the timed window is in contact
@@ -89,9 +103,11 @@ def workload_scene(name: str, rank: int = 0) -> dict:
 def workload_name(name: str, n: int, N: int) -> str:
     return {
         "sand": f"sand pile (configs[1]): {n} particles/GPU, Drucker-Prager sand, floor + "
-                f"kinematic pusher box, dt=2e-3, N={N} substeps",
+                f"kinematic pusher box (face at the sand face at t=0, +0.2 m/s), dt=2e-3, "
+                f"N={N} substeps",
         "sand1m": f"sand pile 1M (north-star target scene): {n} particles/GPU, Drucker-Prager "
-                  f"sand, floor + kinematic pusher box, dt=2e-3, N={N} substeps",
+                  f"sand, floor + kinematic pusher box (face at the sand face at t=0, "
+                  f"+0.2 m/s), dt=2e-3, N={N} substeps",
         "cube": f"elastic cube (configs[0]): {n} particles, dt=1e-3, N={N}",
         "cloth": f"cloth sheet over a sphere (configs[2]): {n} particles (vertices + faces), "
                  f"codimensional cloth, dt=2e-3, N={N}",
@@ -115,65 +131,130 @@ def peaks():
         return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
 
 
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def relaunch(args, argv) -> int:
+    """``--gpus N`` outside torchrun: re-run this script as N ranks (one per
+    GPU) under torch.distributed.run on 127.0.0.1.  Rank 0 prints the line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={_free_port()}", str(Path(__file__).resolve()), *argv]
+    return subprocess.call(cmd)
+
+
 # ------------------------------------------------------------------ CPU oracle
 
-def cpu_oracle_sample(scene: dict, budget_s: float = 30.0) -> dict:
-    """Time the oracle port on one substep of the workload (1 thread)."""
+def oracle_window(scene: dict, budget_s: float, max_substeps: int | None = None) -> dict:
+    """Time the oracle port on the contiguous prefix of the workload's window:
+    substeps 0, 1, 2, ... of the scene from t = 0 (rigid-step boundaries
+    handled exactly as oracle.step.step does), one thread, until ``budget_s``
+    of timed work is spent (at least one substep)."""
     os.environ.setdefault("OMP_NUM_THREADS", "1")
     sys.path.insert(0, str(ROOT / "tests"))
-    from scenes import oracle_state
+    from oracle import grid as og
     from oracle import step as ostep
-    sc = dict(scene)
-    sc["dt"] = scene["dt"] / scene["substeps"]
-    sc["substeps"] = 1
-    arr = host_particles(sc)
-    s = oracle_state(sc, arr["x"], arr["v"], arr["f"], arr["c"], arr["mass"], arr["vol"],
+    from scenes import oracle_state
+    arr = host_particles(scene)
+    s = oracle_state(scene, arr["x"], arr["v"], arr["f"], arr["c"], arr["mass"], arr["vol"],
                      arr["mid"])
     n = arr["x"].shape[0]
-    t0 = time.perf_counter()
-    out = ostep.step(s)
-    dt = time.perf_counter() - t0
-    return dict(value=n / dt, unit=UNIT, cores=1, kind="port",
-                sample=(f"1 substep of the full workload ({n} particles, "
-                        f"{out['n_contacts_mean']:.0f} contacts, "
-                        f"{out['iterations_mean']:.0f} solver iters) from t=0, "
-                        f"{dt:.2f} s, numpy single-thread"),
-                seconds=dt)
+    N = scene["substeps"]
+    dt_s = scene["dt"] / N
+    secs, iters, ncs = [], [], []
+    k = 0
+    while True:
+        t0 = time.perf_counter()
+        if k % N == 0:  # rigid-step start (coupling.py:168-182)
+            ostep.check_health(s)
+            og.sort_plan(s.x, s.h, s.step_index)
+            s.cache.clear()
+            s.acc_lin[:] = 0.0
+            s.acc_ang[:] = 0.0
+        info = ostep.substep(s, dt_s)
+        ostep.check_health(s)
+        if k % N == N - 1:  # rigid update (coupling.py:192-219)
+            t_new = s.time + s.dt
+            for bi, body in enumerate(s.bodies):
+                ostep.rigid_update(body, s.acc_lin[bi], s.acc_ang[bi], s.gravity, s.dt, t_new)
+            s.time = t_new
+            s.step_index += 1
+        secs.append(time.perf_counter() - t0)
+        iters.append(int(info["report"].iterations))
+        ncs.append(int(info["contacts"].n))
+        k += 1
+        if sum(secs) + secs[-1] > budget_s or (max_substeps and k >= max_substeps):
+            break
+    t = sum(secs)
+    return dict(n=n, substeps=k, seconds=t, value=n * k / t, iters=iters, contacts=ncs)
 
 
-def run_reference(args):
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return 0
-    scene = workload_scene(args.workload)
+def _window_sample_text(r: dict, N: int) -> str:
+    return (f"substeps 0..{r['substeps'] - 1} of the timed window's scene from t=0 "
+            f"(contiguous prefix of the GPU window; {r['n']} particles, "
+            f"{np.mean(r['contacts']):.0f} contacts and {np.mean(r['iters']):.1f} solver "
+            f"iterations per substep on average), {r['seconds']:.1f} s, one rigid step = "
+            f"{N} substeps")
+
+
+def _ref_worker(args_tuple):
+    workload, env, budget = args_tuple
     os.environ["OMP_NUM_THREADS"] = "1"
-    # one warm-up sample on a 1/64 subset keeps imports/allocators warm
+    scene = workload_scene(workload, env)
+    # untimed warm-up: one substep of a small sub-block (imports, allocators)
     small = json.loads(json.dumps(scene))
     for vol in small.get("volumes", []):
         vol["half"] = [a / 4 for a in vol["half"]]
-    cpu_oracle_sample(small)
-    vals, secs = [], []
-    budget = 150.0
-    t_start = time.perf_counter()
-    for i in range(max(1, args.steps)):
-        r = cpu_oracle_sample(scene)
-        vals.append(r["value"])
-        secs.append(r["seconds"])
-        if time.perf_counter() - t_start + r["seconds"] > budget:
-            break
-    value = float(np.mean(vals))
-    n = host_particles(scene)["x"].shape[0]
-    line = dict(metric=METRIC, value=value, unit=UNIT, impl="reference", n_gpus=args.gpus,
-                steps=args.steps, warmup=args.warmup,
-                ms_per_step=float(np.mean(secs)) * 1e3 * scene["substeps"],
+    if small.get("volumes"):
+        oracle_window(small, 0.0, max_substeps=1)
+    r = oracle_window(scene, budget)
+    r["N"] = scene["substeps"]
+    return r
+
+
+def run_reference(args):
+    """The reference arm: the CPU oracle port of the pure-NumPy reference on
+    this host's cores (see the module docstring)."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return 0
+    envs = max(args.gpus, world)
+    P = max(1, min(os.cpu_count() or 1, envs))
+    jobs = [(args.workload, e, args.ref_budget) for e in range(P)]
+    t_wall = time.perf_counter()
+    if P == 1:
+        res = [_ref_worker(jobs[0])]
+    else:
+        import multiprocessing as mpr
+        with mpr.get_context("spawn").Pool(P) as pool:
+            res = pool.map(_ref_worker, jobs)
+    t_wall = time.perf_counter() - t_wall
+    value = float(sum(r["value"] for r in res))
+    N = res[0]["N"]
+    steps = min(r["substeps"] for r in res)
+    ms_sub = 1e3 * float(np.mean([r["seconds"] / r["substeps"] for r in res]))
+    sample = (f"{P} concurrent process(es), one environment each; per process: "
+              + _window_sample_text(res[0], N))
+    line = dict(metric=METRIC, value=value, unit=UNIT, impl="reference", n_gpus=envs,
+                steps=steps, warmup=1, ms_per_step=ms_sub,
+                ms_per_rigid_step=ms_sub * N, rigid_steps_per_s=1e3 / (ms_sub * N),
                 higher_is_better=True, scaling="weak", vs_baseline=None, dtype="f64",
-                data="synthetic",
-                config=dict(workload=workload_name(args.workload, n, scene["substeps"]),
-                            substeps=scene["substeps"], samples_timed=len(vals)),
-                cpu_baseline=dict(value=value, unit=UNIT, cores=1, kind="port",
-                                  sample=(f"{len(vals)} x one substep of the full workload "
-                                          "from t=0 (oracle/ NumPy port of the pure-NumPy "
-                                          "reference; single-threaded by design)")),
+                data="synthetic (seeded jittered lattice)",
+                config=dict(workload=workload_name(args.workload, res[0]["n"], N),
+                            step_unit=("one SUBSTEP of the window per timed step (a rigid "
+                                       f"step is {N} substeps); steps = substeps timed per "
+                                       "process"),
+                            substeps=N, envs=P, processes=P, wall_s=t_wall,
+                            solver_iters_per_substep=[r["iters"] for r in res],
+                            contacts_per_substep=[r["contacts"] for r in res]),
+                cpu_baseline=dict(value=value, unit=UNIT, cores=P, kind="port",
+                                  sample=sample),
                 e2e=dict(value=value, unit=UNIT, h2d_bytes_per_step=0, d2h_bytes_per_step=0))
     print(json.dumps(line), flush=True)
     return 0
@@ -247,8 +328,9 @@ def algorithmic_bytes(stage: str, n: int, n_act: int, sand: bool, prof: dict | N
 
 
 def run_ours(args):
+    import copy
+
     import torch
-    import torch.distributed as dist
 
     import paper_2503_05046_b200 as mp
     from paper_2503_05046_b200 import _lib, scenes
@@ -264,10 +346,8 @@ def run_ours(args):
     N = scene["substeps"]
     sand = any(m.get("model") == "sand" for m in scene["materials"])
 
-    # The timed window always starts from the initial state (t = 0), the same
-    # state the CPU oracle sample starts from; warm-up runs on the same scene
-    # and is then rolled back (tensors restored in place, bodies re-copied).
-    import copy
+    # The timed window is the first K steps from t = 0.  Warm-up runs on the
+    # same scene and is rolled back (tensors restored in place, bodies re-copied).
     p_keys = ("x", "v", "f", "c", "plastic")
     snap = {k: getattr(state.particles, k).clone() for k in p_keys}
     d3_0 = state.cloth.d3.clone() if state.cloth is not None else None
@@ -288,17 +368,35 @@ def run_ours(args):
     torch.cuda.synchronize()
     restore()
     stream = state._stream
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
-    barrier = D.barrier
+    def profiled_step(ncu: bool = False) -> dict:
+        """Live per-stage timing of one substep in the middle of the window:
+        restore, advance half the window, profile the next step's first
+        substep (direct launches, CUDA events on the sim's stream)."""
+        restore()
+        for _ in range(args.steps // 2):
+            mp.advance_step(state)
+        prof = {"ncu": ncu}
+        mp.advance_step(state, profile=prof)
+        return prof
+
+    if args.ncu_window:
+        prof = profiled_step(ncu=True)
+        if rank == 0:
+            print(json.dumps(dict(ncu_window=args.workload, stage_ms=prof["stage_ms"],
+                                  iterations=prof["iterations"], ls_evals=prof["ls_evals"],
+                                  n_contacts=prof["n_contacts"], n_active=prof["n_active"])))
+        D.shutdown()
+        return 0
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
     # ---- timed region: K steps, L2 flushed between steps (outside timing)
     clocks = ClockSampler(local)
     clocks.start()
     launches0 = _lib.launch_count()
-    total_ms = 0.0
-    iters, ncont = [], []
-    barrier()
+    step_ms, sums = [], []
+    D.barrier()
     for _ in range(args.steps):
         with torch.cuda.stream(stream):
             flush.zero_()
@@ -309,25 +407,36 @@ def run_ours(args):
         with torch.cuda.stream(stream):
             ev1.record(stream)
         ev1.synchronize()
-        total_ms += ev0.elapsed_time(ev1)
-        iters.append(s.iterations_mean)
-        ncont.append(s.n_contacts_mean)
-    barrier()
+        step_ms.append(ev0.elapsed_time(ev1))
+        sums.append(s)
+    D.barrier()
     clk = clocks.stop()
     launches = _lib.launch_count() - launches0
-    total_ms = D.max_over_ranks(total_ms)  # device time of the job: slowest rank
+    total_ms = D.max_over_ranks(sum(step_ms))  # device time of the job: slowest rank
     ms_per_step = total_ms / args.steps
     n_all = int(D.sum_over_ranks(n))       # every rank runs its own environment
     value = D.job_throughput(n_all * N * args.steps, total_ms * 1e-3)
+    first_ms = D.max_over_ranks(step_ms[0])
 
-    # ---- live per-stage timing (one profiled substep, direct launches), taken
-    # in the middle of the timed window's regime: restore, advance half the
-    # window, profile the next step's first substep
-    restore()
-    for _ in range(args.steps // 2):
-        mp.advance_step(state)
-    prof = {}
-    mp.advance_step(state, profile=prof)
+    # solver work in the window (per rigid step: mean/max over its substeps)
+    it_total = int(sum(round(x.iterations_mean * N) for x in sums))
+    unconv = int(sum(x.substeps_unconverged for x in sums))
+    it_unconv = int(sum(x.iterations_unconverged for x in sums))
+    solver_window = dict(
+        substeps=N * args.steps, iterations_total=it_total,
+        iterations_per_substep_mean=it_total / (N * args.steps),
+        iterations_max=int(max(x.iterations_max for x in sums)),
+        iterations_mean_per_step=[round(x.iterations_mean, 2) for x in sums],
+        iterations_max_per_step=[int(x.iterations_max) for x in sums],
+        solves_at_max_iters=unconv, iterations_in_unconverged_solves=it_unconv,
+        unconverged_share_of_iterations=(it_unconv / it_total if it_total else 0.0),
+        max_iters=state.solver_params.max_iters,
+        ls_evals_total=int(sum(x.ls_evals for x in sums)),
+        contacts_mean=float(np.mean([x.n_contacts_mean for x in sums])),
+        active_nodes_mean=float(np.mean([x.n_active_nodes for x in sums])))
+
+    # ---- live per-stage timing (one profiled substep, direct launches)
+    prof = profiled_step()
     st = prof["stage_ms"]
     substep_ms = sum(st.values())
     hbm, peak_src = peaks()
@@ -340,14 +449,23 @@ def run_ours(args):
     def kernel_roof(stage: str) -> dict:
         abytes = algorithmic_bytes(stage, n, prof["n_active"], sand, prof)
         achieved = abytes / (st[stage] * 1e-3) / 1e9
-        kname = "k_qn_solve" if stage == "solve" else stage
-        return dict(bound="hbm", kernel=kname, achieved=achieved, peak=hbm, unit="GB/s",
-                    frac=achieved / hbm, traffic=traffic_all.get(kname),
-                    algorithmic_bytes=abytes, launch_ms=st[stage],
-                    share_of_substep=st[stage] / substep_ms)
+        kname = {"solve": "k_qn_solve", "p2g": "k_p2g", "g2p": "k_g2p"}[stage]
+        tr = traffic_all.get(kname) or {}
+        out = dict(bound="hbm", kernel=kname, achieved=achieved, peak=hbm, unit="GB/s",
+                   frac=achieved / hbm, traffic=tr.get("dram_bytes"),
+                   algorithmic_bytes=abytes, launch_ms=st[stage],
+                   share_of_substep=st[stage] / substep_ms)
+        if tr:
+            out["ncu"] = {k: v for k, v in tr.items() if k != "dram_bytes"}
+            if tr.get("fp64_flop") and tr.get("fp64_peak_tflops"):
+                tfl = tr["fp64_flop"] / (st[stage] * 1e-3) / 1e12
+                out["fp64"] = dict(achieved_tflops=tfl, peak_tflops=tr["fp64_peak_tflops"],
+                                   frac=tfl / tr["fp64_peak_tflops"],
+                                   flop_per_launch=tr["fp64_flop"],
+                                   note="flops from the ncu capture of the same launch "
+                                        "(sass dfma*2 + dmul + dadd), time from this run")
+        return out
 
-    # the dominant kernel of the profiled substep (the contact solve whenever
-    # contacts are present); P2G / G2P ride along as the transfer kernels
     dom = max(("solve", "p2g", "g2p"), key=lambda k: st[k])
     roofline = kernel_roof(dom)
     roofline["peak_source"] = peak_src
@@ -355,8 +473,10 @@ def run_ours(args):
         roofline["note"] = ("latency-bound: per iteration two grid barriers and ~12 "
                             "line-search group reductions (DESIGN.md section 3) leave HBM "
                             "mostly idle")
-    roofline["secondary"] = {k: kernel_roof(k) for k in ("p2g", "g2p") if k != dom}
+    roofline["secondary"] = {k: kernel_roof(k) for k in ("solve", "p2g", "g2p") if k != dom}
     roofline["stages_ms"] = st
+    roofline["profiled_substep"] = (f"substep 0 of window step {args.steps // 2} "
+                                    "(direct launches, CUDA events on the sim stream)")
     roofline["solver"] = dict(iterations=prof["iterations"], ls_evals=prof["ls_evals"],
                               contacts=prof["n_contacts"], ms=st["solve"],
                               us_per_iter=(1e3 * st["solve"] / prof["iterations"]
@@ -379,7 +499,7 @@ def run_ours(args):
         cur = torch.cuda.current_stream()
         e_ms = 0.0
         restore()
-        barrier()
+        D.barrier()
         for _ in range(ke):
             flush.zero_()
             a = torch.cuda.Event(enable_timing=True)
@@ -396,24 +516,30 @@ def run_ours(args):
         e_ms = D.max_over_ranks(e_ms)
         e2e = dict(value=D.job_throughput(n_all * N * ke, e_ms * 1e-3), unit=UNIT,
                    h2d_bytes_per_step=h2d,
-                   d2h_bytes_per_step=d2h, steps=ke, ms_per_step=e_ms / ke)
+                   d2h_bytes_per_step=d2h, steps=ke, ms_per_step=e_ms / ke,
+                   rigid_steps_per_s=1e3 * ke / e_ms)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_oracle_sample(scene)
-        cpu.pop("seconds", None)
+        r = oracle_window(scene, 30.0)
+        cpu = dict(value=r["value"], unit=UNIT, cores=1, kind="port",
+                   sample=_window_sample_text(r, N),
+                   gpu_same_prefix=("the GPU arm's first rigid step of the same window: "
+                                    f"{first_ms:.2f} ms device time"))
 
     if rank == 0:
         line = dict(
             metric=METRIC, value=value, unit=UNIT, n_gpus=world, steps=args.steps,
-            warmup=args.warmup, ms_per_step=ms_per_step, higher_is_better=True, scaling="weak",
+            warmup=args.warmup, ms_per_step=ms_per_step,
+            rigid_steps_per_s=1e3 / ms_per_step,
+            higher_is_better=True, scaling="weak",
             vs_baseline=None, dtype="f64", data="synthetic (seeded jittered lattice)",
             config=dict(workload=workload_name(args.workload, n, N),
                         particles_per_gpu=n, substeps=N, envs=world,
                         parallelism=f"{world} independent envs (1/GPU)",
+                        window="the first K rigid steps from t=0 (warm-up rolled back)",
                         l2="flushed (256 MiB write) between timed steps",
-                        contacts_mean=float(np.mean(ncont)),
-                        solver_iters_mean=float(np.mean(iters))),
+                        first_step_ms=first_ms, solver=solver_window),
             roofline=roofline, cpu_baseline=cpu, e2e=e2e, gpu_launches=int(launches),
             clocks=clk)
         print(json.dumps(line), flush=True)
@@ -421,8 +547,11 @@ def run_ours(args):
     return 0
 
 
-def main():
-    args = parse()
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
+    args = parse(argv)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args, argv)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

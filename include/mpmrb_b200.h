@@ -218,6 +218,14 @@ int mpmrb_seed_box(mpmrb_ctx* ctx, const int64_t* lo_host, const int64_t* hi_hos
 /* transfer.py:148-248 scatter_reduce: out (n_out, nch) = sum over (rows,k). */
 int mpmrb_scatter_reduce(mpmrb_ctx* ctx, const int64_t* node_ids, const double* values,
                          int64_t rows, int64_t k, int64_t nch, int64_t n_out, double* out);
+/* transfer.py:135-145,178-187 scatter_reduce(mode="deterministic"): the same
+ * sums as mpmrb_scatter_reduce, each (node, channel) folded left to right in
+ * flattened (row, slot) order from 0.0 -- the reference's np.bincount order,
+ * so the result is bitwise identical to the reference's for the same inputs
+ * and independent of any sort plan.  rows * k and n_out must be < 2^31. */
+int mpmrb_scatter_reduce_ordered(mpmrb_ctx* ctx, const int64_t* node_ids, const double* values,
+                                 int64_t rows, int64_t k, int64_t nch, int64_t n_out,
+                                 double* out);
 /* mpm.py:56-63 compute_stresses (Kirchhoff tau per particle). */
 int mpmrb_compute_stresses(mpmrb_ctx* ctx, const double* f, const int64_t* material_id,
                            int64_t n, const mpmrb_material* mats_host, int32_t n_mats,
@@ -226,6 +234,14 @@ int mpmrb_compute_stresses(mpmrb_ctx* ctx, const double* f, const int64_t* mater
 int mpmrb_p2g(mpmrb_ctx* ctx, const mpmrb_grid_view* grid, const mpmrb_particles* p,
               const mpmrb_material* mats_host, int32_t n_mats, double dt, double* mass,
               double* mom_apic, double* mom_force);
+/* mpm.py:66-99 particle_to_grid(mode="deterministic"): the reference's
+ * (n, 27, 7) contributions summed with the ordered scatter
+ * (mpmrb_scatter_reduce_ordered): every node channel is folded in particle-id
+ * / slot order, so the grid is bitwise reproducible and independent of the
+ * particle order's plan.  Same arguments as mpmrb_p2g. */
+int mpmrb_p2g_ordered(mpmrb_ctx* ctx, const mpmrb_grid_view* grid, const mpmrb_particles* p,
+                      const mpmrb_material* mats_host, int32_t n_mats, double dt, double* mass,
+                      double* mom_apic, double* mom_force);
 /* mpm.py:102-115 grid_update. */
 int mpmrb_grid_update(mpmrb_ctx* ctx, int64_t n_nodes, const double* mass,
                       const double* mom_apic, const double* mom_force,

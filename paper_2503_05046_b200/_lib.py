@@ -123,9 +123,12 @@ _SIGS = {
     "mpmrb_seed_box": ([_P, C.POINTER(_I64), C.POINTER(_I64), C.c_int32, _D, _D, C.POINTER(_D),
                         C.POINTER(_D), C.POINTER(C.c_uint64), _P, _I64, C.POINTER(_I64)], C.c_int),
     "mpmrb_scatter_reduce": ([_P, _P, _P, _I64, _I64, _I64, _I64, _P], C.c_int),
+    "mpmrb_scatter_reduce_ordered": ([_P, _P, _P, _I64, _I64, _I64, _I64, _P], C.c_int),
     "mpmrb_compute_stresses": ([_P, _P, _P, _I64, C.POINTER(Material), C.c_int32, _P], C.c_int),
     "mpmrb_p2g": ([_P, C.POINTER(GridView), C.POINTER(Particles), C.POINTER(Material), C.c_int32,
                    _D, _P, _P, _P], C.c_int),
+    "mpmrb_p2g_ordered": ([_P, C.POINTER(GridView), C.POINTER(Particles), C.POINTER(Material),
+                           C.c_int32, _D, _P, _P, _P], C.c_int),
     "mpmrb_grid_update": ([_P, _I64, _P, _P, _P, C.POINTER(_D), _D, _P, _P, _P], C.c_int),
     "mpmrb_g2p": ([_P, C.POINTER(GridView), C.POINTER(Particles), C.POINTER(Material), C.c_int32,
                    _P, _D, C.POINTER(_I64)], C.c_int),

@@ -213,7 +213,13 @@ def advance_step(state: SimState, profile: dict | None = None) -> StepSummary:
             if profile is not None and k == 0:
                 ms = (C.c_float * 7)()
                 sz = (C.c_int32 * 5)()
+                if profile.get("ncu"):  # bracket exactly this substep for ncu
+                    torch.cuda.synchronize()
+                    torch.cuda.profiler.start()
                 _lib.check(L.mpmrb_sim_profile_substep(sim, ms, sz))
+                if profile.get("ncu"):
+                    torch.cuda.synchronize()
+                    torch.cuda.profiler.stop()
                 profile["stage_ms"] = dict(zip(STAGES, [float(a) for a in ms]))
                 profile.update(n_blocks=int(sz[0]), n_active=int(sz[1]), n_contacts=int(sz[2]),
                                iterations=int(sz[3]), ls_evals=int(sz[4]))

@@ -247,6 +247,16 @@ int mpmrb_scatter_reduce(mpmrb_ctx* c, const int64_t* node_ids, const double* va
   return c->check_status("scatter_reduce");
 }
 
+int mpmrb_scatter_reduce_ordered(mpmrb_ctx* c, const int64_t* node_ids, const double* values,
+                                 int64_t rows, int64_t k, int64_t nch, int64_t n_out,
+                                 double* out) {
+  CHECK_CTX(c);
+  int rc = launch_scatter_reduce_ordered(*c, (const long long*)node_ids, values, rows, k, nch,
+                                         n_out, out);
+  if (rc) return rc;
+  return c->check_status("scatter_reduce_ordered");
+}
+
 static int upload_mats(Ctx& c, const mpmrb_material* mats_host, int n) {
   if (c.scratch[SS_MATS].grow(sizeof(mpmrb_material) * (n > 0 ? n : 1))) return MPMRB_E_CUDA;
   if (n > 0)
@@ -290,6 +300,20 @@ int mpmrb_p2g(mpmrb_ctx* c, const mpmrb_grid_view* g, const mpmrb_particles* p,
                   n_mats, dt, mass, mom_apic, mom_force);
   if (rc) return rc;
   return c->check_status("particle_to_grid");
+}
+
+int mpmrb_p2g_ordered(mpmrb_ctx* c, const mpmrb_grid_view* g, const mpmrb_particles* p,
+                      const mpmrb_material* mats_host, int32_t n_mats, double dt, double* mass,
+                      double* mom_apic, double* mom_force) {
+  CHECK_CTX(c);
+  const long long N = g->n_blocks * kNodesPerBlock;
+  int rc = upload_mats(*c, mats_host, n_mats);
+  if (rc) return rc;
+  rc = launch_p2g_ordered(*c, grid_dev(g), particles_dev(p),
+                          c->scratch[SS_MATS].as<mpmrb_material>(), n_mats, dt, N, mass,
+                          mom_apic, mom_force);
+  if (rc) return rc;
+  return c->check_status("p2g_ordered");
 }
 
 int mpmrb_grid_update(mpmrb_ctx* c, int64_t n_nodes, const double* mass, const double* mom_apic,

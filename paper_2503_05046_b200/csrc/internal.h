@@ -38,7 +38,7 @@ struct Ctx {
   DevStatus* status = nullptr;   // device
   DevStatus* status_host = nullptr;  // pinned mirror
   long long launches = 0;
-  DevBuf scratch[24];
+  DevBuf scratch[32];
   // phase timers of the solver kernel (enabled by MPMRB_SOLVER_PROF=1)
   unsigned long long* solver_prof = nullptr;
   int check_status(const char* where);  // sync + read + clear device status
@@ -48,7 +48,9 @@ struct Ctx {
 enum ScratchSlot {
   SS_TILE = 0, SS_TILE2, SS_HIST, SS_KEYS, SS_TMP0, SS_TMP1, SS_TMP2, SS_TMP3, SS_COUNT,
   SS_SOLVER0, SS_SOLVER1, SS_SOLVER2, SS_SOLVER3, SS_SOLVER4, SS_SOLVER5, SS_SOLVER6,
-  SS_SOLVER7, SS_SOLVER8, SS_MATS, SS_GEOMS, SS_PROBLEM, SS_HOSTINFO
+  SS_SOLVER7, SS_SOLVER8, SS_MATS, SS_GEOMS, SS_PROBLEM, SS_HOSTINFO,
+  // ordered (deterministic) scatter / P2G
+  SS_ORD_K, SS_ORD_I, SS_ORD_S, SS_ORD_N, SS_ORD_V, SS_ORD_O
 };
 
 inline unsigned grid_for(long long n, int threads) {
@@ -151,6 +153,14 @@ int launch_clamp(Ctx& c, const double* f, long long n, double* out, unsigned lon
 int launch_health(Ctx& c, const double* x, const double* v, long long n, double h, int* bad);
 
 // reorder.cu: once-per-step (block, cell) particle order
+int sort_pairs_u32(Ctx& c, unsigned* ka, int* va, unsigned* kb, int* vb, long long n, int bits,
+                   int* vals_out, unsigned** keys_out);
+int launch_p2g_ordered(Ctx& c, const GridDev& g, const ParticlesDev& p,
+                       const mpmrb_material* mats_dev, int nmat, double dt, long long n_nodes,
+                       double* mass, double* mom_apic, double* mom_force);
+int launch_scatter_reduce_ordered(Ctx& c, const long long* ids, const double* vals,
+                                  long long rows, long long k, long long nch, long long n_out,
+                                  double* out);
 int launch_particle_sort(Ctx& c, const double* x, long long n, double h,
                          const unsigned long long* hkeys, const int* hvals, long long hash_cap,
                          long long n_blocks_cap, unsigned* keys2, int* vals2, int* perm_out);

@@ -38,6 +38,67 @@ __global__ void k_scatter_reduce(const long long* __restrict__ ids, const double
   for (long long ch = 0; ch < nch; ++ch) atomicAdd(&out[node * nch + ch], vals[e * nch + ch]);
 }
 
+// Deterministic scatter (transfer.py:135-145, 178-187): the reference sums
+// each (node, channel) with np.bincount, i.e. sequentially in flattened
+// (row, slot) order starting from 0.0.  The entries are stably sorted by node
+// id (their entry index rides along as the value), so each node's entries sit
+// contiguously in that same order; one thread per node then folds them left
+// to right -- the same float operations in the same order as the reference,
+// hence bitwise-identical sums, independent of any sort plan.
+__global__ void k_ordered_keys(const long long* __restrict__ ids, long long e_n, long long n_out,
+                               unsigned* __restrict__ keys, int* __restrict__ vals,
+                               DevStatus* st) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < e_n;
+       e += (long long)gridDim.x * blockDim.x) {
+    long long node = ids[e];
+    if (node < 0 || node >= n_out) {
+      raise_status(st, MPMRB_E_INVALID, 12, e);
+      node = 0;
+    }
+    keys[e] = (unsigned)node;
+    vals[e] = (int)e;
+  }
+}
+
+// seg_start[node] = first sorted position with key >= node (n_out + 1 entries)
+__global__ void k_ordered_bounds(const unsigned* __restrict__ skeys, long long e_n, long long n_out,
+                                 long long* __restrict__ seg_start) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i <= e_n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long prev = i == 0 ? -1 : (long long)skeys[i - 1];
+    const long long cur = i == e_n ? n_out : (long long)skeys[i];
+    for (long long q = prev + 1; q <= cur; ++q) seg_start[q] = i;
+  }
+}
+
+template <int NCH>
+__global__ void k_ordered_sum(const int* __restrict__ sidx, const long long* __restrict__ seg_start,
+                              const double* __restrict__ vals, long long n_out, long long nch,
+                              double* __restrict__ out) {
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n_out;
+       q += (long long)gridDim.x * blockDim.x) {
+    const long long a = seg_start[q], b = seg_start[q + 1];
+    if (NCH > 0) {
+      double acc[NCH > 0 ? NCH : 1];
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) acc[ch] = 0.0;
+      for (long long j = a; j < b; ++j) {
+        const long long e = sidx[j];
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) acc[ch] += vals[e * NCH + ch];
+      }
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) out[q * NCH + ch] = acc[ch];
+    } else {
+      for (long long ch = 0; ch < nch; ++ch) {
+        double acc = 0.0;
+        for (long long j = a; j < b; ++j) acc += vals[(long long)sidx[j] * nch + ch];
+        out[q * nch + ch] = acc;
+      }
+    }
+  }
+}
+
 __global__ void k_stresses(const double* __restrict__ f, const long long* __restrict__ mid,
                            long long n, const mpmrb_material* __restrict__ mats, int nmat,
                            double* __restrict__ tau, DevStatus* st) {
@@ -155,6 +216,56 @@ __device__ __forceinline__ void particle_payload(const ParticlesDev& p, long lon
   for (int d = 0; d < 3; ++d) {
     mv[d] = m * p.v[3 * i + d];
     fi[d] = (role == MPMRB_CLOTH_VERTEX && p.fext) ? dt * p.fext[3 * i + d] : 0.0;
+  }
+}
+
+// Deterministic P2G (mpm.py:66-99 with mode="deterministic"): the (n, 27, 7)
+// per-entry contributions of the reference, materialised in its slot order
+// (x-major OFFSETS, mpm.py:25) and channel layout [w m, w (m v + m C dpos),
+// w (S dpos)], for the ordered scatter (launch_scatter_reduce_ordered).
+__global__ void k_p2g_entries(GridDev g, ParticlesDev p, const mpmrb_material* __restrict__ mats,
+                              int nmat, double dt, long long* __restrict__ nodes,
+                              double* __restrict__ vals, DevStatus* st) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= p.n) return;
+  Stencil1 s;
+  double m, mv[3], fi[3];
+  M3 mC, S;
+  particle_payload(p, i, g.h, dt, mats, nmat, s, m, mv, mC, S, fi, st);
+  StencilBlocks sb;
+  if (!resolve_blocks(s, g.hkeys, g.hvals, g.mask, sb)) {
+    raise_status(st, MPMRB_E_ALLOCATION, 23, i);
+    return;
+  }
+  const double h = g.h;
+  for (int k = 0; k < 27; ++k) {
+    const int ox = k / 9, oy = (k / 3) % 3, oz = k % 3;
+    const double dp[3] = {(ox - s.fx[0]) * h, (oy - s.fx[1]) * h, (oz - s.fx[2]) * h};
+    const double w = (s.w[0][ox] * s.w[1][oy]) * s.w[2][oz];
+    nodes[i * 27 + k] = stencil_node(s, sb, ox, oy, oz);
+    double* o = vals + (i * 27 + k) * 7;
+    o[0] = w * m;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const double a = (dp[0] * mC(d, 0) + dp[1] * mC(d, 1)) + dp[2] * mC(d, 2);
+      const double b = (dp[0] * S(d, 0) + dp[1] * S(d, 1)) + dp[2] * S(d, 2);
+      o[1 + d] = w * (mv[d] + a);
+      o[4 + d] = w * (b + fi[d]);
+    }
+  }
+}
+
+__global__ void k_split7(const double* __restrict__ in, long long n, double* __restrict__ mass,
+                         double* __restrict__ mom_apic, double* __restrict__ mom_force) {
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
+       q += (long long)gridDim.x * blockDim.x) {
+    const double* r = in + 7 * q;
+    mass[q] = r[0];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      mom_apic[3 * q + d] = r[1 + d];
+      mom_force[3 * q + d] = r[4 + d];
+    }
   }
 }
 
@@ -606,6 +717,49 @@ int launch_scatter_reduce(Ctx& c, const long long* ids, const double* vals, long
   return MPMRB_OK;
 }
 
+int launch_scatter_reduce_ordered(Ctx& c, const long long* ids, const double* vals,
+                                  long long rows, long long k, long long nch, long long n_out,
+                                  double* out) {
+  const long long e_n = rows * k;
+  if (n_out == 0) return MPMRB_OK;
+  if (e_n == 0) {
+    MPMRB_CUDA_OK(cudaMemsetAsync(out, 0, sizeof(double) * n_out * nch, c.stream));
+    return MPMRB_OK;
+  }
+  if (e_n >= (1LL << 31) || n_out >= (1LL << 31))
+    return set_error(MPMRB_E_INVALID, "ordered scatter: %lld entries / %lld nodes exceed int32",
+                     e_n, n_out);
+  // scratch: keys 2 e_n (u32), idx 3 e_n (i32), seg_start n_out + 1 (i64)
+  if (c.scratch[SS_ORD_K].grow(sizeof(unsigned) * 2 * e_n) ||
+      c.scratch[SS_ORD_I].grow(sizeof(int) * 3 * e_n) ||
+      c.scratch[SS_ORD_S].grow(sizeof(long long) * (n_out + 1)))
+    return MPMRB_E_CUDA;
+  unsigned* keys = c.scratch[SS_ORD_K].as<unsigned>();
+  int* idx = c.scratch[SS_ORD_I].as<int>();
+  long long* seg = c.scratch[SS_ORD_S].as<long long>();
+  k_ordered_keys<<<grid_for(e_n, 256), 256, 0, c.stream>>>(ids, e_n, n_out, keys, idx, c.status);
+  c.launches++;
+  int bits = 1;
+  while ((1LL << bits) < n_out) ++bits;
+  unsigned* skeys = nullptr;
+  int rc = sort_pairs_u32(c, keys, idx, keys + e_n, idx + e_n, e_n, bits, idx + 2 * e_n, &skeys);
+  if (rc) return rc;
+  k_ordered_bounds<<<grid_for(e_n + 1, 256), 256, 0, c.stream>>>(skeys, e_n, n_out, seg);
+  c.launches++;
+  const int* sidx = idx + 2 * e_n;
+  const unsigned g = grid_for(n_out, 128);
+  switch (nch) {
+    case 1: k_ordered_sum<1><<<g, 128, 0, c.stream>>>(sidx, seg, vals, n_out, nch, out); break;
+    case 3: k_ordered_sum<3><<<g, 128, 0, c.stream>>>(sidx, seg, vals, n_out, nch, out); break;
+    case 7: k_ordered_sum<7><<<g, 128, 0, c.stream>>>(sidx, seg, vals, n_out, nch, out); break;
+    case 9: k_ordered_sum<9><<<g, 128, 0, c.stream>>>(sidx, seg, vals, n_out, nch, out); break;
+    default: k_ordered_sum<0><<<g, 128, 0, c.stream>>>(sidx, seg, vals, n_out, nch, out); break;
+  }
+  c.launches++;
+  MPMRB_CUDA_OK(cudaGetLastError());
+  return MPMRB_OK;
+}
+
 int launch_stresses(Ctx& c, const double* f, const long long* mid, long long n,
                     const mpmrb_material* mats_dev, int nmat, double* tau) {
   if (n == 0) return MPMRB_OK;
@@ -620,6 +774,36 @@ int launch_p2g(Ctx& c, const GridDev& g, const ParticlesDev& p, const mpmrb_mate
   if (p.n == 0) return MPMRB_OK;
   k_p2g<<<grid_for(p.n, kP2GThreads), kP2GThreads, 0, c.stream>>>(g, p, mats_dev, nmat, dt, mass,
                                                                   mom_apic, mom_force, c.status);
+  c.launches++;
+  MPMRB_CUDA_OK(cudaGetLastError());
+  return MPMRB_OK;
+}
+
+int launch_p2g_ordered(Ctx& c, const GridDev& g, const ParticlesDev& p,
+                       const mpmrb_material* mats_dev, int nmat, double dt, long long n_nodes,
+                       double* mass, double* mom_apic, double* mom_force) {
+  if (p.n == 0 || n_nodes == 0) {
+    if (n_nodes) {
+      MPMRB_CUDA_OK(cudaMemsetAsync(mass, 0, 8 * n_nodes, c.stream));
+      MPMRB_CUDA_OK(cudaMemsetAsync(mom_apic, 0, 24 * n_nodes, c.stream));
+      MPMRB_CUDA_OK(cudaMemsetAsync(mom_force, 0, 24 * n_nodes, c.stream));
+    }
+    return MPMRB_OK;
+  }
+  const long long e_n = p.n * 27;
+  if (c.scratch[SS_ORD_N].grow(sizeof(long long) * e_n) ||
+      c.scratch[SS_ORD_V].grow(sizeof(double) * 7 * e_n) ||
+      c.scratch[SS_ORD_O].grow(sizeof(double) * 7 * n_nodes))
+    return MPMRB_E_CUDA;
+  long long* nodes = c.scratch[SS_ORD_N].as<long long>();
+  double* vals = c.scratch[SS_ORD_V].as<double>();
+  double* out7 = c.scratch[SS_ORD_O].as<double>();
+  k_p2g_entries<<<grid_for(p.n, 128), 128, 0, c.stream>>>(g, p, mats_dev, nmat, dt, nodes, vals,
+                                                         c.status);
+  c.launches++;
+  int rc = launch_scatter_reduce_ordered(c, nodes, vals, p.n, 27, 7, n_nodes, out7);
+  if (rc) return rc;
+  k_split7<<<grid_for(n_nodes, 256), 256, 0, c.stream>>>(out7, n_nodes, mass, mom_apic, mom_force);
   c.launches++;
   MPMRB_CUDA_OK(cudaGetLastError());
   return MPMRB_OK;

@@ -140,21 +140,12 @@ unsigned gs_grid(long long n, int threads) {
 
 }  // namespace
 
-int launch_particle_sort(Ctx& c, const double* x, long long n, double h,
-                         const unsigned long long* hkeys, const int* hvals, long long hash_cap,
-                         long long n_blocks_cap, unsigned* keys2, int* vals2, int* perm_out) {
-  if (n == 0) return MPMRB_OK;
-  const unsigned mask = (unsigned)(hash_cap - 1);
-  unsigned* ka = keys2;
-  unsigned* kb = keys2 + n;
-  int* va = vals2;
-  int* vb = vals2 + n;
-  k_sort_keys<<<gs_grid(n, 256), 256, 0, c.stream>>>(x, n, h, hkeys, hvals, mask, ka, va,
-                                                     c.status);
-  c.launches++;
-  int bits = 6;
-  while ((1LL << (bits - 6)) < n_blocks_cap) ++bits;
-  const int passes = (bits + 7) / 8;
+// Stable LSD radix sort of (key, value) pairs on the low `bits` bits of the
+// keys.  Ping-pongs between (ka, va) and (kb, vb); the final values go to
+// vals_out (which may alias neither input) and the final keys to *keys_out.
+int sort_pairs_u32(Ctx& c, unsigned* ka, int* va, unsigned* kb, int* vb, long long n, int bits,
+                   int* vals_out, unsigned** keys_out) {
+  const int passes = bits <= 0 ? 1 : (bits + 7) / 8;
   const int ntiles = (int)((n + kRTile - 1) / kRTile);
   const long long hist_n = (long long)kRBuckets * ntiles;
   if (c.scratch[SS_HIST].grow(sizeof(int) * hist_n) || c.scratch[SS_TMP0].grow(sizeof(int) * hist_n))
@@ -169,7 +160,7 @@ int launch_particle_sort(Ctx& c, const double* x, long long n, double h,
     if (rc) return rc;
     const bool last = p == passes - 1;
     k_radix_scatter<<<cta, kRWarps * 32, 0, c.stream>>>(ka, va, n, shift, ntiles, scanned, kb,
-                                                        last ? perm_out : vb);
+                                                        last ? vals_out : vb);
     c.launches += 2;
     unsigned* tk = ka;
     ka = kb;
@@ -178,8 +169,26 @@ int launch_particle_sort(Ctx& c, const double* x, long long n, double h,
     va = vb;
     vb = tv;
   }
+  if (keys_out) *keys_out = ka;
   MPMRB_CUDA_OK(cudaGetLastError());
   return MPMRB_OK;
+}
+
+int launch_particle_sort(Ctx& c, const double* x, long long n, double h,
+                         const unsigned long long* hkeys, const int* hvals, long long hash_cap,
+                         long long n_blocks_cap, unsigned* keys2, int* vals2, int* perm_out) {
+  if (n == 0) return MPMRB_OK;
+  const unsigned mask = (unsigned)(hash_cap - 1);
+  unsigned* ka = keys2;
+  unsigned* kb = keys2 + n;
+  int* va = vals2;
+  int* vb = vals2 + n;
+  k_sort_keys<<<gs_grid(n, 256), 256, 0, c.stream>>>(x, n, h, hkeys, hvals, mask, ka, va,
+                                                     c.status);
+  c.launches++;
+  int bits = 6;
+  while ((1LL << (bits - 6)) < n_blocks_cap) ++bits;
+  return sort_pairs_u32(c, ka, va, kb, vb, n, bits, perm_out, nullptr);
 }
 
 int launch_particle_gather(Ctx& c, const int* perm, long long n, const double* src, int width,

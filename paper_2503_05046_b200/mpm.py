@@ -62,9 +62,13 @@ def particle_to_grid(particles: ParticleSet, grid: SparseGrid, stencil: Stencil 
                      materials: list[Material], dt: float, plan: SortPlan, epoch: int,
                      mode: str = "deterministic", workers: int | None = None,
                      stats: ScatterStats | None = None) -> None:
-    """Fill grid.mass, grid.mom_apic, grid.mom_force (mpm.py:66-99) in one
-    fused stress + 27x7 scatter kernel.  ``stencil`` is accepted for API
-    compatibility; the kernel recomputes it from particles.x."""
+    """Fill grid.mass, grid.mom_apic, grid.mom_force (mpm.py:66-99).
+    ``mode="deterministic"`` (the reference's default) materialises the
+    (n, 27, 7) contributions and sums every node channel in particle-id /
+    slot order (ordered scatter: bitwise reproducible, plan-independent);
+    ``mode="fast"`` is one fused stress + 27x7 scatter kernel with float64
+    atomics.  ``stencil`` is accepted for API compatibility; the kernels
+    recompute it from particles.x."""
     if epoch != plan.epoch:
         raise PlanEpochError(f"plan epoch {plan.epoch} used in step {epoch}")
     if mode not in ("deterministic", "fast"):
@@ -72,9 +76,9 @@ def particle_to_grid(particles: ParticleSet, grid: SparseGrid, stencil: Stencil 
     tab, nm = material_table(materials)
     g = grid.view()
     pv = particles.view()
-    _lib.check(_lib.lib().mpmrb_p2g(_lib.ctx(), C.byref(g), C.byref(pv), tab, nm, float(dt),
-                                    _lib.ptr(grid.mass), _lib.ptr(grid.mom_apic),
-                                    _lib.ptr(grid.mom_force)))
+    fn = _lib.lib().mpmrb_p2g_ordered if mode == "deterministic" else _lib.lib().mpmrb_p2g
+    _lib.check(fn(_lib.ctx(), C.byref(g), C.byref(pv), tab, nm, float(dt), _lib.ptr(grid.mass),
+                  _lib.ptr(grid.mom_apic), _lib.ptr(grid.mom_force)))
     if stats is not None:
         stats.rows = particles.n
         stats.chunks = 1

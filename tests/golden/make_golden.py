@@ -363,6 +363,62 @@ def gen_steps():
     save("steps", **out)
 
 
+def _c1_run(mode, workers):
+    from mpmrb.coupling import advance_step
+    from paper_2503_05046_b200.scenes import elastic_cube_scene
+    scene = elastic_cube_scene()
+    st = build_ref_state(scene)
+    st.mode, st.workers = mode, workers
+    p = st.particles
+    out = dict(scene_json=np.array(json.dumps(scene)), x0=p.x.copy(), v0=p.v.copy())
+    keep = (10, 25, 50, 75, 100)
+    wr, nc, ncmax, it, itmax, conv, act = [], [], [], [], [], [], []
+    for k in range(1, scene["steps"] + 1):
+        s = advance_step(st)
+        wr.append(s.wrench)
+        nc.append(s.n_contacts_mean)
+        ncmax.append(s.n_contacts_max)
+        it.append(s.iterations_mean)
+        itmax.append(s.iterations_max)
+        conv.append(s.all_converged)
+        act.append(s.n_active_nodes)
+        if k in keep:
+            out[f"x_{k}"] = st.particles.x.copy()
+            out[f"v_{k}"] = st.particles.v.copy()
+        if k % 10 == 0:
+            print(f"c1 {mode} step {k}: contacts {s.n_contacts_mean:.1f} "
+                  f"iters {s.iterations_mean:.2f}", flush=True)
+    out.update(wrench=np.stack(wr), contacts_mean=np.array(nc), contacts_max=np.array(ncmax),
+               iters_mean=np.array(it), iters_max=np.array(itmax), conv=np.array(conv),
+               active_mean=np.array(act),
+               bodies_pos=np.array([b.position for b in st.bodies]))
+    return out
+
+
+def gen_c1():
+    """configs[0]: the 8,000-particle elastic cube dropped
+    onto a kinematic ground box, h = 0.01, dt = 1e-3, N = 10, run for the full
+    100 rigid steps through the reference's advance_step (coupling.py:168-219)
+    in its default deterministic mode.  Stored per step: wrench, contact /
+    iteration means, convergence, active nodes; particle x / v at steps 10,
+    25, 50, 75, 100.
+
+    The same run in the reference's own "fast" mode (transfer.py:204-248:
+    bin-ordered chunks summed by 4 workers, then merged -- a different float
+    summation order that the reference tolerates at <= 1e-12 per scatter,
+    test_transfer.py:85-93) is stored under ``fast_*``: the trajectory
+    divergence that reassociation alone causes in the reference itself."""
+    import sys as _s
+    _s.path.insert(0, str(Path(__file__).resolve().parents[2]))
+    det = _c1_run("deterministic", None)
+    fast = _c1_run("fast", 4)
+    out = dict(det)
+    for k, v in fast.items():
+        if k not in ("scene_json", "x0", "v0"):
+            out[f"fast_{k}"] = v
+    save("c1_cube", **out)
+
+
 def gen_outputs():
     """Reference frame bytes (outputs.py:33-42), CSV frame and contact log
     (outputs.py:61-105) for small seeded arrays."""

@@ -50,6 +50,15 @@ def variant(base, name):
         for p in [pusher["position"]] + pusher["trajectory"]["positions"]:
             p[0] += 0.006
             p[2] += 0.03
+    elif name == "touch3":
+        # the bench scene: eps_v = 1e-3, pusher face starting at the sand face
+        v["contact"]["eps_v"] = 1e-3
+        for p in [pusher["position"]] + pusher["trajectory"]["positions"]:
+            p[0] += 0.005
+    elif name == "inside3":
+        v["contact"]["eps_v"] = 1e-3
+        for p in [pusher["position"]] + pusher["trajectory"]["positions"]:
+            p[0] += 0.006
     elif name == "elastic":
         v["materials"][0]["model"] = "elastic"
     elif name == "eps_r1e-1":
@@ -91,7 +100,7 @@ def main():
     steps = int(sys.argv[1]) if len(sys.argv) > 1 else 25
     half = tuple(float(a) for a in sys.argv[2].split(",")) if len(sys.argv) > 2 else (0.2, 0.2, 0.1)
     names = sys.argv[3:] or ["base"]
-    base = scenes.sand_pile_scene(half=half)
+    base = scenes.sand_pile_scene(half=half, eps_v=1e-4)  # round-1 scene
     for nm in names:
         t0 = time.perf_counter()
         run(variant(base, nm), steps, nm)

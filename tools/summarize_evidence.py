@@ -1,6 +1,6 @@
 """Summarise the round's GPU evidence for profiles/:
 
-    python tools/summarize_evidence.py LAUNCHES.csv NCU.ncu-rep TAG
+    python tools/summarize_evidence.py LAUNCHES.csv NCU.ncu-rep TAG [WORKLOAD] [ROUND] [CMD]
 
 * the ncu launch list (`--metrics gpu__time_duration.sum`) -> per-kernel
   launches, total device time, share and us/launch;
@@ -87,26 +87,38 @@ def full(path: Path):
         grid = r[col["Grid Size"]]
         lines.append(f"{k:14s} {grid:>10s} {d:9.2f} {b / 1e6:9.2f} {b / d / 1e3 if d else 0:10.1f} "
                      f"{l2:8.2f} {occ:7.2f} {regs:5.0f}")
-        traffic[k] = b
+        fl = (2.0 * get(r, "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum", 0.0)
+              + get(r, "smsp__sass_thread_inst_executed_op_dmul_pred_on.sum", 0.0)
+              + get(r, "smsp__sass_thread_inst_executed_op_dadd_pred_on.sum", 0.0))
+        traffic[k] = dict(dram_bytes=b, fp64_flop=fl or None, cold_duration_us=d,
+                          l2_hit_pct=l2, occupancy_pct=occ, registers=regs)
+        lines[-1] += f"  fp64 GFLOP {fl / 1e9:8.3f}"
     return "\n".join(lines) + "\n", traffic
 
 
-def main(launch_csv, ncu_rep, tag):
+def main(launch_csv, ncu_rep, tag, workload="sand1m", rnd="r02",
+         cmd="python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-e2e"):
     prof = ROOT / "profiles"
     if launch_csv != "-":
-        (prof / f"r01_launches_{tag}_summary.txt").write_text(
-            launches(Path(launch_csv), "python bench.py --steps 20 --warmup 3 --no-cpu-baseline "
-                                       "--no-e2e  (256k sand pile)"))
+        (prof / f"{rnd}_launches_{tag}_summary.txt").write_text(
+            launches(Path(launch_csv), f"{cmd}  (workload {workload})"))
     if ncu_rep != "-":
         txt, traffic = full(Path(ncu_rep))
-        (prof / f"r01_ncu_{tag}_summary.txt").write_text(
-            f"ncu --set full --clock-control none ({Path(ncu_rep).name}; one launch each)\n" + txt)
+        (prof / f"{rnd}_ncu_{tag}_summary.txt").write_text(
+            f"ncu --set full --clock-control none ({Path(ncu_rep).name}; one launch each, "
+            "the profiled substep of bench.py --ncu-window)\n" + txt)
+        peak = None
+        pf = prof / "fp_peak.json"
+        if pf.exists():
+            peak = json.loads(pf.read_text()).get("fp64_fma_tflops")
         tf = prof / "ncu_traffic.json"
         d = json.loads(tf.read_text()) if tf.exists() else {}
-        d["_note"] = ("dram__bytes_read.sum + dram__bytes_write.sum per launch from ncu --set full "
-                      f"(profiles/r01_ncu_{tag}_summary.txt); bench.py reports it as roofline.traffic")
-        d.setdefault("sand", {}).update({("k_qn_solve" if k == "k_qn_solve" else k.replace("k_", "")): v
-                                         for k, v in traffic.items()})
+        d["_note"] = ("per launch, from ncu --set full of the SAME profiled substep bench.py "
+                      "times (bench.py --ncu-window, ncu --profile-from-start off): dram_bytes = "
+                      "dram__bytes_read.sum + dram__bytes_write.sum (roofline.traffic); fp64_flop "
+                      "= 2 dfma + dmul + dadd thread instructions; fp64_peak_tflops from "
+                      "profiles/fp_peak.json (tools/fp_peak.cu)")
+        d[workload] = {k: dict(v, fp64_peak_tflops=peak) for k, v in traffic.items()}
         tf.write_text(json.dumps(d, indent=1) + "\n")
 
 
