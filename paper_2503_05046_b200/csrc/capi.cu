@@ -504,12 +504,12 @@ static int qn_solve_impl(mpmrb_ctx* c, const mpmrb_problem* pr, const mpmrb_solv
   rc |= c->scratch[SS_SOLVER0].grow(4 * 27 * ncc);           // cnodes
   rc |= c->scratch[SS_SOLVER1].grow(8 * 27 * ncc);           // cw
   rc |= c->scratch[SS_SOLVER2].grow(8 * 3 * ndd);            // dv
-  rc |= c->scratch[SS_SOLVER3].grow(8 * kCellSumStride * 27 * ncc);  // cellsum
+  rc |= c->scratch[SS_SOLVER3].grow(8 * kCellSumStride * ncc);  // contact records
   rc |= c->scratch[SS_SOLVER4].grow(8 * 8 * ncc);            // vc, dvc, vhat, mug
   rc |= c->scratch[SS_SOLVER5].grow(8 * (2 * 8 * kMaxSolverCtas + 8));  // grid partials
   rc |= c->scratch[SS_SOLVER6].grow(4096);                   // sizes, SolveOut
   rc |= c->scratch[SS_SOLVER7].grow(4 * 12 * (ndd + 2) + 64);  // node adjacency ints
-  rc |= c->scratch[SS_SOLVER8].grow(2 * 4 * 27 * ncc);       // adjacency entries (+tmp)
+  rc |= c->scratch[SS_SOLVER8].grow(3 * 4 * 27 * ncc);       // adjacency entries (int2) + tmp
   rc |= c->scratch[SS_PROBLEM].grow(4 * 4 * (ncc + 2));      // contact groups
   rc |= c->scratch[SS_HOSTINFO].grow(kSolverSyncBytes);  // reduction slots, tags, barrier
   if (rc) return MPMRB_E_CUDA;
@@ -549,8 +549,8 @@ static int qn_solve_impl(mpmrb_ctx* c, const mpmrb_problem* pr, const mpmrb_solv
     su.head_off = ci + (ncc + 2);
     su.grp_of = ci + 2 * (ncc + 2);
     su.grp_start = ci + 3 * (ncc + 2);
-    su.ent = c->scratch[SS_SOLVER8].as<int>();
-    su.ent_tmp = su.ent + 27 * ncc;
+    su.ent = c->scratch[SS_SOLVER8].as<int2>();
+    su.ent_tmp = reinterpret_cast<int*>(su.ent + 27 * ncc);
   }
   rc = launch_solver_setup(*c, sizes, sizes + 1, nd, nc, c->scratch[SS_SOLVER0].as<int>(), su,
                            c->scratch[SS_TILE]);
@@ -605,9 +605,6 @@ static int qn_solve_impl(mpmrb_ctx* c, const mpmrb_problem* pr, const mpmrb_solv
   if (force) a.force_ctas = atoi(force);
   const char* force_ls = getenv("MPMRB_SOLVER_LS_CTAS");
   if (force_ls) a.force_ls_ctas = atoi(force_ls);
-  a.ls_mode = getenv("MPMRB_LS_MODE") ? atoi(getenv("MPMRB_LS_MODE")) : 0;
-  a.node_lanes = getenv("MPMRB_NODE_LANES") ? atoi(getenv("MPMRB_NODE_LANES")) : 0;
-  if (a.node_lanes != 2 && a.node_lanes != 4) a.node_lanes = 0;
   for (int k = 0; k < 3; ++k) a.ext_free[k] = ext_free ? ext_free[k] : 0.0;
   double* p_dev = reinterpret_cast<double*>(misc + 2304 + 256);  // after SolveOut
   a.p_out = p_dev;

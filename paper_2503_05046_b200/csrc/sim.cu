@@ -318,8 +318,8 @@ int Sim::reserve(long long n, long long nb_needed) {
   rc |= b_sdvc.grow(8 * 3 * nc_cap);
   rc |= b_su_c.grow(4 * 4 * (nc_cap + 2));  // head, head_off, grp_of, grp_start
   rc |= b_su_n.grow(4 * 12 * (N + 2) + 64);  // cnt, fill, off, flag, flag_off, cn, fn, counts, cn_rec
-  rc |= b_su_ent.grow(2 * 4 * 27 * nc_cap);
-  rc |= b_cellsum.grow(8 * kCellSumStride * 27 * nc_cap);
+  rc |= b_su_ent.grow(3 * 4 * 27 * nc_cap);  // entries (int2) + tmp
+  rc |= b_cellsum.grow(8 * kCellSumStride * nc_cap);  // per-contact records
   rc |= b_gamma.grow(8 * 3 * nc_cap);
   rc |= b_gworld.grow(8 * 3 * nc_cap);
   long long scan_n = (N + 1) > (n + 1) ? (N + 1) : (n + 1);
@@ -409,8 +409,8 @@ int Sim::capture_or_launch() {
     su.fn = ni + 6 * (N + 2);
     su.counts = ni + 7 * (N + 2);
     su.cn_rec = reinterpret_cast<int4*>(ni + 8 * (N + 2));
-    su.ent = b_su_ent.as<int>();
-    su.ent_tmp = su.ent + 27 * nc_cap;
+    su.ent = b_su_ent.as<int2>();
+    su.ent_tmp = reinterpret_cast<int*>(su.ent + 27 * nc_cap);
   }
   rc = launch_solver_setup(c, counters + 1, counters + 2, N, nc_cap, b_cnodes.as<int>(), su,
                            b_tiles);
@@ -443,9 +443,6 @@ int Sim::capture_or_launch() {
   a.skip_if_no_contacts = 1;
   a.force_ctas = force_ctas;
   a.force_ls_ctas = force_ls_ctas;
-  a.ls_mode = getenv("MPMRB_LS_MODE") ? atoi(getenv("MPMRB_LS_MODE")) : 0;
-  a.node_lanes = getenv("MPMRB_NODE_LANES") ? atoi(getenv("MPMRB_NODE_LANES")) : 0;
-  if (a.node_lanes != 2 && a.node_lanes != 4) a.node_lanes = 0;
   a.ext_free[0] = a.ext_free[1] = a.ext_free[2] = 0.0;
   a.p_out = nullptr;
   a.v = b_sv.as<double>();

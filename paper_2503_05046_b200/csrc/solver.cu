@@ -3,18 +3,21 @@
 // cooperative kernel: no host round trip per iteration or per line-search
 // evaluation.
 //
-// Structure (v4).
+// Structure (v5).
 //  * Free nodes (active nodes no contact stencil touches) have g = m(v - v*),
 //    H = m I, so dv = -(v - v*) and v - v* shrinks by (1 - alpha) per step.
 //    Their whole contribution to every reduction is a closed form in
 //    P = prod(1 - alpha) and three sums taken once (S0, Q0, Q1 below); they
 //    are written once, in the epilogue, as v = v* + P (v0 - v*).  The
 //    iteration only touches contact nodes and contacts.
-//  * Contacts are grouped by identical stencils (all contacts of one grid cell
-//    share their 27 nodes).  The contact owners sum w R^T g_c and w^2 R^T G R
-//    per (group, slot) ("cellsum"); each contact node gathers its (group, slot)
-//    entries through a sorted CSR.  Fixed summation order, no atomics: a solve
-//    is bitwise reproducible run to run.
+//  * Each contact owner writes one 80 B record per iteration: R^T g_c and
+//    R^T G_c R.  Each contact node gathers the records of the contacts whose
+//    stencil holds it, weighted by w and w^2 of its slot, through a sorted CSR
+//    of (contact run, slot) entries (the contacts of one grid cell share all
+//    27 nodes and form one run).  Fixed summation order (ascending contact id
+//    per node), no atomics: a solve is bitwise reproducible run to run.  (v4
+//    summed w R^T g per (run, slot) in the contact phase instead: 27 records
+//    per run, ~100 MB written and read per iteration at 1M particles.)
 //  * The exact line search (solver.py:266-298) runs on a small group of CTAs
 //    (sized to the contact count) whose all-reduces use fence-free
 //    self-validating slots (~1 us for 16 CTAs vs ~3 us for a 148-CTA grid
@@ -22,19 +25,17 @@
 //    one rsqrt, no division.
 //
 // Phases per iteration (solver.py:338-357):
-//   N  contact nodes: pending v += alpha dv, gather cellsum -> J^T g and the
+//   N  contact nodes: pending v += alpha dv, gather records -> J^T g and the
 //      Hessian block, gradient, residual/norms, 3x3 Cholesky -> dv, a1, a2;
 //      free-node terms in closed form                         [grid reduce]
 //   D  contacts: dvc = R J dv and phi'(0)            [gather to the LS group]
 //   LS group: <= ls_max evaluations                [group reduce each]
 //      -> alpha broadcast to every CTA
-//   U  contacts: vc += alpha dvc, contact gradient/Hessian -> cellsum
+//   U  contacts: vc += alpha dvc, contact gradient/Hessian -> records
 //                                                             [grid sync]
 //
 // vc is advanced as vc + alpha dvc (= R J (v + alpha dv) + b exactly in real
 // arithmetic) instead of being re-gathered from v; the difference is roundoff.
-#include <cooperative_groups.h>
-
 #include <cstdio>
 #include <cstdlib>
 
@@ -42,8 +43,6 @@
 #include "contact.cuh"
 #include "internal.h"
 #include "solver.cuh"
-
-namespace cg = cooperative_groups;
 
 namespace mpmrb {
 
@@ -54,19 +53,15 @@ constexpr int kChunk = 32;        // contacts per ownership chunk: one warp, one
 constexpr int kWarps = kThreads / 32;
 constexpr int kSwStride = 33;  // staged weights sw[k * 33 + lane]: rows padded (bank conflicts)
 constexpr int kMaxRed = 8;        // reduction lanes per grid reduce
-#ifndef MPMRB_HAND_SLEEP
-#define MPMRB_HAND_SLEEP 0  // ns between the group's polls of the handoff slots
-#endif
-#ifndef MPMRB_KLS
-#define MPMRB_KLS 4  // = the contacts per thread the group is sized for (no dead slots)
-#endif
-constexpr int kLS = MPMRB_KLS;    // contacts per line-search thread held in registers
+// contacts per line-search thread held in registers (= the contacts per thread
+// the group is sized for, so no dead slots; 3 and 5 measured slower at 2M)
+constexpr int kLS = 4;
+constexpr int kEPL = 4;  // phase N: adjacency entries per lane in flight (no spills at 4)
 
 // slot areas (64-bit words), see kSolverSlotWords
 constexpr long long kSlotA = 0;                                  // [2][ctas][6]  gather (3 values)
 constexpr long long kSlotB = kSlotA + 2LL * kMaxSolverCtas * 6;  // [2][ctas][4]  group (2 values)
 constexpr long long kSlotC = kSlotB + 2LL * kMaxSolverCtas * 4;  // [2][4]        broadcast (2)
-constexpr long long kSlotL = kSlotC + 2LL * 4;                     // [2][4]        group leader sum
 
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
@@ -142,30 +137,19 @@ __device__ __forceinline__ void slot_poll_sum(const unsigned long long* slots, i
 }
 
 // ------------------------------------------------------------ grid reductions
-// Grid barrier: one acq_rel arrival atomic per CTA on a counter, the last
-// arriver resets it and releases a generation word that the others poll with
-// a short sleep between polls.  Polling a separate word with backoff keeps the
-// pollers off the counter's L2 slice: cg::this_grid().sync() spins every CTA
-// on the arrival word itself, which under load delayed the release by ~10 us
-// (tools/solver_scaling.py per-CTA timeline).
-__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
-  unsigned old;
-  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
-  return old;
-}
+// Grid barrier on a monotonic arrival counter: every CTA adds 1 (release)
+// and polls, with a short sleep, until all arrivals of this barrier have
+// landed (acquire).  No reset and no release hop by a last arriver; the
+// counter's value at the barrier's start persists across solves (chan[3]).
+// cg::this_grid().sync() spins every CTA on the arrival word itself, which
+// under load delayed the release by ~10 us (tools/solver_scaling.py).
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-#ifndef MPMRB_BAR_MONO
-#define MPMRB_BAR_MONO 1
-#endif
 __device__ __forceinline__ void red_release_add_u32(unsigned* p, unsigned v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 struct Sync {
@@ -173,8 +157,8 @@ struct Sync {
   int nctas;
   unsigned long long* prof;  // CTA 0 / thread 0 only: [10] time inside grid syncs
   unsigned long long* cta_in_sync;  // thread 0 of each CTA (profiling only)
-  unsigned* bar;     // [0] arrival count, [32] generation (separate 128 B lines)
-  unsigned* gen;     // this CTA's view of the generation (thread 0)
+  unsigned* bar;     // [0] monotonic arrival count
+  unsigned* gen;     // the count at this barrier's start (thread 0)
   __device__ __forceinline__ void operator()() const {
     if (nctas == 1) {
       __syncthreads();
@@ -183,25 +167,10 @@ struct Sync {
     unsigned long long t0 = (prof || cta_in_sync) ? gtime() : 0ull;
     __syncthreads();
     if (threadIdx.x == 0) {
-#if MPMRB_BAR_MONO
-      // monotonic arrival counter: *gen holds its value at this barrier's
-      // start; every CTA adds 1 (release) and waits until all nctas arrivals
-      // have landed (acquire).  No reset and no release hop by a last arriver.
-      const unsigned target = *gen + (unsigned)nctas;
+const unsigned target = *gen + (unsigned)nctas;
       red_release_add_u32(bar, 1u);
       while ((int)(ld_acquire_u32(bar) - target) < 0) __nanosleep(32);
       *gen = target;
-#else
-      const unsigned target = *gen + 1u;
-      const unsigned old = atom_add_acq_rel(bar, 1u);
-      if (old == (unsigned)nctas - 1u) {
-        atomicExch(bar, 0u);
-        st_release_u32(bar + 32, target);
-      } else {
-        while (ld_acquire_u32(bar + 32) != target) __nanosleep(64);
-      }
-      *gen = target;
-#endif
     }
     __syncthreads();
     if (prof) atomicAdd(prof + 10, gtime() - t0);
@@ -288,7 +257,7 @@ __device__ void reduce_all(const Sync& sync, int& parity, double (&v)[K], double
 // call, `rpar`), so no trailing barrier is needed before the next call.
 template <int K>
 __device__ void group_reduce(int G, unsigned long long* slots, unsigned& tag, double (&v)[K],
-                             double (&out)[K], double* sm, unsigned& rpar, int mode = 0) {
+                             double (&out)[K], double* sm, unsigned& rpar) {
   double* res = sm + 32 * kMaxRed + 4 * (rpar & 1u);
   ++rpar;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -303,20 +272,7 @@ __device__ void group_reduce(int G, unsigned long long* slots, unsigned& tag, do
       unsigned long long* base = slots + kSlotB + (long long)(tag & 1u) * kMaxSolverCtas * 4;
       if (lane == 0) slot_publish<K>(base + (long long)blockIdx.x * 2 * K, bs, tag);
       double r[K];
-      if (mode == 2) {
-        // leader tree: CTA 0 sums the G slots and republishes the total
-        unsigned long long* lead = slots + kSlotL + (long long)(tag & 1u) * 4;
-        if (blockIdx.x == 0) {
-          slot_poll_sum<K, 2>(base, G, tag, r);
-          if (lane == 0) slot_publish<K>(lead, r, tag);
-        } else {
-          slot_poll_sum<K, 1>(lead, 1, tag, r);
-        }
-      } else if (mode == 1) {
-        slot_poll_sum<K, 2, 32>(base, G, tag, r);
-      } else {
-        slot_poll_sum<K, 2>(base, G, tag, r);
-      }
+      slot_poll_sum<K, 2>(base, G, tag, r);
       if (lane == 0)
 #pragma unroll
         for (int k = 0; k < K; ++k) res[k] = r[k];
@@ -326,34 +282,6 @@ __device__ void group_reduce(int G, unsigned long long* slots, unsigned& tag, do
   __syncthreads();
 #pragma unroll
   for (int k = 0; k < K; ++k) out[k] = res[k];
-}
-
-// All-reduce of K values over the line-search group when it is cluster 0:
-// every CTA writes its block sum into slot [parity][rank] of EVERY CTA's
-// shared memory (st.shared::cluster), one hardware cluster barrier, then each
-// CTA sums the CL slots locally in rank order (identical in every CTA).
-constexpr int kMaxCluster = 16;
-template <int K>
-__device__ void cluster_reduce(int CL, double (*s_cl)[kMaxCluster][2], int& cpar,
-                               double (&v)[K], double (&out)[K], double* sm) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  double bs[K];
-  block_reduce<K>(v, sm, bs);
-  cg::cluster_group cl = cg::this_cluster();
-  const int me = (int)cl.block_rank();
-  if (wid == 0 && lane < CL) {
-    double* dst = cl.map_shared_rank(&s_cl[cpar][me][0], lane);
-#pragma unroll
-    for (int k = 0; k < K; ++k) dst[k] = bs[k];
-  }
-  cl.sync();
-#pragma unroll
-  for (int k = 0; k < K; ++k) {
-    double x = 0.0;
-    for (int r = 0; r < CL; ++r) x += s_cl[cpar][r][k];
-    out[k] = x;
-  }
-  cpar ^= 1;
 }
 
 __device__ __forceinline__ void load_frame(const double* fr, long long c, double* R) {
@@ -480,15 +408,8 @@ __device__ __forceinline__ void ls_terms(const ContactModel& cm, double inv_eps,
 
 // The same with the per-line-search constants of a contact precomputed
 // (LsRec): gap0 = vhat - vc_n, dvn, K dvn^2, |dvt|^2, mu gamma_lag.
-#ifndef MPMRB_LSREC7
-#define MPMRB_LSREC7 0
-#endif
 struct LsRec {
-#if MPMRB_LSREC7
-  double t0, t1, d0, d1, gap0, dvn, mug;  // K dvn^2, |dvt|^2 recomputed per evaluation
-#else
   double t0, t1, d0, d1, gap0, dvn, kdvn2, dd, mug;
-#endif
 };
 __device__ __forceinline__ LsRec ls_rec(const ContactModel& cm, const double* vc,
                                         const double* dvc, double vhat, double mug) {
@@ -499,22 +420,15 @@ __device__ __forceinline__ LsRec ls_rec(const ContactModel& cm, const double* vc
   r.d1 = dvc[1];
   r.gap0 = vhat - vc[2];
   r.dvn = dvc[2];
-#if !MPMRB_LSREC7
   r.kdvn2 = cm.K * (dvc[2] * dvc[2]);
   r.dd = dvc[0] * dvc[0] + dvc[1] * dvc[1];
-#endif
   r.mug = mug;
   return r;
 }
 __device__ __forceinline__ void ls_terms_rec(const ContactModel& cm, double eps2, double inv_eps,
                                              const LsRec& c, double alpha, double& d1,
                                              double& d2) {
-#if MPMRB_LSREC7
-  const double kdvn2 = cm.K * (c.dvn * c.dvn);
-  const double cdd = c.d0 * c.d0 + c.d1 * c.d1;
-#else
   const double kdvn2 = c.kdvn2, cdd = c.dd;
-#endif
   const double gap = c.gap0 - alpha * c.dvn;
   if (gap > 0.0) d1 -= (cm.K * gap) * c.dvn;
   if (gap >= 0.0) d2 += kdvn2;
@@ -593,96 +507,65 @@ __device__ __forceinline__ void node_finish(const SolverArgs& a, long long i, co
   }
 }
 
-// Phase U (and the init) on one warp chunk of contacts [c0, c0 + 32): new
-// contact velocity, contact gradient / Hessian / energy, then the per
-// (group, slot) sums (groups never cross a chunk).  Warp-synchronous; s_gw is
-// this warp's 32 x 9 scratch.
-// The groups of a chunk: first group, group count, and (one per lane) the
-// group bounds; constant over a solve, so resident warps load them once.
-struct ChunkGroups {
-  int g0, ngc, my_gs, gs_32;
-};
-__device__ __forceinline__ ChunkGroups chunk_groups(const SolverArgs& a, long long c0, int nc) {
-  const int lane = threadIdx.x & 31;
-  const long long c_last = (c0 + kChunk < nc ? c0 + kChunk : nc) - 1;
-  ChunkGroups cg;
-  cg.g0 = a.su.grp_of[c0];
-  cg.ngc = a.su.grp_of[c_last] - cg.g0 + 1;  // <= 32 groups in a chunk
-  cg.my_gs = (lane <= cg.ngc) ? a.su.grp_start[cg.g0 + lane] : 0;
-  cg.gs_32 = (cg.ngc == 32) ? a.su.grp_start[cg.g0 + 32] : 0;
-  return cg;
-}
-
+// Phase U (and the init) on one warp chunk of contacts [c0, c0 + 32), one
+// contact per lane: new contact velocity, then the contact's record for the
+// node gathers of the next N phase -- world gradient R^T g_c (3) and Hessian
+// block R^T G_c R (6) -- and its energy.  The stencil weight is applied by the
+// gathering node (w and w^2 per (contact, slot)), so a contact's record is
+// written once instead of once per stencil slot.
 __device__ __forceinline__ void contact_update_chunk(const SolverArgs& a, const ContactModel& cm,
                                                      long long c0, int nc, bool init,
-                                                     double alpha, double* s_gw,
-                                                     const double* s_w, double& e_acc,
-                                                     const ChunkGroups& cg) {
+                                                     double alpha, const double* s_w,
+                                                     double& e_acc) {
   const int lane = threadIdx.x & 31;
   const long long c = c0 + lane;
-  if (c < nc) {
-    double R[9], vc[3], gw[3], rgr[6], vhat, mug;
-    load_frame(a.frames, c, R);
-    if (init) {
-      gather_contact_sw(a, c, a.v0, R, s_w, lane, vc);
+  if (c >= nc) return;
+  double R[9], vc[3], gw[3], rgr[6], vhat, mug;
+  load_frame(a.frames, c, R);
+  if (init) {
+    gather_contact_sw(a, c, a.v0, R, s_w, lane, vc);
 #pragma unroll
-      for (int d = 0; d < 3; ++d) vc[d] += a.bias[3 * c + d];
-      vhat = -a.phi[c] / cm.den;
-      mug = a.mu[c] * a.gamma_lag[c];
-      a.cvhat[c] = vhat;
-      a.cmug[c] = mug;
-    } else {
+    for (int d = 0; d < 3; ++d) vc[d] += a.bias[3 * c + d];
+    vhat = -a.phi[c] / cm.den;
+    mug = a.mu[c] * a.gamma_lag[c];
+    a.cvhat[c] = vhat;
+    a.cmug[c] = mug;
+  } else {
 #pragma unroll
-      for (int d = 0; d < 3; ++d) vc[d] = a.vc[3 * c + d] + alpha * a.dvc[3 * c + d];
-      vhat = a.cvhat[c];
-      mug = a.cmug[c];
-    }
-#pragma unroll
-    for (int d = 0; d < 3; ++d) a.vc[3 * c + d] = vc[d];
-    e_acc += contact_terms(cm, vc, vhat, mug, R, gw, rgr);
-    double* sg = s_gw + 9 * lane;
-#pragma unroll
-    for (int d = 0; d < 3; ++d) sg[d] = gw[d];
-#pragma unroll
-    for (int q = 0; q < 6; ++q) sg[3 + q] = rgr[q];
+    for (int d = 0; d < 3; ++d) vc[d] = a.vc[3 * c + d] + alpha * a.dvc[3 * c + d];
+    vhat = a.cvhat[c];
+    mug = a.cmug[c];
   }
-  __syncwarp();
-  const int g0 = cg.g0, ngc = cg.ngc, my_gs = cg.my_gs, gs_32 = cg.gs_32;
-  const int pairs = ngc * 27;
-  for (int p0 = 0; p0 < pairs; p0 += 32) {
-    const int p = p0 + lane;
-    const int gl = p < pairs ? p / 27 : 0, k = p - gl * 27;
-    const int g = g0 + gl;
-    const int cs = __shfl_sync(0xffffffffu, my_gs, gl);
-    const int ce_sh = __shfl_sync(0xffffffffu, my_gs, (gl + 1) & 31);
-    const int ce = (gl + 1 < 32) ? ce_sh : gs_32;
-    if (p >= pairs) continue;
-    double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-    for (int cc = cs; cc < ce; ++cc) {
-      const double w = s_w[k * kSwStride + (cc - c0)];
-      const double w2 = w * w;
-      const double* sg = s_gw + 9 * (cc - c0);
 #pragma unroll
-      for (int d = 0; d < 3; ++d) acc[d] += w * sg[d];
-#pragma unroll
-      for (int q = 3; q < 9; ++q) acc[q] += w2 * sg[q];
-    }
-    double2* out = reinterpret_cast<double2*>(a.cellsum + ((long long)g * 27 + k) * kCellSumStride);
-    out[0] = make_double2(acc[0], acc[1]);
-    out[1] = make_double2(acc[2], acc[3]);
-    out[2] = make_double2(acc[4], acc[5]);
-    out[3] = make_double2(acc[6], acc[7]);
-    out[4] = make_double2(acc[8], 0.0);
-  }
-  __syncwarp();
+  for (int d = 0; d < 3; ++d) a.vc[3 * c + d] = vc[d];
+  e_acc += contact_terms(cm, vc, vhat, mug, R, gw, rgr);
+  double2* out = reinterpret_cast<double2*>(a.cellsum + c * kCellSumStride);
+  out[0] = make_double2(gw[0], gw[1]);
+  out[1] = make_double2(gw[2], rgr[0]);
+  out[2] = make_double2(rgr[1], rgr[2]);
+  out[3] = make_double2(rgr[3], rgr[4]);
+  out[4] = make_double2(rgr[5], 0.0);
+}
+
+// Adds one contact's record, weighted by its stencil weight w for this node,
+// to a node's sums: J^T g (w R^T g) and the Hessian block (w^2 R^T G R).
+__device__ __forceinline__ void add_contact_record(double w, const double2 (&q)[5], double* acc) {
+  const double w2 = w * w;
+  acc[0] += w * q[0].x;
+  acc[1] += w * q[0].y;
+  acc[2] += w * q[1].x;
+  acc[3] += w2 * q[1].y;
+  acc[4] += w2 * q[2].x;
+  acc[5] += w2 * q[2].y;
+  acc[6] += w2 * q[3].x;
+  acc[7] += w2 * q[3].y;
+  acc[8] += w2 * q[4].x;
 }
 
 __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
   __shared__ double sm[32 * kMaxRed + kMaxRed];
-  __shared__ double s_gw[kWarps * kChunk * 9];
   extern __shared__ double s_dyn[];  // [kWarps][27][32] staged stencil weights
   __shared__ double s_bc[4];
-  __shared__ double s_cl[2][kMaxCluster][2];
   __shared__ int s_flag;
   const int nd = *a.nd_dev;
   const int nc = *a.nc_dev;
@@ -706,11 +589,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
   if (nctas == 1 && blockIdx.x != 0) return;
   // line-search group: ~3 contacts per thread, at least one CTA
   int G = 1;
-  const int CL = (nctas > 1) ? (int)cg::this_cluster().num_blocks() : 1;
-  int cpar = 0;
-  if (nctas > 1 && CL > 1) {
-    G = CL;  // the line-search group is cluster 0 (DSMEM reductions)
-  } else if (nctas > 1) {
+  if (nctas > 1) {
     // kLS contacts per thread, all in registers (4: measured optimum between
     // per-evaluation compute
     // and the all-to-all reduction latency, which grows with the group)
@@ -732,7 +611,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
             (a.prof && threadIdx.x == 0) ? &in_sync_acc : nullptr, a.bar, &bar_gen};
   int parity = 0;
   unsigned grp_par = 0;  // group_reduce result buffer parity
-  const long long tid = (long long)blockIdx.x * kThreads + threadIdx.x;
   const long long nthr = (long long)nctas * kThreads;
   const ContactModel cm{a.K, a.den, a.eps_v};
   const double inv_eps = 1.0 / a.eps_v;
@@ -763,12 +641,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
   const long long vt = ((long long)wid * nctas + blockIdx.x) * 32 + lane;
   const long long chunk0 = ((long long)wid * nctas + blockIdx.x) * kChunk;
   const long long chunk_step = (long long)nctas * kThreads;
-  double* s_gw_w = s_gw + wid * (kChunk * 9);
   double* s_w_w = s_dyn + wid * (27 * kSwStride);
   // every warp owns at most one chunk: its weights stay staged for the solve
   const bool resident = (long long)nc <= (long long)nctas * kThreads;
 
-  ChunkGroups my_cg{0, 0, 0, 0};  // resident warps: the groups of their one chunk
   // ---- init: contact nodes v = v0; free-node sums; contacts
   for (long long t = vt; t < n_cn; t += nthr) {
     const long long i = a.su.cn[t];
@@ -791,12 +667,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
         r3[2] += m * vs * e0;
       }
     }
-    for (long long c0 = chunk0; c0 < nc; c0 += chunk_step)
-    {
-      const ChunkGroups cgr = chunk_groups(a, c0, nc);
-      if (resident) my_cg = cgr;
+    for (long long c0 = chunk0; c0 < nc; c0 += chunk_step) {
       stage_weights(a, c0, nc, s_w_w);
-      contact_update_chunk(a, cm, c0, nc, true, 0.0, s_gw_w, s_w_w, e_acc, cgr);
+      contact_update_chunk(a, cm, c0, nc, true, 0.0, s_w_w, e_acc);
     }
     double s3[3];
     reduce_all<3>(sync, parity, r3, s3, sm);  // also publishes vc / cellsum grid-wide
@@ -810,8 +683,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
   // while the contact nodes fit in one pass of the grid, else 2 (twice the
   // nodes in flight per warp; tools/gpu_ab.sh: 16.4 -> 10.7 us of N work per
   // iteration with 31k contact nodes, no change with 9k)
-  const int NL = a.node_lanes > 0 ? a.node_lanes
-                                  : (4LL * n_cn > (long long)nctas * kThreads ? 2 : 4);
+  const int NL = 4LL * n_cn > (long long)nctas * kThreads ? 2 : 4;
   int iterations = 0, ls_evals_total = 0, status = 0;
   bool converged = false;
   double alpha_prev = 0.0;  // pending v += alpha dv, applied by each node's owner in N
@@ -850,33 +722,39 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
           }
         }
         double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-        // up to 4 entries per lane per pass: all keys, then all records, in flight
-        for (int eb = rec.y + gl; eb < rec.z; eb += 4 * NL) {
-          int key[4];
+        // up to kEPL entries per lane per pass: all entries, then the records and
+        // weights of their first contacts, in flight; an entry (contact run
+        // c0 .. c0+len of one stencil, slot k) adds its contacts in order
+        for (int eb = rec.y + gl; eb < rec.z; eb += kEPL * NL) {
+          int2 e[kEPL];
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
-            key[j] = (eb + NL * j < rec.z) ? __ldg(&a.su.ent[eb + NL * j]) : -1;
-          double2 q[4][5];
+          for (int j = 0; j < kEPL; ++j)
+            e[j] = (eb + NL * j < rec.z) ? __ldg(&a.su.ent[eb + NL * j]) : make_int2(0, 0);
+          double2 q[kEPL][5];
+          double w[kEPL];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const double2* src = reinterpret_cast<const double2*>(
-                a.cellsum + ((long long)((key[j] < 0 ? 0 : key[j]) >> 5) * 27 + (key[j] & 31)) *
-                                kCellSumStride);
+          for (int j = 0; j < kEPL; ++j) {
+            const long long c = e[j].x >> 5;
+            w[j] = __ldg(&a.cw[(long long)(e[j].x & 31) * a.nc_cap + c]);
+            const double2* src = reinterpret_cast<const double2*>(a.cellsum + c * kCellSumStride);
 #pragma unroll
             for (int r = 0; r < 5; ++r) q[j][r] = src[r];
           }
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            if (key[j] < 0) continue;
-            acc[0] += q[j][0].x;
-            acc[1] += q[j][0].y;
-            acc[2] += q[j][1].x;
-            acc[3] += q[j][1].y;
-            acc[4] += q[j][2].x;
-            acc[5] += q[j][2].y;
-            acc[6] += q[j][3].x;
-            acc[7] += q[j][3].y;
-            acc[8] += q[j][4].x;
+          for (int j = 0; j < kEPL; ++j)
+            if (e[j].y > 0) add_contact_record(w[j], q[j], acc);
+#pragma unroll
+          for (int j = 0; j < kEPL; ++j) {
+#pragma unroll 1
+            for (int t = 1; t < e[j].y; ++t) {
+              const long long c = (e[j].x >> 5) + t;
+              const double wt = __ldg(&a.cw[(long long)(e[j].x & 31) * a.nc_cap + c]);
+              const double2* src = reinterpret_cast<const double2*>(a.cellsum + c * kCellSumStride);
+              double2 qt[5];
+#pragma unroll
+              for (int r = 0; r < 5; ++r) qt[r] = src[r];
+              add_contact_record(wt, qt, acc);
+            }
           }
         }
 #pragma unroll
@@ -969,7 +847,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
       }
       if (in_group && threadIdx.x < 32) {
         double r[3];
-        slot_poll_sum<3, (kMaxSolverCtas + 31) / 32, MPMRB_HAND_SLEEP>(base, nctas, tagA, r);
+        slot_poll_sum<3, (kMaxSolverCtas + 31) / 32>(base, nctas, tagA, r);
         fence_acq_rel_gpu();  // acquire: the producers' dvc writes are visible below
         if (threadIdx.x == 0) {
           s_bc[0] = r[0];
@@ -1035,8 +913,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
                        rr[1]);
             }
             unsigned long long tls1 = prof ? gtime() : 0ull;
-            if (CL > 1) cluster_reduce<2>(CL, s_cl, cpar, rr, ss, sm);
-            else group_reduce<2>(G, a.slots, tagB, rr, ss, sm, grp_par, a.ls_mode);
+            group_reduce<2>(G, a.slots, tagB, rr, ss, sm, grp_par);
             if (prof) {
               unsigned long long tls2 = gtime();
               pt[12] += tls1 - tls0;
@@ -1092,15 +969,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
     e_acc = 0.0;
     cta_start();
     for (long long c0 = chunk0; c0 < nc; c0 += chunk_step)
-    {
-      if (resident) {
-        contact_update_chunk(a, cm, c0, nc, false, alpha_final, s_gw_w, s_w_w, e_acc, my_cg);
-      } else {
-        const ChunkGroups cgr = chunk_groups(a, c0, nc);  // loads overlap the staging
-        stage_weights(a, c0, nc, s_w_w);
-        contact_update_chunk(a, cm, c0, nc, false, alpha_final, s_gw_w, s_w_w, e_acc, cgr);
-      }
-    }
+      contact_update_chunk(a, cm, c0, nc, false, alpha_final, s_w_w, e_acc);
     lap(8);
     cta_stop(2);
     sync();  // cellsum and vc visible grid-wide
@@ -1196,7 +1065,7 @@ __global__ void k_su_heads(const int* __restrict__ nc_dev, long long nc_cap,
   const long long nc = *nc_dev;
   for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < nc;
        c += (long long)gridDim.x * blockDim.x)
-    head[c] = (c % kChunk == 0 || !same_stencil(cnodes, nc_cap, c, c - 1)) ? 1 : 0;
+    head[c] = (c == 0 || !same_stencil(cnodes, nc_cap, c, c - 1)) ? 1 : 0;
 }
 
 __global__ void k_su_groups(const int* __restrict__ nc_dev, const int* __restrict__ head,
@@ -1235,26 +1104,29 @@ __global__ void k_su_fill(const int* __restrict__ counts, long long nc_cap,
     const int node = cnodes[k * nc_cap + grp_start[g]];
     if (node < 0) continue;
     const int pos = off[node] + atomicAdd(&fill[node], 1);
-    ent_tmp[pos] = (int)((g << 5) | k);
+    ent_tmp[pos] = (int)(((long long)grp_start[g] << 5) | k);
   }
 }
 
 // Place every entry at its sorted position inside its node's segment: the
 // rank is the number of smaller keys in the same segment (keys are unique).
+// The entry carries its group's contact run: (first contact << 5 | slot, run
+// length), so the N phase sums a node's contacts in ascending contact order.
 __global__ void k_su_rank(const int* __restrict__ nd_dev, long long nc_cap,
-                          const int* __restrict__ cnodes, const int* __restrict__ grp_start,
-                          const int* __restrict__ off, const int* __restrict__ ent_tmp,
-                          int* __restrict__ ent) {
+                          const int* __restrict__ cnodes, const int* __restrict__ grp_of,
+                          const int* __restrict__ grp_start, const int* __restrict__ off,
+                          const int* __restrict__ ent_tmp, int2* __restrict__ ent) {
   const long long total = off[*nd_dev];
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
     const int key = ent_tmp[e];
-    const long long g = key >> 5, k = key & 31;
-    const int node = cnodes[k * nc_cap + grp_start[g]];
+    const long long c0 = key >> 5, k = key & 31;
+    const int node = cnodes[k * nc_cap + c0];
     const int b = off[node], en = off[node + 1];
     int rank = 0;
     for (int p = b; p < en; ++p) rank += (__ldg(&ent_tmp[p]) < key) ? 1 : 0;
-    ent[b + rank] = key;
+    const int g = grp_of[c0];
+    ent[b + rank] = make_int2(key, grp_start[g + 1] - (int)c0);
   }
 }
 
@@ -1295,6 +1167,9 @@ unsigned su_grid(long long cap) {
 int launch_solver_setup(Ctx& c, const int* nd_dev, const int* nc_dev, long long nd_cap,
                         long long nc_cap, const int* cnodes, const SolverSetup& su,
                         DevBuf& tiles) {
+  // adjacency entries pack (contact << 5 | slot) into an int32
+  if (nc_cap >= (1LL << 26))
+    return set_error(MPMRB_E_INVALID, "contact capacity %lld exceeds 2^26", nc_cap);
   MPMRB_CUDA_OK(cudaMemsetAsync(su.cnt, 0, sizeof(int) * (nd_cap + 1), c.stream));
   MPMRB_CUDA_OK(cudaMemsetAsync(su.fill, 0, sizeof(int) * (nd_cap + 1), c.stream));
   MPMRB_CUDA_OK(cudaMemsetAsync(su.flag, 0, sizeof(int) * (nd_cap + 1), c.stream));
@@ -1315,8 +1190,8 @@ int launch_solver_setup(Ctx& c, const int* nd_dev, const int* nc_dev, long long 
                                                                 su.grp_start, su.off, su.fill,
                                                                 su.ent_tmp);
   k_su_rank<<<su_grid(27 * ncc), kSetupThreads, 0, c.stream>>>(nd_dev, nc_cap, cnodes,
-                                                                su.grp_start, su.off, su.ent_tmp,
-                                                                su.ent);
+                                                                su.grp_of, su.grp_start, su.off,
+                                                                su.ent_tmp, su.ent);
   k_su_flag<<<su_grid(nd_cap + 1), kSetupThreads, 0, c.stream>>>(nd_dev, su.cnt, su.flag);
   c.launches += 3;
   rc = scan_exclusive_i32(c, su.flag, su.flag_off, nd_cap + 1, nullptr, su.counts + 1, tiles);
@@ -1329,64 +1204,20 @@ int launch_solver_setup(Ctx& c, const int* nd_dev, const int* nc_dev, long long 
 }
 
 int launch_qn_solve(Ctx& c, const SolverArgs& a, int grid_ctas) {
-  // Grid: one CTA per SM (launch bounds + 128 registers), cooperative,
-  // launched as clusters of CL CTAs (cluster 0 is the line-search group) when
-  // CL clusters fill the GPU; MPMRB_SOLVER_CLUSTER=0 disables clusters.
-  static int sms = -1, cl_size = 0, cl_grid = 0;
+  // Grid: one 256-thread CTA per SM (255 registers), cooperative so that all
+  // CTAs are co-resident for the in-kernel barriers.  Measured and rejected:
+  // clusters with DSMEM line-search reductions (1.2 vs 0.9 us per reduction
+  // on 12-16 CTAs, tools/reduce_bench.cu).
+  static int sms = -1;
   if (sms < 0) {
     int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    MPMRB_CUDA_OK(cudaGetDevice(&dev));
+    MPMRB_CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     if (sms > kMaxSolverCtas) sms = kMaxSolverCtas;
-    int want = 0;  // measured: slot reductions over a 12-16 CTA group beat 4-CTA clusters
-    const char* env = getenv("MPMRB_SOLVER_CLUSTER");
-    if (env) want = atoi(env);
-    if (want > kMaxCluster) want = kMaxCluster;
-    if (want > 1)
-      cudaFuncSetAttribute(k_qn_solve, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    for (int cs = want; cs > 1; cs /= 2) {
-      cudaLaunchConfig_t q = {};
-      q.blockDim = dim3(kThreads);
-      q.gridDim = dim3(cs);
-      cudaLaunchAttribute qa[1];
-      qa[0].id = cudaLaunchAttributeClusterDimension;
-      qa[0].val.clusterDim.x = cs;
-      qa[0].val.clusterDim.y = 1;
-      qa[0].val.clusterDim.z = 1;
-      q.attrs = qa;
-      q.numAttrs = 1;
-      int ncl = 0;
-      q.dynamicSmemBytes = sizeof(double) * kWarps * 27 * kSwStride;
-      cudaFuncSetAttribute(k_qn_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)q.dynamicSmemBytes);
-      cudaError_t qe = cudaOccupancyMaxActiveClusters(&ncl, k_qn_solve, &q);
-      if (getenv("MPMRB_SOLVER_VERBOSE"))
-        fprintf(stderr, "solver: cluster %d -> max active clusters %d (%s)\n", cs, ncl,
-                cudaGetErrorString(qe));
-      if (qe == cudaSuccess && ncl > 0) {
-        int g = ncl * cs;
-        if (g > sms) g = (sms / cs) * cs;
-        // keep clusters only if they still cover >= 85% of the SMs
-        if (g * 100 >= sms * 85) {
-          cl_size = cs;
-          cl_grid = g;
-          break;
-        }
-      }
-      cudaGetLastError();
-    }
   }
   int g = sms;
-  bool use_cluster = cl_size > 1;
-  if (use_cluster) g = cl_grid;
-  if (grid_ctas > 0 && grid_ctas < g) {
-    g = grid_ctas;
-    use_cluster = false;
-  }
-  if (a.force_ctas > 1) {
-    g = a.force_ctas < sms ? a.force_ctas : sms;
-    use_cluster = false;
-  }
+  if (grid_ctas > 0 && grid_ctas < g) g = grid_ctas;
+  if (a.force_ctas > 1) g = a.force_ctas < sms ? a.force_ctas : sms;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)g);
   cfg.blockDim = dim3(kThreads);
@@ -1398,15 +1229,11 @@ int launch_qn_solve(Ctx& c, const SolverArgs& a, int grid_ctas) {
   }
   cfg.dynamicSmemBytes = dyn;
   cfg.stream = c.stream;
-  cudaLaunchAttribute attr[2];
+  cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
-  attr[1].id = cudaLaunchAttributeClusterDimension;
-  attr[1].val.clusterDim.x = use_cluster ? cl_size : 1;
-  attr[1].val.clusterDim.y = 1;
-  attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = use_cluster ? 2 : 1;
+  cfg.numAttrs = 1;
   MPMRB_CUDA_OK(cudaLaunchKernelEx(&cfg, k_qn_solve, a));
   c.launches++;
   return MPMRB_OK;

@@ -10,7 +10,7 @@ constexpr int kMaxSolverCtas = 160;
 constexpr int kSolverProf = 16;  // phase timers (ns), see solver.cu
 // + per-CTA work time (ns) of the N, D and U phases: [16 + phase*kMaxSolverCtas + cta]
 constexpr int kSolverProfWords = 16 + 5 * 160;
-constexpr int kCellSumStride = 10;  // 9 channels (J^T g: 3, R^T G R: 6) padded to 80 B
+constexpr int kCellSumStride = 10;  // per-contact record: R^T g (3), R^T G R (6), padded to 80 B
 
 struct SolveOut {
   int converged;
@@ -26,11 +26,11 @@ struct SolveOut {
 // Per-solve structure built by launch_solver_setup from the contact stencils.
 //
 // Contact groups: maximal runs of consecutive contacts with identical stencil
-// node lists (the contacts of one grid cell share all 27 nodes), never
-// crossing a 512-contact chunk boundary.  The J^T scatters of the gradient and
-// of the block-diagonal Hessian are accumulated per (group, slot) by the
-// contact owners, and gathered per node through a node -> (group, slot) CSR
-// whose entries are sorted: a fixed summation order, no atomics.
+// node lists (the contacts of one grid cell share all 27 nodes).  Each contact
+// owner writes one record per iteration (R^T g, R^T G R); each contact node
+// gathers, through a node -> (group, slot) CSR whose entries are sorted, the
+// records of the group's contacts weighted by their slot weight: a fixed
+// summation order (ascending contact id per node), no atomics.
 struct SolverSetup {
   int* head;       // (nc_cap+1) scratch: contact starts a group
   int* head_off;   // (nc_cap+1) exclusive scan of head
@@ -40,7 +40,8 @@ struct SolverSetup {
   int* fill;       // (nd_cap+1) scratch
   int* off;        // (nd_cap+1) CSR offsets
   int* ent_tmp;    // (27 nc_cap) scratch: entries in atomic fill order
-  int* ent;        // (27 nc_cap) packed (group << 5) | slot, ascending within a node
+  int2* ent;       // (27 nc_cap) (first contact of the group << 5 | slot, group length),
+                   // ascending within a node
   int* flag;       // (nd_cap+1) scratch: node has entries
   int* flag_off;   // (nd_cap+1) exclusive scan of flag
   int* cn;         // (nd_cap) contact nodes (ascending)
@@ -74,8 +75,6 @@ struct SolverArgs {
   int skip_if_no_contacts;
   int force_ctas;  // 0 = automatic
   int force_ls_ctas;  // 0 = automatic
-  int ls_mode;        // line-search group reduction: 0 all-to-all, 1 + backoff, 2 leader
-  int node_lanes;     // lanes per contact node in phase N (2 or 4; 0 = automatic)
   // free nodes held outside this problem (slab decomposition, slab.py): their
   // sums S0 = sum m |v0 - v*|^2, Q0 = sum m |v*|^2, Q1 = sum m v*.(v0 - v*),
   // added to the problem's own; the final P = prod(1 - alpha) goes to p_out
@@ -88,7 +87,7 @@ struct SolverArgs {
   double* dvc;       // (nc,3)
   double* cvhat;     // (nc,) -phi/(dt+tau_d)
   double* cmug;      // (nc,) mu*gamma_lag
-  double* cellsum;   // (27 nc_cap, kCellSumStride) per (group, slot) sums
+  double* cellsum;   // (nc_cap, kCellSumStride) per-contact records
   double* partials;  // [2][8][kMaxSolverCtas] grid reductions
   unsigned long long* slots;  // self-validating reduction slots (see solver.cu)
   unsigned* chan;    // [4] channel tags carried across solves ([3]: barrier generation)

@@ -87,12 +87,17 @@ def full(path: Path):
         grid = r[col["Grid Size"]]
         lines.append(f"{k:14s} {grid:>10s} {d:9.2f} {b / 1e6:9.2f} {b / d / 1e3 if d else 0:10.1f} "
                      f"{l2:8.2f} {occ:7.2f} {regs:5.0f}")
-        fl = (2.0 * get(r, "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum", 0.0)
-              + get(r, "smsp__sass_thread_inst_executed_op_dmul_pred_on.sum", 0.0)
-              + get(r, "smsp__sass_thread_inst_executed_op_dadd_pred_on.sum", 0.0))
-        traffic[k] = dict(dram_bytes=b, fp64_flop=fl or None, cold_duration_us=d,
-                          l2_hit_pct=l2, occupancy_pct=occ, registers=regs)
-        lines[-1] += f"  fp64 GFLOP {fl / 1e9:8.3f}"
+        # FP64 work: thread instructions per elapsed cycle (summed over SMSPs)
+        # x elapsed cycles; flops count a DFMA as 2.  The pipe fraction is the
+        # FP64 compute roofline (DFMA, DMUL and DADD each take an issue slot).
+        cyc = get(r, "sm__cycles_elapsed.avg", 0.0) or get(r, "gpc__cycles_elapsed.max", 0.0)
+        rate = {op: get(r, f"smsp__sass_thread_inst_executed_op_{op}_pred_on.sum.per_cycle_elapsed", 0.0)
+                for op in ("dfma", "dmul", "dadd")}
+        fl = (2.0 * rate["dfma"] + rate["dmul"] + rate["dadd"]) * cyc
+        pipe = get(r, "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_elapsed", None)
+        traffic[k] = dict(dram_bytes=b, fp64_flop=fl or None, fp64_pipe_pct_of_peak=pipe,
+                          cold_duration_us=d, l2_hit_pct=l2, occupancy_pct=occ, registers=regs)
+        lines[-1] += f"  fp64 GFLOP {fl / 1e9:8.3f}  fp64 pipe {pipe or 0:5.1f}% of peak"
     return "\n".join(lines) + "\n", traffic
 
 
