@@ -508,8 +508,8 @@ static int qn_solve_impl(mpmrb_ctx* c, const mpmrb_problem* pr, const mpmrb_solv
   rc |= c->scratch[SS_SOLVER4].grow(8 * 8 * ncc);            // vc, dvc, vhat, mug
   rc |= c->scratch[SS_SOLVER5].grow(8 * (2 * 8 * kMaxSolverCtas + 8));  // grid partials
   rc |= c->scratch[SS_SOLVER6].grow(4096);                   // sizes, SolveOut
-  rc |= c->scratch[SS_SOLVER7].grow(4 * 12 * (ndd + 2) + 64);  // node adjacency ints
-  rc |= c->scratch[SS_SOLVER8].grow(3 * 4 * 27 * ncc);       // adjacency entries (int2) + tmp
+  rc |= c->scratch[SS_SOLVER7].grow(4 * 14 * (ndd + 2) + 64);  // node adjacency ints
+  rc |= c->scratch[SS_SOLVER8].grow(2 * 4 * 27 * ncc);       // adjacency entries + tmp
   rc |= c->scratch[SS_PROBLEM].grow(4 * 4 * (ncc + 2));      // contact groups
   rc |= c->scratch[SS_HOSTINFO].grow(kSolverSyncBytes);  // reduction slots, tags, barrier
   if (rc) return MPMRB_E_CUDA;
@@ -549,8 +549,10 @@ static int qn_solve_impl(mpmrb_ctx* c, const mpmrb_problem* pr, const mpmrb_solv
     su.head_off = ci + (ncc + 2);
     su.grp_of = ci + 2 * (ncc + 2);
     su.grp_start = ci + 3 * (ncc + 2);
-    su.ent = c->scratch[SS_SOLVER8].as<int2>();
-    su.ent_tmp = reinterpret_cast<int*>(su.ent + 27 * ncc);
+    su.cnt_exp = ni + 12 * (ndd + 2);
+    su.off_exp = ni + 13 * (ndd + 2);
+    su.ent = c->scratch[SS_SOLVER8].as<int>();
+    su.ent_tmp = su.ent + 27 * ncc;
   }
   rc = launch_solver_setup(*c, sizes, sizes + 1, nd, nc, c->scratch[SS_SOLVER0].as<int>(), su,
                            c->scratch[SS_TILE]);

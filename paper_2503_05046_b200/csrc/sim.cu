@@ -317,8 +317,8 @@ int Sim::reserve(long long n, long long nb_needed) {
   rc |= b_svc.grow(8 * 5 * nc_cap);  // vc (3), vhat, mu*gamma_lag
   rc |= b_sdvc.grow(8 * 3 * nc_cap);
   rc |= b_su_c.grow(4 * 4 * (nc_cap + 2));  // head, head_off, grp_of, grp_start
-  rc |= b_su_n.grow(4 * 12 * (N + 2) + 64);  // cnt, fill, off, flag, flag_off, cn, fn, counts, cn_rec
-  rc |= b_su_ent.grow(3 * 4 * 27 * nc_cap);  // entries (int2) + tmp
+  rc |= b_su_n.grow(4 * 14 * (N + 2) + 64);  // cnt, fill, off, flag, flag_off, cn, fn, counts, cn_rec (4), cnt_exp, off_exp
+  rc |= b_su_ent.grow(2 * 4 * 27 * nc_cap);  // entries + tmp
   rc |= b_cellsum.grow(8 * kCellSumStride * nc_cap);  // per-contact records
   rc |= b_gamma.grow(8 * 3 * nc_cap);
   rc |= b_gworld.grow(8 * 3 * nc_cap);
@@ -409,8 +409,10 @@ int Sim::capture_or_launch() {
     su.fn = ni + 6 * (N + 2);
     su.counts = ni + 7 * (N + 2);
     su.cn_rec = reinterpret_cast<int4*>(ni + 8 * (N + 2));
-    su.ent = b_su_ent.as<int2>();
-    su.ent_tmp = reinterpret_cast<int*>(su.ent + 27 * nc_cap);
+    su.cnt_exp = ni + 12 * (N + 2);
+    su.off_exp = ni + 13 * (N + 2);
+    su.ent = b_su_ent.as<int>();
+    su.ent_tmp = su.ent + 27 * nc_cap;
   }
   rc = launch_solver_setup(c, counters + 1, counters + 2, N, nc_cap, b_cnodes.as<int>(), su,
                            b_tiles);

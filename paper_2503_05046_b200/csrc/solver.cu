@@ -722,40 +722,27 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
           }
         }
         double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-        // up to kEPL entries per lane per pass: all entries, then the records and
-        // weights of their first contacts, in flight; an entry (contact run
-        // c0 .. c0+len of one stencil, slot k) adds its contacts in order
+        // up to kEPL (contact, slot) entries per lane per pass: all entries,
+        // then all records and weights, in flight
         for (int eb = rec.y + gl; eb < rec.z; eb += kEPL * NL) {
-          int2 e[kEPL];
+          int key[kEPL];
 #pragma unroll
           for (int j = 0; j < kEPL; ++j)
-            e[j] = (eb + NL * j < rec.z) ? __ldg(&a.su.ent[eb + NL * j]) : make_int2(0, 0);
+            key[j] = (eb + NL * j < rec.z) ? __ldg(&a.su.ent[eb + NL * j]) : -1;
           double2 q[kEPL][5];
           double w[kEPL];
 #pragma unroll
           for (int j = 0; j < kEPL; ++j) {
-            const long long c = e[j].x >> 5;
-            w[j] = __ldg(&a.cw[(long long)(e[j].x & 31) * a.nc_cap + c]);
+            const int kk = key[j] < 0 ? 0 : key[j];
+            const long long c = kk >> 5;
+            w[j] = __ldg(&a.cw[(long long)(kk & 31) * a.nc_cap + c]);
             const double2* src = reinterpret_cast<const double2*>(a.cellsum + c * kCellSumStride);
 #pragma unroll
             for (int r = 0; r < 5; ++r) q[j][r] = src[r];
           }
 #pragma unroll
           for (int j = 0; j < kEPL; ++j)
-            if (e[j].y > 0) add_contact_record(w[j], q[j], acc);
-#pragma unroll
-          for (int j = 0; j < kEPL; ++j) {
-#pragma unroll 1
-            for (int t = 1; t < e[j].y; ++t) {
-              const long long c = (e[j].x >> 5) + t;
-              const double wt = __ldg(&a.cw[(long long)(e[j].x & 31) * a.nc_cap + c]);
-              const double2* src = reinterpret_cast<const double2*>(a.cellsum + c * kCellSumStride);
-              double2 qt[5];
-#pragma unroll
-              for (int r = 0; r < 5; ++r) qt[r] = src[r];
-              add_contact_record(wt, qt, acc);
-            }
-          }
+            if (key[j] >= 0) add_contact_record(w[j], q[j], acc);
         }
 #pragma unroll
         for (int q = 0; q < 9; ++q)
@@ -1081,15 +1068,20 @@ __global__ void k_su_groups(const int* __restrict__ nc_dev, const int* __restric
   }
 }
 
+// Per node: (run, slot) entries and the contacts they expand to.
 __global__ void k_su_count(const int* __restrict__ counts, long long nc_cap,
                            const int* __restrict__ cnodes, const int* __restrict__ grp_start,
-                           int* __restrict__ cnt) {
+                           int* __restrict__ cnt, int* __restrict__ cnt_exp) {
   const long long np = (long long)counts[0] * 27;
   for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < np;
        p += (long long)gridDim.x * blockDim.x) {
     const long long g = p / 27, k = p - g * 27;
-    const int node = cnodes[k * nc_cap + grp_start[g]];
-    if (node >= 0) atomicAdd(&cnt[node], 1);
+    const int c0 = grp_start[g];
+    const int node = cnodes[k * nc_cap + c0];
+    if (node >= 0) {
+      atomicAdd(&cnt[node], 1);
+      atomicAdd(&cnt_exp[node], grp_start[g + 1] - c0);
+    }
   }
 }
 
@@ -1108,25 +1100,33 @@ __global__ void k_su_fill(const int* __restrict__ counts, long long nc_cap,
   }
 }
 
-// Place every entry at its sorted position inside its node's segment: the
-// rank is the number of smaller keys in the same segment (keys are unique).
-// The entry carries its group's contact run: (first contact << 5 | slot, run
-// length), so the N phase sums a node's contacts in ascending contact order.
+// Expand every (run, slot) entry into its contacts at their sorted position
+// in the node's segment: the position is the number of contacts of the
+// node's runs with a smaller key (keys are unique, runs are disjoint), so
+// each node lists (contact << 5 | slot) in ascending contact order.
 __global__ void k_su_rank(const int* __restrict__ nd_dev, long long nc_cap,
                           const int* __restrict__ cnodes, const int* __restrict__ grp_of,
                           const int* __restrict__ grp_start, const int* __restrict__ off,
-                          const int* __restrict__ ent_tmp, int2* __restrict__ ent) {
+                          const int* __restrict__ off_exp, const int* __restrict__ ent_tmp,
+                          int* __restrict__ ent) {
   const long long total = off[*nd_dev];
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
     const int key = ent_tmp[e];
-    const long long c0 = key >> 5, k = key & 31;
-    const int node = cnodes[k * nc_cap + c0];
+    const int c0 = key >> 5, k = key & 31;
+    const int node = cnodes[(long long)k * nc_cap + c0];
     const int b = off[node], en = off[node + 1];
-    int rank = 0;
-    for (int p = b; p < en; ++p) rank += (__ldg(&ent_tmp[p]) < key) ? 1 : 0;
-    const int g = grp_of[c0];
-    ent[b + rank] = make_int2(key, grp_start[g + 1] - (int)c0);
+    int before = 0;
+    for (int p = b; p < en; ++p) {
+      const int o = __ldg(&ent_tmp[p]);
+      if (o < key) {
+        const int oc = o >> 5;
+        before += __ldg(&grp_start[__ldg(&grp_of[oc]) + 1]) - oc;
+      }
+    }
+    const int len = grp_start[grp_of[c0] + 1] - c0;
+    int* dst = ent + off_exp[node] + before;
+    for (int t = 0; t < len; ++t) dst[t] = ((c0 + t) << 5) | k;
   }
 }
 
@@ -1139,7 +1139,7 @@ __global__ void k_su_flag(const int* __restrict__ nd_dev, const int* __restrict_
 }
 
 __global__ void k_su_lists(const int* __restrict__ nd_dev, const int* __restrict__ flag,
-                           const int* __restrict__ flag_off, const int* __restrict__ off,
+                           const int* __restrict__ flag_off, const int* __restrict__ off_exp,
                            int* __restrict__ cn, int4* __restrict__ cn_rec,
                            int* __restrict__ fn) {
   const long long nd = *nd_dev;
@@ -1148,7 +1148,7 @@ __global__ void k_su_lists(const int* __restrict__ nd_dev, const int* __restrict
     const int o = flag_off[i];
     if (flag[i]) {
       cn[o] = (int)i;
-      cn_rec[o] = make_int4((int)i, off[i], off[i + 1], 0);
+      cn_rec[o] = make_int4((int)i, off_exp[i], off_exp[i + 1], 0);
     } else {
       fn[i - o] = (int)i;
     }
@@ -1171,6 +1171,7 @@ int launch_solver_setup(Ctx& c, const int* nd_dev, const int* nc_dev, long long 
   if (nc_cap >= (1LL << 26))
     return set_error(MPMRB_E_INVALID, "contact capacity %lld exceeds 2^26", nc_cap);
   MPMRB_CUDA_OK(cudaMemsetAsync(su.cnt, 0, sizeof(int) * (nd_cap + 1), c.stream));
+  MPMRB_CUDA_OK(cudaMemsetAsync(su.cnt_exp, 0, sizeof(int) * (nd_cap + 1), c.stream));
   MPMRB_CUDA_OK(cudaMemsetAsync(su.fill, 0, sizeof(int) * (nd_cap + 1), c.stream));
   MPMRB_CUDA_OK(cudaMemsetAsync(su.flag, 0, sizeof(int) * (nd_cap + 1), c.stream));
   MPMRB_CUDA_OK(cudaMemsetAsync(su.counts, 0, sizeof(int) * 2, c.stream));
@@ -1181,23 +1182,25 @@ int launch_solver_setup(Ctx& c, const int* nd_dev, const int* nc_dev, long long 
   k_su_groups<<<su_grid(ncc), kSetupThreads, 0, c.stream>>>(nc_dev, su.head, su.head_off,
                                                             su.counts, su.grp_of, su.grp_start);
   k_su_count<<<su_grid(27 * ncc), kSetupThreads, 0, c.stream>>>(su.counts, nc_cap, cnodes,
-                                                                 su.grp_start, su.cnt);
+                                                                 su.grp_start, su.cnt, su.cnt_exp);
   c.launches += 3;
   // exclusive scan over nd_cap+1 entries (cnt is zero past nd: off[nd] = total)
   rc = scan_exclusive_i32(c, su.cnt, su.off, nd_cap + 1, nullptr, nullptr, tiles);
+  if (rc) return rc;
+  rc = scan_exclusive_i32(c, su.cnt_exp, su.off_exp, nd_cap + 1, nullptr, nullptr, tiles);
   if (rc) return rc;
   k_su_fill<<<su_grid(27 * ncc), kSetupThreads, 0, c.stream>>>(su.counts, nc_cap, cnodes,
                                                                 su.grp_start, su.off, su.fill,
                                                                 su.ent_tmp);
   k_su_rank<<<su_grid(27 * ncc), kSetupThreads, 0, c.stream>>>(nd_dev, nc_cap, cnodes,
                                                                 su.grp_of, su.grp_start, su.off,
-                                                                su.ent_tmp, su.ent);
+                                                                su.off_exp, su.ent_tmp, su.ent);
   k_su_flag<<<su_grid(nd_cap + 1), kSetupThreads, 0, c.stream>>>(nd_dev, su.cnt, su.flag);
   c.launches += 3;
   rc = scan_exclusive_i32(c, su.flag, su.flag_off, nd_cap + 1, nullptr, su.counts + 1, tiles);
   if (rc) return rc;
   k_su_lists<<<su_grid(nd_cap + 1), kSetupThreads, 0, c.stream>>>(
-      nd_dev, su.flag, su.flag_off, su.off, su.cn, su.cn_rec, su.fn);
+      nd_dev, su.flag, su.flag_off, su.off_exp, su.cn, su.cn_rec, su.fn);
   c.launches++;
   MPMRB_CUDA_OK(cudaGetLastError());
   return MPMRB_OK;

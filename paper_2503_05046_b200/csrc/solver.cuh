@@ -26,11 +26,11 @@ struct SolveOut {
 // Per-solve structure built by launch_solver_setup from the contact stencils.
 //
 // Contact groups: maximal runs of consecutive contacts with identical stencil
-// node lists (the contacts of one grid cell share all 27 nodes).  Each contact
-// owner writes one record per iteration (R^T g, R^T G R); each contact node
-// gathers, through a node -> (group, slot) CSR whose entries are sorted, the
-// records of the group's contacts weighted by their slot weight: a fixed
-// summation order (ascending contact id per node), no atomics.
+// node lists (the contacts of one grid cell share all 27 nodes); they make
+// the node adjacency cheap to build.  Each contact owner writes one record per
+// iteration (R^T g, R^T G R); each contact node gathers, through a node ->
+// (contact, slot) CSR sorted by contact, the records weighted by the slot
+// weight: a fixed summation order (ascending contact id per node), no atomics.
 struct SolverSetup {
   int* head;       // (nc_cap+1) scratch: contact starts a group
   int* head_off;   // (nc_cap+1) exclusive scan of head
@@ -39,14 +39,15 @@ struct SolverSetup {
   int* cnt;        // (nd_cap+1) scratch: entries per node
   int* fill;       // (nd_cap+1) scratch
   int* off;        // (nd_cap+1) CSR offsets
-  int* ent_tmp;    // (27 nc_cap) scratch: entries in atomic fill order
-  int2* ent;       // (27 nc_cap) (first contact of the group << 5 | slot, group length),
-                   // ascending within a node
+  int* cnt_exp;    // (nd_cap+1) scratch: contacts per node
+  int* off_exp;    // (nd_cap+1) CSR offsets of the expanded entries
+  int* ent_tmp;    // (27 nc_cap) scratch: (run, slot) entries in atomic fill order
+  int* ent;        // (27 nc_cap) (contact << 5 | slot), ascending contact within a node
   int* flag;       // (nd_cap+1) scratch: node has entries
   int* flag_off;   // (nd_cap+1) exclusive scan of flag
   int* cn;         // (nd_cap) contact nodes (ascending)
   int* fn;         // (nd_cap) free nodes (ascending)
-  int4* cn_rec;    // (nd_cap) per contact node: (node, CSR begin, CSR end, 0)
+  int4* cn_rec;    // (nd_cap) per contact node: (node, expanded CSR begin, end, 0)
   int* counts;     // device [0] n_groups, [1] n_contact_nodes
 };
 

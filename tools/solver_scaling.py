@@ -2,7 +2,9 @@
 forced CTA counts (MPMRB_SOLVER_CTAS), reporting us/iteration and (with
 MPMRB_SOLVER_PROF=1) the in-kernel phase breakdown.
 
-    python tools/solver_scaling.py [steps_to_advance] [half_x]
+    python tools/solver_scaling.py [steps_to_advance] [half_x] [half_z] [gap]
+
+(10 0.4 0.1 0 is the profiled substep of the 1M bench window.)
 """
 
 import os
@@ -21,8 +23,9 @@ from paper_2503_05046_b200.collision import contact_velocities  # noqa: E402
 from paper_2503_05046_b200.contact_model import normal_impulse  # noqa: E402
 
 
-def build_problem(steps=16, hx=0.2):
-    sc = scenes.sand_pile_scene(half=(hx, hx, hx / 2))
+def build_problem(steps=16, hx=0.2, hz=None, gap=None):
+    kw = {} if gap is None else {"gap": gap}
+    sc = scenes.sand_pile_scene(half=(hx, hx, hz if hz else hx / 2), **kw)
     st = scenes.build_state(sc)
     for _ in range(steps):
         mp.advance_step(st)
@@ -65,7 +68,9 @@ def build_problem(steps=16, hx=0.2):
 def main():
     steps = int(sys.argv[1]) if len(sys.argv) > 1 else 14
     hx = float(sys.argv[2]) if len(sys.argv) > 2 else 0.2
-    prob = build_problem(steps, hx)
+    hz = float(sys.argv[3]) if len(sys.argv) > 3 else None
+    gap = float(sys.argv[4]) if len(sys.argv) > 4 else None
+    prob = build_problem(steps, hx, hz, gap)
     par = mp.SolverParams(eps_r=5e-2, max_iters=200)
     import ctypes as C
     from paper_2503_05046_b200 import _lib
