@@ -106,6 +106,11 @@ def main():
         ncta = int(prof[8] & 0xffffffff)
         for ph, name in enumerate(["N", "D", "U", "N-reduce", "in-grid-sync (all)"]):
             v = cp[ph, :ncta]
+            if os.environ.get("PER_CTA") == "2":
+                print(f"   {name} all CTAs: " + " ".join(f"{x:.1f}" for x in v))
+            elif os.environ.get("PER_CTA"):
+                print(f"   {name} per CTA 0-7: " + " ".join(f"{x:.1f}" for x in v[:8])
+                      + "  p10/50/90: " + " ".join(f"{x:.1f}" for x in np.percentile(v, [10, 50, 90])))
             print(f"   per-CTA {name} work us/iter: mean {v.mean():.2f} max {v.max():.2f} "
                   f"(cta {int(v.argmax())}) min {v.min():.2f}", flush=True)
         ph = [prof[k] / 1e3 / it for k in range(6)]
