@@ -60,6 +60,11 @@ def parse(argv=None):
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=WORKLOADS, default="sand1m")
+    ap.add_argument("--precision", choices=["f64", "f32"], default="f64",
+                    help="f64: the reference's float64 throughout (default); f32: the fused "
+                         "path's performance mode (float32 particle state and arithmetic, "
+                         "float64 positions, grid and contact solve) -- narrower than the "
+                         "reference")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-budget", type=float, default=90.0,
@@ -308,15 +313,22 @@ class ClockSampler:
 
 # ------------------------------------------------------------------ ours
 
-def algorithmic_bytes(stage: str, n: int, n_act: int, sand: bool, prof: dict | None = None
-                      ) -> float:
+def algorithmic_bytes(stage: str, n: int, n_act: int, sand: bool, prof: dict | None = None,
+                      precision: str = "f64") -> float:
     """Algorithmic HBM bytes per launch (float64):
     P2G reads x,v (24+24), C,F (72+72), m, V0, material id (8 each) = 216 B
     per particle and writes 7 channels x 8 B = 56 B per active node; G2P reads
     x, F (96) and writes x, v, C, F (192) = 288 B per particle (+16 B plastic
     read+write for sand) and reads v_next (24 B) per active node; the contact
     solve moves 80 B per active node + 128 B per contact per iteration and
-    48 B per contact per line-search evaluation."""
+    48 B per contact per line-search evaluation.  fp32 mode (float32 v, C, F,
+    m, V0, plastic; float64 x and grid): P2G 24 + 12 + 36 + 36 + 4 + 4 + 8 =
+    124 B per particle; G2P reads x, F (24 + 36) and writes x, v, C, F
+    (24 + 12 + 36 + 36) = 168 B (+8 B plastic)."""
+    if precision == "f32" and stage == "p2g":
+        return 124.0 * n + 56.0 * n_act
+    if precision == "f32" and stage == "g2p":
+        return (168.0 + (8.0 if sand else 0.0)) * n + 24.0 * n_act
     if stage == "p2g":
         return 216.0 * n + 56.0 * n_act
     if stage == "g2p":
@@ -341,7 +353,7 @@ def run_ours(args):
     torch.cuda.set_device(local)
     D.init("nccl")
     scene = workload_scene(args.workload, rank)
-    state = scenes.build_state(scene)
+    state = scenes.build_state(scene, precision=args.precision)
     n = state.particles.n
     N = scene["substeps"]
     sand = any(m.get("model") == "sand" for m in scene["materials"])
@@ -447,7 +459,7 @@ def run_ours(args):
         traffic_all = {}
 
     def kernel_roof(stage: str) -> dict:
-        abytes = algorithmic_bytes(stage, n, prof["n_active"], sand, prof)
+        abytes = algorithmic_bytes(stage, n, prof["n_active"], sand, prof, args.precision)
         achieved = abytes / (st[stage] * 1e-3) / 1e9
         kname = {"solve": "k_qn_solve", "p2g": "k_p2g", "g2p": "k_g2p"}[stage]
         tr = traffic_all.get(kname) or {}
@@ -533,8 +545,12 @@ def run_ours(args):
             warmup=args.warmup, ms_per_step=ms_per_step,
             rigid_steps_per_s=1e3 / ms_per_step,
             higher_is_better=True, scaling="weak",
-            vs_baseline=None, dtype="f64", data="synthetic (seeded jittered lattice)",
+            vs_baseline=None,
+            dtype=("f64" if args.precision == "f64" else
+                   "f32 particle state/arithmetic; f64 positions, grid, contact solve"),
+            data="synthetic (seeded jittered lattice)",
             config=dict(workload=workload_name(args.workload, n, N),
+                        precision=args.precision,
                         particles_per_gpu=n, substeps=N, envs=world,
                         parallelism=f"{world} independent envs (1/GPU)",
                         window="the first K rigid steps from t=0 (warm-up rolled back)",

@@ -334,6 +334,17 @@ int mpmrb_sim_set_geoms(mpmrb_sim* sim, const mpmrb_geom* geoms_host, int32_t n_
 int mpmrb_sim_set_params(mpmrb_sim* sim, double h, double dt_substep,
                          const double* gravity_host, double stiffness, double tau_d,
                          double eps_v, double margin, const mpmrb_solver_params* solver);
+/* Precision of the fused substep's particle state and arithmetic (north_star
+ * "fp64 oracle mode; fp32 performance mode").  MPMRB_PREC_F64 (default) is the
+ * reference's float64 everywhere.  MPMRB_PREC_F32 keeps the sim-internal
+ * copy of v, F, C, mass, volume, plastic strain and the cached sand stress in
+ * float32 and does the per-particle arithmetic (stress, SVD, return map, P2G
+ * contributions, G2P) in float32; positions, grid channels, contacts and the
+ * contact solve stay float64, and the user's arrays stay float64 (converted
+ * at begin/end_step).  Not combinable with cloth (MPMRB_E_INVALID).  No
+ * reference counterpart (the reference is float64 only). */
+enum { MPMRB_PREC_F64 = 0, MPMRB_PREC_F32 = 1 };
+int mpmrb_sim_set_precision(mpmrb_sim* sim, int32_t precision);
 /* Codimensional cloth (new): triangles with vertex particles
  * and one element particle each.  All arrays are device arrays in the user's
  * (reference) particle order: tri (ne,3) and epart (ne,) particle indices,

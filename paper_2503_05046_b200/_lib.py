@@ -33,6 +33,7 @@ MAT_ELASTIC = 0
 MAT_SAND = 1
 MAT_CLOTH = 2
 CLOTH_NONE, CLOTH_VERTEX, CLOTH_ELEMENT = 0, 1, 2
+PREC_F64, PREC_F32 = 0, 1
 GEOM_HALFSPACE, GEOM_SPHERE, GEOM_BOX, GEOM_CAPSULE = 0, 1, 2, 3
 
 
@@ -155,6 +156,7 @@ _SIGS = {
     "mpmrb_sim_set_params": ([_P, _D, _D, C.POINTER(_D), _D, _D, _D, _D,
                               C.POINTER(SolverParamsC)], C.c_int),
     "mpmrb_sim_set_cloth": ([_P, _I64, _P, _P, _P, _P, _P, _P], C.c_int),
+    "mpmrb_sim_set_precision": ([_P, C.c_int32], C.c_int),
     "mpmrb_sim_begin_step": ([_P, _I64, C.c_int32], C.c_int),
     "mpmrb_sim_substep": ([_P], C.c_int),
     "mpmrb_sim_end_step": ([_P, C.POINTER(StepStats), C.POINTER(_D)], C.c_int),

@@ -106,6 +106,11 @@ class SimState:
     mode: str = "deterministic"
     workers: int | None = None
     cloth: object | None = None  # cloth.ClothMesh (NEW: codimensional cloth)
+    # NEW (north_star): "f64" is the reference's float64 throughout; "f32" is
+    # the performance mode of the fused path (float32 particle state and
+    # arithmetic; positions, grid and contact solve float64), see
+    # include/mpmrb_b200.h mpmrb_sim_set_precision
+    precision: str = "f64"
     time: float = 0.0
     step_index: int = 0
     plan_builds: int = 0
@@ -116,6 +121,8 @@ class SimState:
         self._accum = ImpulseAccumulator(len(self.bodies))
         if not self.h > 0:
             raise ValueError("grid spacing h must be positive")
+        if self.precision not in ("f64", "f32"):
+            raise ValueError("precision must be 'f64' or 'f32'")
         self._sim = None
         self._ctx = None  # the state's own library context (stream, scratch, status)
         self._stream = None
@@ -183,6 +190,8 @@ def advance_step(state: SimState, profile: dict | None = None) -> StepSummary:
     with torch.cuda.stream(stream):
         _lib.bind_stream(state._ctx, stream)
         pv = p.view()
+        _lib.check(L.mpmrb_sim_set_precision(
+            sim, _lib.PREC_F32 if state.precision == "f32" else _lib.PREC_F64))
         _lib.check(L.mpmrb_sim_set_particles(sim, C.byref(pv)))
         tab, nm = material_table(state.materials)
         _lib.check(L.mpmrb_sim_set_materials(sim, tab, nm))

@@ -738,6 +738,18 @@ int mpmrb_sim_set_params(mpmrb_sim* s, double h, double dt_s, const double* g, d
   return MPMRB_OK;
 }
 
+int mpmrb_sim_set_precision(mpmrb_sim* s, int32_t prec) {
+  if (!s) return set_error(MPMRB_E_INVALID, "null sim");
+  if (prec != MPMRB_PREC_F64 && prec != MPMRB_PREC_F32)
+    return set_error(MPMRB_E_INVALID, "precision must be MPMRB_PREC_F64 or MPMRB_PREC_F32");
+  if (prec != s->prec) {
+    s->invalidate();
+    s->n_particles = -1;  // re-lay the internal particle copy in reserve()
+  }
+  s->prec = prec;
+  return MPMRB_OK;
+}
+
 int mpmrb_sim_begin_step(mpmrb_sim* s, int64_t epoch, int32_t n_substeps) {
   if (!s) return set_error(MPMRB_E_INVALID, "null sim");
   return s->begin_step(epoch, n_substeps);

@@ -1,7 +1,9 @@
 // Shared device helpers for the sm_100a MPM–rigid coupling kernels.
 //
-// All hot-path arithmetic is float64, matching the reference (
-// every reference array is float64, e.g. grid.py:55-61).  B200 has full-rate
+// Hot-path arithmetic is float64, matching the reference (every
+// reference array is float64, e.g. grid.py:55-61).  The fused substep also has
+// an fp32 performance mode for the per-particle state and arithmetic (M3T,
+// Stencil1T with T = float; grid, contacts and the solve stay float64).  B200 has full-rate
 // FP64 CUDA cores (no tensor cores are used: the path is gather/scatter and
 // per-particle 3x3 algebra, not a dense contraction).
 #pragma once
@@ -38,30 +40,38 @@ __device__ __forceinline__ void raise_status(DevStatus* st, int code, int detail
 }
 
 // ----------------------------------------------------------------- small linear algebra
-struct M3 {
-  double a[9];  // row-major
-  __device__ __forceinline__ double& operator()(int i, int j) { return a[3 * i + j]; }
-  __device__ __forceinline__ double operator()(int i, int j) const { return a[3 * i + j]; }
+// 3x3 row-major matrices in the particle arithmetic type T: double (the
+// reference's float64) or float (the fp32 performance mode, sim.cu).
+template <class T>
+struct M3T {
+  T a[9];  // row-major
+  __device__ __forceinline__ T& operator()(int i, int j) { return a[3 * i + j]; }
+  __device__ __forceinline__ T operator()(int i, int j) const { return a[3 * i + j]; }
 };
+using M3 = M3T<double>;
 
-__device__ __forceinline__ M3 m3_load(const double* p) {
-  M3 m;
+template <class T>
+__device__ __forceinline__ M3T<T> m3_load(const T* p) {
+  M3T<T> m;
 #pragma unroll
   for (int i = 0; i < 9; ++i) m.a[i] = p[i];
   return m;
 }
-__device__ __forceinline__ void m3_store(double* p, const M3& m) {
+template <class T>
+__device__ __forceinline__ void m3_store(T* p, const M3T<T>& m) {
 #pragma unroll
   for (int i = 0; i < 9; ++i) p[i] = m.a[i];
 }
-__device__ __forceinline__ M3 m3_identity() {
-  M3 m;
+template <class T = double>
+__device__ __forceinline__ M3T<T> m3_identity() {
+  M3T<T> m;
 #pragma unroll
-  for (int i = 0; i < 9; ++i) m.a[i] = (i % 4 == 0) ? 1.0 : 0.0;
+  for (int i = 0; i < 9; ++i) m.a[i] = (i % 4 == 0) ? T(1) : T(0);
   return m;
 }
-__device__ __forceinline__ M3 m3_mul(const M3& x, const M3& y) {
-  M3 r;
+template <class T>
+__device__ __forceinline__ M3T<T> m3_mul(const M3T<T>& x, const M3T<T>& y) {
+  M3T<T> r;
 #pragma unroll
   for (int i = 0; i < 3; ++i)
 #pragma unroll
@@ -69,8 +79,9 @@ __device__ __forceinline__ M3 m3_mul(const M3& x, const M3& y) {
       r(i, j) = x(i, 0) * y(0, j) + x(i, 1) * y(1, j) + x(i, 2) * y(2, j);
   return r;
 }
-__device__ __forceinline__ M3 m3_mul_bt(const M3& x, const M3& y) {  // x @ y^T
-  M3 r;
+template <class T>
+__device__ __forceinline__ M3T<T> m3_mul_bt(const M3T<T>& x, const M3T<T>& y) {  // x @ y^T
+  M3T<T> r;
 #pragma unroll
   for (int i = 0; i < 3; ++i)
 #pragma unroll
@@ -79,23 +90,25 @@ __device__ __forceinline__ M3 m3_mul_bt(const M3& x, const M3& y) {  // x @ y^T
   return r;
 }
 // determinant as column triple product c0 . (c1 x c2) (materials.py:49-54)
-__device__ __forceinline__ double m3_det(const M3& m) {
-  double k0 = m(1, 1) * m(2, 2) - m(2, 1) * m(1, 2);
-  double k1 = m(2, 1) * m(0, 2) - m(0, 1) * m(2, 2);
-  double k2 = m(0, 1) * m(1, 2) - m(1, 1) * m(0, 2);
+template <class T>
+__device__ __forceinline__ T m3_det(const M3T<T>& m) {
+  T k0 = m(1, 1) * m(2, 2) - m(2, 1) * m(1, 2);
+  T k1 = m(2, 1) * m(0, 2) - m(0, 1) * m(2, 2);
+  T k2 = m(0, 1) * m(1, 2) - m(1, 1) * m(0, 2);
   return m(0, 0) * k0 + m(1, 0) * k1 + m(2, 0) * k2;
 }
 // inverse-transpose via the adjugate (materials.py:57-67)
-__device__ __forceinline__ M3 m3_inv_transpose(const M3& m) {
+template <class T>
+__device__ __forceinline__ M3T<T> m3_inv_transpose(const M3T<T>& m) {
   // columns a0,a1,a2 of m; result columns are a1xa2, a2xa0, a0xa1 over det
-  double c0[3] = {m(1, 1) * m(2, 2) - m(2, 1) * m(1, 2), m(2, 1) * m(0, 2) - m(0, 1) * m(2, 2),
-                  m(0, 1) * m(1, 2) - m(1, 1) * m(0, 2)};
-  double c1[3] = {m(1, 2) * m(2, 0) - m(2, 2) * m(1, 0), m(2, 2) * m(0, 0) - m(0, 2) * m(2, 0),
-                  m(0, 2) * m(1, 0) - m(1, 2) * m(0, 0)};
-  double c2[3] = {m(1, 0) * m(2, 1) - m(2, 0) * m(1, 1), m(2, 0) * m(0, 1) - m(0, 0) * m(2, 1),
-                  m(0, 0) * m(1, 1) - m(1, 0) * m(0, 1)};
-  double det = m(0, 0) * c0[0] + m(1, 0) * c0[1] + m(2, 0) * c0[2];
-  M3 r;
+  T c0[3] = {m(1, 1) * m(2, 2) - m(2, 1) * m(1, 2), m(2, 1) * m(0, 2) - m(0, 1) * m(2, 2),
+             m(0, 1) * m(1, 2) - m(1, 1) * m(0, 2)};
+  T c1[3] = {m(1, 2) * m(2, 0) - m(2, 2) * m(1, 0), m(2, 2) * m(0, 0) - m(0, 2) * m(2, 0),
+             m(0, 2) * m(1, 0) - m(1, 2) * m(0, 0)};
+  T c2[3] = {m(1, 0) * m(2, 1) - m(2, 0) * m(1, 1), m(2, 0) * m(0, 1) - m(0, 0) * m(2, 1),
+             m(0, 0) * m(1, 1) - m(1, 0) * m(0, 1)};
+  T det = m(0, 0) * c0[0] + m(1, 0) * c0[1] + m(2, 0) * c0[2];
+  M3T<T> r;
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
     r(i, 0) = c0[i] / det;
@@ -105,7 +118,8 @@ __device__ __forceinline__ M3 m3_inv_transpose(const M3& m) {
   return r;
 }
 
-__device__ __forceinline__ bool m3_finite(const M3& m) {
+template <class T>
+__device__ __forceinline__ bool m3_finite(const M3T<T>& m) {
   bool ok = true;
 #pragma unroll
   for (int i = 0; i < 9; ++i) ok &= isfinite(m.a[i]);
@@ -174,6 +188,45 @@ __device__ __forceinline__ void make_stencil1(const double* x, double h, Stencil
   }
 }
 
+// The same stencil with fractions and weights in the particle arithmetic
+// type T (fp32 performance mode): the base cell is still the IEEE float64
+// floor(x/h - 0.5) of the float64 position, so nodes and blocks are the
+// float64 path's.
+template <class T>
+struct Stencil1T {
+  int64_t base[3];
+  T fx[3];
+  T w[3][3];
+};
+template <class T>
+__device__ __forceinline__ void make_stencil1_t(const double* x, double h, Stencil1T<T>& s) {
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double q = __ddiv_rn(x[a], h);
+    const int64_t b = (int64_t)floor(__dsub_rn(q, 0.5));
+    const T f = (T)__dsub_rn(q, (double)b);
+    s.base[a] = b;
+    s.fx[a] = f;
+    const T t0 = T(1.5) - f, t1 = f - T(1), t2 = f - T(0.5);
+    s.w[a][0] = T(0.5) * (t0 * t0);
+    s.w[a][1] = T(0.75) - t1 * t1;
+    s.w[a][2] = T(0.5) * (t2 * t2);
+  }
+}
+template <>
+__device__ __forceinline__ void make_stencil1_t<double>(const double* x, double h,
+                                                       Stencil1T<double>& s) {
+  Stencil1 d;
+  make_stencil1(x, h, d);
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    s.base[a] = d.base[a];
+    s.fx[a] = d.fx[a];
+#pragma unroll
+    for (int o = 0; o < 3; ++o) s.w[a][o] = d.w[a][o];
+  }
+}
+
 // Resolve the <=8 blocks a stencil touches; blk[ix][iy][iz] indexed by
 // whether axis offset lands in the low (0) or high (1) block.
 struct StencilBlocks {
@@ -181,7 +234,8 @@ struct StencilBlocks {
   int64_t lo[3];
 };
 
-__device__ __forceinline__ bool resolve_blocks(const Stencil1& s,
+template <class S>
+__device__ __forceinline__ bool resolve_blocks(const S& s,
                                                const unsigned long long* __restrict__ hkeys,
                                                const int* __restrict__ hvals, uint32_t mask,
                                                StencilBlocks& sb) {
@@ -215,7 +269,8 @@ __device__ __forceinline__ bool resolve_blocks(const Stencil1& s,
 }
 
 // Linear node id of stencil slot (ox,oy,oz) (grid.py:121: block*64 + (lx*4+ly)*4+lz)
-__device__ __forceinline__ int stencil_node(const Stencil1& s, const StencilBlocks& sb, int ox,
+template <class S>
+__device__ __forceinline__ int stencil_node(const S& s, const StencilBlocks& sb, int ox,
                                             int oy, int oz) {
   int64_t cx = s.base[0] + ox, cy = s.base[1] + oy, cz = s.base[2] + oz;
   int ix = (int)((cx >> 2) != sb.lo[0]);

@@ -89,26 +89,34 @@ int launch_scatter_reduce(Ctx& c, const long long* ids, const double* vals, long
                           long long k, long long nch, long long n_out, double* out);
 int launch_stresses(Ctx& c, const double* f, const long long* mid, long long n,
                     const mpmrb_material* mats_dev, int nmat, double* tau);
-struct ParticlesDev {
+// Particle state as the kernels see it.  T is the precision of the
+// per-particle state and arithmetic: double (the reference's float64, and the
+// user's arrays) or float (the sim-internal copy in the fp32 performance
+// mode).  Positions are always float64.
+template <class T>
+struct ParticlesT {
   double* x;
-  double* v;
-  double* f;
-  double* c;
-  const double* mass;
-  const double* vol0;
+  T* v;
+  T* f;
+  T* c;
+  const T* mass;
+  const T* vol0;
   const long long* mid;
-  double* plastic;
+  T* plastic;
   long long n;
-  // codimensional cloth (NULL when absent): role per particle (MPMRB_CLOTH_*),
-  // element stresses written by the cloth kernel, vertex forces
+  // codimensional cloth (NULL when absent; float64 mode only): role per
+  // particle (MPMRB_CLOTH_*), element stresses written by the cloth kernel,
+  // vertex forces
   const signed char* role = nullptr;
   double* tau = nullptr;   // (n,9)
   double* fext = nullptr;  // (n,3)
   // sand: Hencky stress of the post-return-map F written by G2P for the next
   // substep's P2G (symmetric, 6 entries); valid when *tau_valid != 0
-  double* tau_cache = nullptr;  // (n,6)
+  T* tau_cache = nullptr;  // (n,6)
   int* tau_valid = nullptr;
 };
+using ParticlesDev = ParticlesT<double>;
+using ParticlesF32 = ParticlesT<float>;
 struct ClothDev {
   long long ne = 0;
   const int* tri = nullptr;
@@ -131,6 +139,12 @@ int launch_grid_update(Ctx& c, long long n_nodes_cap, const int* nb_dev, const d
                        double gz, double dt, unsigned char* active, double* v_k, double* v_star,
                        double* v_next_or_null, int* block_active_count_or_null);
 int launch_g2p(Ctx& c, const GridDev& g, const ParticlesDev& p, const mpmrb_material* mats_dev,
+               int nmat, const double* v_next, double dt, unsigned long long* clamped_dev,
+               int* health_dev);
+// fp32 performance mode: the same transfers on float32 particle state
+int launch_p2g(Ctx& c, const GridDev& g, const ParticlesF32& p, const mpmrb_material* mats_dev,
+               int nmat, double dt, double* mass, double* mom_apic, double* mom_force);
+int launch_g2p(Ctx& c, const GridDev& g, const ParticlesF32& p, const mpmrb_material* mats_dev,
                int nmat, const double* v_next, double dt, unsigned long long* clamped_dev,
                int* health_dev);
 
@@ -168,6 +182,11 @@ int launch_particle_gather(Ctx& c, const int* perm, long long n, const double* s
                            double* dst);
 int launch_particle_scatter(Ctx& c, const int* perm, long long n, const double* src, int width,
                             double* dst);
+// float64 user arrays <-> float32 sim-internal copy (fp32 performance mode)
+int launch_particle_gather_f32(Ctx& c, const int* perm, long long n, const double* src, int width,
+                               float* dst);
+int launch_particle_scatter_f32(Ctx& c, const int* perm, long long n, const float* src, int width,
+                                double* dst);
 int launch_gather_i64(Ctx& c, const int* perm, long long n, const long long* src, long long* dst);
 int launch_map_ids(Ctx& c, const int* ids, const int* perm, const int* n_dev, long long cap,
                    int* out);

@@ -1,4 +1,5 @@
-// Particle <-> grid transfers on sm_100a (float64).
+// Particle <-> grid transfers on sm_100a: float64, or float32 particle state
+// and arithmetic in the fp32 performance mode (the grid stays float64).
 //
 //  * k_p2g   : stress (polar / Hencky) + 27-node x 7-channel APIC/MLS scatter
 //              (mpm.py:66-99, materials.py:113-122).  One thread per particle,
@@ -20,9 +21,10 @@ namespace mpmrb {
 
 namespace {
 
-__device__ __forceinline__ M3 particle_stress(const M3& f, const mpmrb_material& m) {
-  return (m.kind == MPMRB_MAT_SAND) ? kirchhoff_hencky(f, m.mu, m.lam)
-                                    : kirchhoff_fixed_corotated(f, m.mu, m.lam);
+template <class T>
+__device__ __forceinline__ M3T<T> particle_stress(const M3T<T>& f, const mpmrb_material& m) {
+  return (m.kind == MPMRB_MAT_SAND) ? kirchhoff_hencky<T>(f, (T)m.mu, (T)m.lam)
+                                    : kirchhoff_fixed_corotated<T>(f, (T)m.mu, (T)m.lam);
 }
 
 __global__ void k_scatter_reduce(const long long* __restrict__ ids, const double* __restrict__ vals,
@@ -115,32 +117,32 @@ __global__ void k_stresses(const double* __restrict__ f, const long long* __rest
 
 // Scatter of one particle's 27 x 7 contributions with global float64 atomics
 // (the fallback when a chunk's particles are spread too widely for a tile).
-__device__ __forceinline__ void p2g_scatter_one(const GridDev& g, const double* fx,
-                                                const double (*w1)[3], const StencilBlocks& sb,
-                                                const Stencil1& s, double m, const double* mv,
-                                                const M3& mC, const M3& S, const double* fi,
+template <class T>
+__device__ __forceinline__ void p2g_scatter_one(const GridDev& g, const Stencil1T<T>& s,
+                                                const StencilBlocks& sb, T m, const T* mv,
+                                                const M3T<T>& mC, const M3T<T>& S, const T* fi,
                                                 double* gmass, double* mom_apic,
                                                 double* mom_force) {
-  const double h = g.h;
+  const T h = (T)g.h;
 #pragma unroll 1
   for (int ox = 0; ox < 3; ++ox) {
-    const double dx = (ox - fx[0]) * h;
+    const T dx = (T(ox) - s.fx[0]) * h;
 #pragma unroll 1
     for (int oy = 0; oy < 3; ++oy) {
-      const double dy = (oy - fx[1]) * h;
-      const double wxy = w1[0][ox] * w1[1][oy];
+      const T dy = (T(oy) - s.fx[1]) * h;
+      const T wxy = s.w[0][ox] * s.w[1][oy];
 #pragma unroll
       for (int oz = 0; oz < 3; ++oz) {
-        const double dz = (oz - fx[2]) * h;
-        const double w = wxy * w1[2][oz];
+        const T dz = (T(oz) - s.fx[2]) * h;
+        const T w = wxy * s.w[2][oz];
         const int node = stencil_node(s, sb, ox, oy, oz);
-        atomicAdd(&gmass[node], w * m);
+        atomicAdd(&gmass[node], (double)(w * m));
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
-          double a = mv[d] + (mC(d, 0) * dx + mC(d, 1) * dy + mC(d, 2) * dz);
-          double b = S(d, 0) * dx + S(d, 1) * dy + S(d, 2) * dz + fi[d];
-          atomicAdd(&mom_apic[3 * node + d], w * a);
-          atomicAdd(&mom_force[3 * node + d], w * b);
+          T a = mv[d] + (mC(d, 0) * dx + mC(d, 1) * dy + mC(d, 2) * dz);
+          T b = S(d, 0) * dx + S(d, 1) * dy + S(d, 2) * dz + fi[d];
+          atomicAdd(&mom_apic[3 * node + d], (double)(w * a));
+          atomicAdd(&mom_force[3 * node + d], (double)(w * b));
         }
       }
     }
@@ -162,24 +164,17 @@ __device__ __forceinline__ void p2g_scatter_one(const GridDev& g, const double* 
 constexpr int kP2GThreads = 128;
 constexpr int kWarpTile = 128;  // nodes per warp tile (e.g. 4 x 4 x 8)
 
-// two ints packed in one shared-memory double slot (payload staging)
-__device__ __forceinline__ double pack2i(int lo, int hi) {
-  return __hiloint2double(hi, lo);
-}
-__device__ __forceinline__ int2 double_as_int2(double d) {
-  return make_int2(__double2loint(d), __double2hiint(d));
-}
-
 // Per-particle P2G payload: m, m v, m C, S = -dt D^-1 V0 tau and the external
 // impulse dt f of cloth vertex forces.  Cloth roles (cloth.cu): vertex
 // particles carry no stress (their in-plane forces arrive in fext), element
 // particles carry the transverse stress written by k_cloth_forces.
-__device__ __forceinline__ void particle_payload(const ParticlesDev& p, long long i, double h,
+template <class T>
+__device__ __forceinline__ void particle_payload(const ParticlesT<T>& p, long long i, double h,
                                                  double dt, const mpmrb_material* mats, int nmat,
-                                                 Stencil1& s, double& m, double* mv, M3& mC,
-                                                 M3& S, double* fi, DevStatus* st) {
+                                                 Stencil1T<T>& s, T& m, T* mv, M3T<T>& mC,
+                                                 M3T<T>& S, T* fi, DevStatus* st) {
   double xp[3] = {p.x[3 * i], p.x[3 * i + 1], p.x[3 * i + 2]};
-  make_stencil1(xp, h, s);
+  make_stencil1_t<T>(xp, h, s);
   long long mid = p.mid[i];
   if (mid < 0 || mid >= nmat) {
     raise_status(st, MPMRB_E_INVALID, 21, i);
@@ -187,14 +182,15 @@ __device__ __forceinline__ void particle_payload(const ParticlesDev& p, long lon
   }
   m = p.mass[i];
   const int role = p.role ? p.role[i] : MPMRB_CLOTH_NONE;
-  M3 tau;
+  M3T<T> tau;
   if (role == MPMRB_CLOTH_ELEMENT && p.tau) {
-    tau = m3_load(p.tau + 9 * i);
+#pragma unroll
+    for (int k = 0; k < 9; ++k) tau.a[k] = (T)p.tau[9 * i + k];
   } else if (role != MPMRB_CLOTH_NONE || mats[mid].kind == MPMRB_MAT_CLOTH) {
 #pragma unroll
-    for (int k = 0; k < 9; ++k) tau.a[k] = 0.0;
+    for (int k = 0; k < 9; ++k) tau.a[k] = T(0);
   } else if (p.tau_cache && mats[mid].kind == MPMRB_MAT_SAND && *p.tau_valid) {
-    const double* t6 = p.tau_cache + 6 * i;  // xx yy zz xy xz yz
+    const T* t6 = p.tau_cache + 6 * i;  // xx yy zz xy xz yz
     tau.a[0] = t6[0];
     tau.a[4] = t6[1];
     tau.a[8] = t6[2];
@@ -202,11 +198,11 @@ __device__ __forceinline__ void particle_payload(const ParticlesDev& p, long lon
     tau.a[2] = tau.a[6] = t6[4];
     tau.a[5] = tau.a[7] = t6[5];
   } else {
-    tau = particle_stress(m3_load(p.f + 9 * i), mats[mid]);
+    tau = particle_stress<T>(m3_load(p.f + 9 * i), mats[mid]);
   }
   const double dinv = 4.0 / (h * h);
-  const double coef = (-dt * dinv) * p.vol0[i];
-  const M3 C = m3_load(p.c + 9 * i);
+  const T coef = (T)((-dt * dinv) * (double)p.vol0[i]);
+  const M3T<T> C = m3_load(p.c + 9 * i);
 #pragma unroll
   for (int k = 0; k < 9; ++k) {
     S.a[k] = coef * tau.a[k];
@@ -215,7 +211,7 @@ __device__ __forceinline__ void particle_payload(const ParticlesDev& p, long lon
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
     mv[d] = m * p.v[3 * i + d];
-    fi[d] = (role == MPMRB_CLOTH_VERTEX && p.fext) ? dt * p.fext[3 * i + d] : 0.0;
+    fi[d] = (role == MPMRB_CLOTH_VERTEX && p.fext) ? (T)(dt * p.fext[3 * i + d]) : T(0);
   }
 }
 
@@ -228,10 +224,10 @@ __global__ void k_p2g_entries(GridDev g, ParticlesDev p, const mpmrb_material* _
                               double* __restrict__ vals, DevStatus* st) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= p.n) return;
-  Stencil1 s;
+  Stencil1T<double> s;
   double m, mv[3], fi[3];
   M3 mC, S;
-  particle_payload(p, i, g.h, dt, mats, nmat, s, m, mv, mC, S, fi, st);
+  particle_payload<double>(p, i, g.h, dt, mats, nmat, s, m, mv, mC, S, fi, st);
   StencilBlocks sb;
   if (!resolve_blocks(s, g.hkeys, g.hvals, g.mask, sb)) {
     raise_status(st, MPMRB_E_ALLOCATION, 23, i);
@@ -275,7 +271,8 @@ __global__ void k_split7(const double* __restrict__ in, long long n, double* __r
 #ifndef MPMRB_G2P_MINB
 #define MPMRB_G2P_MINB 4
 #endif
-__global__ void __launch_bounds__(kP2GThreads, MPMRB_P2G_MINB) k_p2g(GridDev g, ParticlesDev p,
+template <class T>
+__global__ void __launch_bounds__(kP2GThreads, MPMRB_P2G_MINB) k_p2g(GridDev g, ParticlesT<T> p,
                                                      const mpmrb_material* __restrict__ mats,
                                                      int nmat, double dt,
                                                      double* __restrict__ gmass,
@@ -283,7 +280,8 @@ __global__ void __launch_bounds__(kP2GThreads, MPMRB_P2G_MINB) k_p2g(GridDev g, 
                                                      double* __restrict__ mom_force,
                                                      DevStatus* st) {
   __shared__ double s_tile[kP2GThreads / 32][7][kWarpTile];
-  __shared__ double s_pay[kP2GThreads / 32][39][16];  // 16 particles' payloads
+  __shared__ T s_pay[kP2GThreads / 32][37][16];  // 16 particles' payloads
+  __shared__ int s_cell[kP2GThreads / 32][3][16];  // their cells in the tile
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const long long w0 = ((long long)blockIdx.x * kP2GThreads) + wid * 32;
   if (w0 >= p.n) return;
@@ -310,16 +308,16 @@ __global__ void __launch_bounds__(kP2GThreads, MPMRB_P2G_MINB) k_p2g(GridDev g, 
   if ((long long)nx * ny * nz > kWarpTile || !spans2) {
     // spread warp: per-particle scatter with global atomics
     if (live) {
-      Stencil1 s;
-      double m, mv[3], fi[3];
-      M3 mC, S;
-      particle_payload(p, i, h, dt, mats, nmat, s, m, mv, mC, S, fi, st);
+      Stencil1T<T> s;
+      T m, mv[3], fi[3];
+      M3T<T> mC, S;
+      particle_payload<T>(p, i, h, dt, mats, nmat, s, m, mv, mC, S, fi, st);
       StencilBlocks sb;
       if (!resolve_blocks(s, g.hkeys, g.hvals, g.mask, sb)) {
         raise_status(st, MPMRB_E_ALLOCATION, 20, i);
         return;
       }
-      p2g_scatter_one(g, s.fx, s.w, sb, s, m, mv, mC, S, fi, gmass, mom_apic, mom_force);
+      p2g_scatter_one<T>(g, s, sb, m, mv, mC, S, fi, gmass, mom_apic, mom_force);
     }
     return;
   }
@@ -330,12 +328,12 @@ __global__ void __launch_bounds__(kP2GThreads, MPMRB_P2G_MINB) k_p2g(GridDev g, 
 #pragma unroll
     for (int ch = 0; ch < 7; ++ch) tile[ch][q] = 0.0;
   // 3. payload of this lane's particle (registers)
-  Stencil1 s;
-  double m = 0.0, mv[3] = {0.0, 0.0, 0.0}, fi[3] = {0.0, 0.0, 0.0};
-  M3 mC, S;
+  Stencil1T<T> s;
+  T m = T(0), mv[3] = {T(0), T(0), T(0)}, fi[3] = {T(0), T(0), T(0)};
+  M3T<T> mC, S;
   int cb[3] = {0, 0, 0};
   if (live) {
-    particle_payload(p, i, h, dt, mats, nmat, s, m, mv, mC, S, fi, st);
+    particle_payload<T>(p, i, h, dt, mats, nmat, s, m, mv, mC, S, fi, st);
 #pragma unroll
     for (int a = 0; a < 3; ++a) cb[a] = (int)s.base[a] - lo[a];
   }
@@ -347,9 +345,10 @@ __global__ void __launch_bounds__(kP2GThreads, MPMRB_P2G_MINB) k_p2g(GridDev g, 
   // through shared memory in two halves of 16 particles.
   const int ox = lane / 9, oy = (lane / 3) % 3, oz = lane % 3;
   const bool slot_lane = lane < 27;
-  double (*pay)[16] = s_pay[wid];
+  T (*pay)[16] = s_pay[wid];
   const int n_live = (int)min((long long)32, p.n - w0);
-  double acc[7];
+  const T hT = (T)h;
+  T acc[7];
   int q_run = -1;  // node of the particle run being summed in acc
 #pragma unroll 1
   for (int half = 0; half < 2; ++half) {
@@ -371,8 +370,8 @@ __global__ void __launch_bounds__(kP2GThreads, MPMRB_P2G_MINB) k_p2g(GridDev g, 
         pay[19 + k][r] = S.a[k];
         pay[28 + k][r] = s.w[k / 3][k % 3];
       }
-      pay[37][r] = pack2i(cb[0], cb[1]);
-      pay[38][r] = pack2i(cb[2], 0);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) s_cell[wid][a][r] = cb[a];
     }
     __syncwarp();
     if (slot_lane) {
@@ -383,26 +382,28 @@ __global__ void __launch_bounds__(kP2GThreads, MPMRB_P2G_MINB) k_p2g(GridDev g, 
       const int pend = min(16, n_live - p0);
 #pragma unroll 1
       for (int r = 0; r < pend; ++r) {
-        const double pm = pay[0][r];
-        const double dx = (ox - pay[7][r]) * h, dy = (oy - pay[8][r]) * h, dz = (oz - pay[9][r]) * h;
-        const double w = (pay[28 + ox][r] * pay[31 + oy][r]) * pay[34 + oz][r];
-        double v[7];
+        const T pm = pay[0][r];
+        const T dx = (T(ox) - pay[7][r]) * hT, dy = (T(oy) - pay[8][r]) * hT,
+                dz = (T(oz) - pay[9][r]) * hT;
+        const T w = (pay[28 + ox][r] * pay[31 + oy][r]) * pay[34 + oz][r];
+        T v[7];
         v[0] = w * pm;
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
-          const double aa = pay[1 + d][r] +
-                            (pay[10 + 3 * d][r] * dx + pay[11 + 3 * d][r] * dy + pay[12 + 3 * d][r] * dz);
-          const double bb = pay[19 + 3 * d][r] * dx + pay[20 + 3 * d][r] * dy + pay[21 + 3 * d][r] * dz;
+          const T aa = pay[1 + d][r] +
+                       (pay[10 + 3 * d][r] * dx + pay[11 + 3 * d][r] * dy + pay[12 + 3 * d][r] * dz);
+          const T bb = pay[19 + 3 * d][r] * dx + pay[20 + 3 * d][r] * dy + pay[21 + 3 * d][r] * dz;
           v[1 + d] = w * aa;
           v[4 + d] = w * (bb + pay[4 + d][r]);
         }
-        const int2 c01 = double_as_int2(pay[37][r]);
-        const int c2 = double_as_int2(pay[38][r]).x;
-        const int q = ((c01.x + ox) * ny + (c01.y + oy)) * nz + (c2 + oz);
+        const int q = ((s_cell[wid][0][r] + ox) * ny + (s_cell[wid][1][r] + oy)) * nz +
+                      (s_cell[wid][2][r] + oz);
         if (q != q_run) {
+          // the run changes on every slot lane at once (the cell changed)
+          __syncwarp(0x07ffffffu);
           if (q_run >= 0)
 #pragma unroll
-            for (int ch = 0; ch < 7; ++ch) tile[ch][q_run] += acc[ch];
+            for (int ch = 0; ch < 7; ++ch) tile[ch][q_run] += (double)acc[ch];
 #pragma unroll
           for (int ch = 0; ch < 7; ++ch) acc[ch] = v[ch];
           q_run = q;
@@ -415,7 +416,7 @@ __global__ void __launch_bounds__(kP2GThreads, MPMRB_P2G_MINB) k_p2g(GridDev g, 
   }
   if (slot_lane && q_run >= 0)
 #pragma unroll
-    for (int ch = 0; ch < 7; ++ch) tile[ch][q_run] += acc[ch];
+    for (int ch = 0; ch < 7; ++ch) tile[ch][q_run] += (double)acc[ch];
   __syncwarp();
   // 5. flush: one atomic per (node, channel).  The tile spans at most 2
   // blocks per axis (<= 8 blocks, nodes <= 10 per axis): lanes 0-7 resolve
@@ -498,12 +499,13 @@ __global__ void k_grid_update(long long n_cap, const int* __restrict__ nb_dev,
   }
 }
 
-__global__ void __launch_bounds__(128, MPMRB_G2P_MINB) k_g2p(GridDev g, ParticlesDev p,
+template <class T>
+__global__ void __launch_bounds__(128, MPMRB_G2P_MINB) k_g2p(GridDev g, ParticlesT<T> p,
                                              const mpmrb_material* __restrict__ mats, int nmat,
                                              const double* __restrict__ v_next, double dt,
                                              unsigned long long* __restrict__ clamped,
                                              int* __restrict__ health, DevStatus* st) {
-  __shared__ double s_v[128 / 32][3][kWarpTile];
+  __shared__ T s_v[128 / 32][3][kWarpTile];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const bool live = i < p.n;
@@ -528,7 +530,7 @@ __global__ void __launch_bounds__(128, MPMRB_G2P_MINB) k_g2p(GridDev g, Particle
                      (((lo[0] + nx - 1) >> 2) - (lo[0] >> 2) <= 1) &&
                      (((lo[1] + ny - 1) >> 2) - (lo[1] >> 2) <= 1) &&
                      (((lo[2] + nz - 1) >> 2) - (lo[2] >> 2) <= 1);
-  double (*tv)[kWarpTile] = s_v[wid];
+  T (*tv)[kWarpTile] = s_v[wid];
   if (tiled) {
     const int blo0 = lo[0] >> 2, blo1 = lo[1] >> 2, blo2 = lo[2] >> 2;
     int myblk = -1;
@@ -551,38 +553,39 @@ __global__ void __launch_bounds__(128, MPMRB_G2P_MINB) k_g2p(GridDev g, Particle
       const long long node =
           (long long)(blk < 0 ? 0 : blk) * kNodesPerBlock + (((gx & 3) << 4) | ((gy & 3) << 2) | (gz & 3));
 #pragma unroll
-      for (int d = 0; d < 3; ++d) tv[d][q] = blk < 0 ? 0.0 : v_next[3 * node + d];
+      for (int d = 0; d < 3; ++d) tv[d][q] = blk < 0 ? T(0) : (T)v_next[3 * node + d];
     }
     __syncwarp();
   }
   if (live) {
     double xp[3] = {p.x[3 * i], p.x[3 * i + 1], p.x[3 * i + 2]};
-    Stencil1 s;
-    make_stencil1(xp, h, s);
+    Stencil1T<T> s;
+    make_stencil1_t<T>(xp, h, s);
     StencilBlocks sb;
     bool ok = true;
     if (!tiled) ok = resolve_blocks(s, g.hkeys, g.hvals, g.mask, sb);
     if (!ok) {
       raise_status(st, MPMRB_E_ALLOCATION, 30, i);
     } else {
-      double vn[3] = {0.0, 0.0, 0.0};
-      M3 B;
+      const T hT = (T)h;
+      T vn[3] = {T(0), T(0), T(0)};
+      M3T<T> B;
 #pragma unroll
-      for (int k = 0; k < 9; ++k) B.a[k] = 0.0;
+      for (int k = 0; k < 9; ++k) B.a[k] = T(0);
       const int cb0 = (int)s.base[0] - lo[0], cb1 = (int)s.base[1] - lo[1],
                 cb2 = (int)s.base[2] - lo[2];
 #pragma unroll 1
       for (int ox = 0; ox < 3; ++ox) {
-        const double dx = (ox - s.fx[0]) * h;
+        const T dx = (T(ox) - s.fx[0]) * hT;
 #pragma unroll 1
         for (int oy = 0; oy < 3; ++oy) {
-          const double dy = (oy - s.fx[1]) * h;
-          const double wxy = s.w[0][ox] * s.w[1][oy];
+          const T dy = (T(oy) - s.fx[1]) * hT;
+          const T wxy = s.w[0][ox] * s.w[1][oy];
 #pragma unroll
           for (int oz = 0; oz < 3; ++oz) {
-            const double dz = (oz - s.fx[2]) * h;
-            const double w = wxy * s.w[2][oz];
-            double vv[3];
+            const T dz = (T(oz) - s.fx[2]) * hT;
+            const T w = wxy * s.w[2][oz];
+            T vv[3];
             if (tiled) {
               const int q = ((cb0 + ox) * ny + (cb1 + oy)) * nz + (cb2 + oz);
 #pragma unroll
@@ -590,9 +593,9 @@ __global__ void __launch_bounds__(128, MPMRB_G2P_MINB) k_g2p(GridDev g, Particle
             } else {
               const int node = stencil_node(s, sb, ox, oy, oz);
 #pragma unroll
-              for (int d = 0; d < 3; ++d) vv[d] = v_next[3 * node + d];
+              for (int d = 0; d < 3; ++d) vv[d] = (T)v_next[3 * node + d];
             }
-            double wv[3];
+            T wv[3];
 #pragma unroll
             for (int d = 0; d < 3; ++d) {
               wv[d] = w * vv[d];
@@ -604,29 +607,31 @@ __global__ void __launch_bounds__(128, MPMRB_G2P_MINB) k_g2p(GridDev g, Particle
           }
         }
       }
-      const double dinv = 4.0 / (h * h);
-      M3 C;
+      const T dinv = (T)(4.0 / (h * h));
+      M3T<T> C;
 #pragma unroll
       for (int k = 0; k < 9; ++k) C.a[k] = dinv * B.a[k];
-      M3 A = m3_identity();
+      M3T<T> A = m3_identity<T>();
+      const T dtT = (T)dt;
 #pragma unroll
-      for (int k = 0; k < 9; ++k) A.a[k] += dt * C.a[k];
+      for (int k = 0; k < 9; ++k) A.a[k] += dtT * C.a[k];
       const bool cloth = p.role && p.role[i] != MPMRB_CLOTH_NONE;
-      M3 F = m3_load(p.f + 9 * i);
+      M3T<T> F = m3_load(p.f + 9 * i);
       if (!cloth) {  // cloth particles carry no F (cloth.cu: d3 per element)
         F = m3_mul(A, F);
-        if (!(m3_det(F) > 0.0) || !m3_finite(F)) {
+        if (!(m3_det(F) > T(0)) || !m3_finite(F)) {
           F = clamp_singular_values(F);
           was_clamped = true;
         }
       }
       long long mid = p.mid[i];
       if (!cloth && mid >= 0 && mid < nmat && mats[mid].kind == MPMRB_MAT_SAND) {
-        double dq = 0.0;
+        T dq = T(0);
+        const T mu = (T)mats[mid].mu, lam = (T)mats[mid].lam, al = (T)mats[mid].dp_alpha;
         if (p.tau_cache) {
-          M3 t;
-          F = dp_return_map_tau(F, mats[mid].mu, mats[mid].lam, mats[mid].dp_alpha, &dq, &t);
-          double* t6 = p.tau_cache + 6 * i;
+          M3T<T> t;
+          F = dp_return_map_tau<T>(F, mu, lam, al, &dq, &t);
+          T* t6 = p.tau_cache + 6 * i;
           t6[0] = t.a[0];
           t6[1] = t.a[4];
           t6[2] = t.a[8];
@@ -634,14 +639,14 @@ __global__ void __launch_bounds__(128, MPMRB_G2P_MINB) k_g2p(GridDev g, Particle
           t6[4] = t.a[2];
           t6[5] = t.a[5];
         } else {
-          F = dp_return_map(F, mats[mid].mu, mats[mid].lam, mats[mid].dp_alpha, &dq);
+          F = dp_return_map<T>(F, mu, lam, al, &dq);
         }
         if (p.plastic) p.plastic[i] += dq;
       }
       double xn[3];
 #pragma unroll
       for (int d = 0; d < 3; ++d) {
-        xn[d] = xp[d] + dt * vn[d];
+        xn[d] = xp[d] + dt * (double)vn[d];
         p.x[3 * i + d] = xn[d];
         p.v[3 * i + d] = vn[d];
       }
@@ -769,14 +774,23 @@ int launch_stresses(Ctx& c, const double* f, const long long* mid, long long n,
   return MPMRB_OK;
 }
 
-int launch_p2g(Ctx& c, const GridDev& g, const ParticlesDev& p, const mpmrb_material* mats_dev,
-               int nmat, double dt, double* mass, double* mom_apic, double* mom_force) {
+template <class T>
+int launch_p2g_t(Ctx& c, const GridDev& g, const ParticlesT<T>& p, const mpmrb_material* mats_dev,
+                 int nmat, double dt, double* mass, double* mom_apic, double* mom_force) {
   if (p.n == 0) return MPMRB_OK;
-  k_p2g<<<grid_for(p.n, kP2GThreads), kP2GThreads, 0, c.stream>>>(g, p, mats_dev, nmat, dt, mass,
-                                                                  mom_apic, mom_force, c.status);
+  k_p2g<T><<<grid_for(p.n, kP2GThreads), kP2GThreads, 0, c.stream>>>(
+      g, p, mats_dev, nmat, dt, mass, mom_apic, mom_force, c.status);
   c.launches++;
   MPMRB_CUDA_OK(cudaGetLastError());
   return MPMRB_OK;
+}
+int launch_p2g(Ctx& c, const GridDev& g, const ParticlesDev& p, const mpmrb_material* mats_dev,
+               int nmat, double dt, double* mass, double* mom_apic, double* mom_force) {
+  return launch_p2g_t<double>(c, g, p, mats_dev, nmat, dt, mass, mom_apic, mom_force);
+}
+int launch_p2g(Ctx& c, const GridDev& g, const ParticlesF32& p, const mpmrb_material* mats_dev,
+               int nmat, double dt, double* mass, double* mom_apic, double* mom_force) {
+  return launch_p2g_t<float>(c, g, p, mats_dev, nmat, dt, mass, mom_apic, mom_force);
 }
 
 int launch_p2g_ordered(Ctx& c, const GridDev& g, const ParticlesDev& p,
@@ -822,15 +836,26 @@ int launch_grid_update(Ctx& c, long long n_cap, const int* nb_dev, const double*
   return MPMRB_OK;
 }
 
-int launch_g2p(Ctx& c, const GridDev& g, const ParticlesDev& p, const mpmrb_material* mats_dev,
-               int nmat, const double* v_next, double dt, unsigned long long* clamped_dev,
-               int* health_dev) {
+template <class T>
+int launch_g2p_t(Ctx& c, const GridDev& g, const ParticlesT<T>& p, const mpmrb_material* mats_dev,
+                 int nmat, const double* v_next, double dt, unsigned long long* clamped_dev,
+                 int* health_dev) {
   if (p.n == 0) return MPMRB_OK;
-  k_g2p<<<grid_for(p.n, 128), 128, 0, c.stream>>>(g, p, mats_dev, nmat, v_next, dt, clamped_dev,
-                                                  health_dev, c.status);
+  k_g2p<T><<<grid_for(p.n, 128), 128, 0, c.stream>>>(g, p, mats_dev, nmat, v_next, dt,
+                                                     clamped_dev, health_dev, c.status);
   c.launches++;
   MPMRB_CUDA_OK(cudaGetLastError());
   return MPMRB_OK;
+}
+int launch_g2p(Ctx& c, const GridDev& g, const ParticlesDev& p, const mpmrb_material* mats_dev,
+               int nmat, const double* v_next, double dt, unsigned long long* clamped_dev,
+               int* health_dev) {
+  return launch_g2p_t<double>(c, g, p, mats_dev, nmat, v_next, dt, clamped_dev, health_dev);
+}
+int launch_g2p(Ctx& c, const GridDev& g, const ParticlesF32& p, const mpmrb_material* mats_dev,
+               int nmat, const double* v_next, double dt, unsigned long long* clamped_dev,
+               int* health_dev) {
+  return launch_g2p_t<float>(c, g, p, mats_dev, nmat, v_next, dt, clamped_dev, health_dev);
 }
 
 }  // namespace mpmrb

@@ -117,6 +117,25 @@ __global__ void k_scatter_back(const double* __restrict__ src, const int* __rest
     dst[(long long)perm[i] * W + k] = src[e];
   }
 }
+// float64 user arrays <-> float32 sim-internal copy (fp32 performance mode)
+template <int W>
+__global__ void k_gather_f32(const double* __restrict__ src, const int* __restrict__ perm,
+                             long long n, float* __restrict__ dst) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n * W;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long i = e / W, k = e - i * W;
+    dst[e] = (float)src[(long long)perm[i] * W + k];
+  }
+}
+template <int W>
+__global__ void k_scatter_back_f32(const float* __restrict__ src, const int* __restrict__ perm,
+                                   long long n, double* __restrict__ dst) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n * W;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long i = e / W, k = e - i * W;
+    dst[(long long)perm[i] * W + k] = (double)src[e];
+  }
+}
 __global__ void k_gather_i64(const long long* __restrict__ src, const int* __restrict__ perm,
                              long long n, long long* __restrict__ dst) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -212,6 +231,34 @@ int launch_particle_scatter(Ctx& c, const int* perm, long long n, const double* 
     case 1: k_scatter_back<1><<<gs_grid(n, 256), 256, 0, c.stream>>>(src, perm, n, dst); break;
     case 3: k_scatter_back<3><<<gs_grid(3 * n, 256), 256, 0, c.stream>>>(src, perm, n, dst); break;
     case 9: k_scatter_back<9><<<gs_grid(9 * n, 256), 256, 0, c.stream>>>(src, perm, n, dst); break;
+    default: return set_error(MPMRB_E_INVALID, "scatter width %d", width);
+  }
+  c.launches++;
+  MPMRB_CUDA_OK(cudaGetLastError());
+  return MPMRB_OK;
+}
+
+int launch_particle_gather_f32(Ctx& c, const int* perm, long long n, const double* src, int width,
+                               float* dst) {
+  if (n == 0) return MPMRB_OK;
+  switch (width) {
+    case 1: k_gather_f32<1><<<gs_grid(n, 256), 256, 0, c.stream>>>(src, perm, n, dst); break;
+    case 3: k_gather_f32<3><<<gs_grid(3 * n, 256), 256, 0, c.stream>>>(src, perm, n, dst); break;
+    case 9: k_gather_f32<9><<<gs_grid(9 * n, 256), 256, 0, c.stream>>>(src, perm, n, dst); break;
+    default: return set_error(MPMRB_E_INVALID, "gather width %d", width);
+  }
+  c.launches++;
+  MPMRB_CUDA_OK(cudaGetLastError());
+  return MPMRB_OK;
+}
+
+int launch_particle_scatter_f32(Ctx& c, const int* perm, long long n, const float* src, int width,
+                                double* dst) {
+  if (n == 0) return MPMRB_OK;
+  switch (width) {
+    case 1: k_scatter_back_f32<1><<<gs_grid(n, 256), 256, 0, c.stream>>>(src, perm, n, dst); break;
+    case 3: k_scatter_back_f32<3><<<gs_grid(3 * n, 256), 256, 0, c.stream>>>(src, perm, n, dst); break;
+    case 9: k_scatter_back_f32<9><<<gs_grid(9 * n, 256), 256, 0, c.stream>>>(src, perm, n, dst); break;
     default: return set_error(MPMRB_E_INVALID, "scatter width %d", width);
   }
   c.launches++;

@@ -281,6 +281,21 @@ int Sim::reserve(long long n, long long nb_needed) {
     q.n = n;
     q.tau_cache = b_taucache.as<double>();
     q.tau_valid = b_tauvalid.as<int>();
+    if (prec == MPMRB_PREC_F32) {
+      if (b_qf.grow(4 * 30 * nn)) return MPMRB_E_CUDA;
+      float* fp = b_qf.as<float>();
+      q32.x = q.x;
+      q32.v = fp;
+      q32.f = fp + 3 * nn;
+      q32.c = fp + 12 * nn;
+      q32.mass = fp + 21 * nn;
+      q32.vol0 = fp + 22 * nn;
+      q32.plastic = fp + 23 * nn;
+      q32.tau_cache = fp + 24 * nn;
+      q32.mid = q.mid;
+      q32.n = n;
+      q32.tau_valid = q.tau_valid;
+    }
   }
   rc |= b_hkeys.grow(8 * hash_cap);
   rc |= b_hvals.grow(4 * hash_cap);
@@ -350,8 +365,11 @@ int Sim::capture_or_launch() {
     rc = launch_cloth_forces(c, cloth, q, b_mats.as<mpmrb_material>(), nmat);
     if (rc) return rc;
   }
-  rc = launch_p2g(c, g, q, b_mats.as<mpmrb_material>(), nmat, dt_s, b_mass.as<double>(), mom_apic,
-                  mom_force);
+  rc = (prec == MPMRB_PREC_F32)
+           ? launch_p2g(c, g, q32, b_mats.as<mpmrb_material>(), nmat, dt_s, b_mass.as<double>(),
+                        mom_apic, mom_force)
+           : launch_p2g(c, g, q, b_mats.as<mpmrb_material>(), nmat, dt_s, b_mass.as<double>(),
+                        mom_apic, mom_force);
   if (rc) return rc;
   mark(2);
   // 3. grid update + ordered active compaction (mpm.py:102-115, solver.py:203-205)
@@ -475,8 +493,11 @@ int Sim::capture_or_launch() {
   c.launches += 2;
   mark(6);
   // 6. G2P (mpm.py:118-138)
-  rc = launch_g2p(c, g, q, b_mats.as<mpmrb_material>(), nmat, b_vnext.as<double>(), dt_s,
-                  b_misc.as<unsigned long long>(), b_misc.as<int>() + 2);
+  rc = (prec == MPMRB_PREC_F32)
+           ? launch_g2p(c, g, q32, b_mats.as<mpmrb_material>(), nmat, b_vnext.as<double>(), dt_s,
+                        b_misc.as<unsigned long long>(), b_misc.as<int>() + 2)
+           : launch_g2p(c, g, q, b_mats.as<mpmrb_material>(), nmat, b_vnext.as<double>(), dt_s,
+                        b_misc.as<unsigned long long>(), b_misc.as<int>() + 2);
   if (rc) return rc;
   if (cloth.ne > 0) {  // d3 advection, return map, element particles to centroids
     rc = launch_cloth_post(c, cloth, q, b_mats.as<mpmrb_material>(), nmat, dt_s);
@@ -520,6 +541,8 @@ int Sim::begin_step(long long epoch, int n_substeps) {
   Ctx& c = *ctx;
   if (!have_particles) return set_error(MPMRB_E_INVALID, "sim: particles not set");
   if (!have_params) return set_error(MPMRB_E_INVALID, "sim: params not set");
+  if (prec == MPMRB_PREC_F32 && cloth.ne > 0)
+    return set_error(MPMRB_E_INVALID, "sim: the fp32 performance mode does not support cloth");
   // size the grid for the current positions (one host sync per step)
   if (b_counters.grow(64) || b_misc.grow(64) || b_solveout.grow(sizeof(SolveOut)) ||
       b_bar.grow(4096) || b_partials.grow(sizeof(double) * (2 * 8 * kMaxSolverCtas + 8)) ||
@@ -589,16 +612,28 @@ int Sim::begin_step(long long epoch, int n_substeps) {
     if (rc) return rc;
     const int* perm = b_perm.as<int>();
     rc = launch_particle_gather(c, perm, p.n, p.x, 3, q.x);
-    if (!rc) rc = launch_particle_gather(c, perm, p.n, p.v, 3, q.v);
-    if (!rc) rc = launch_particle_gather(c, perm, p.n, p.f, 9, q.f);
-    if (!rc) rc = launch_particle_gather(c, perm, p.n, p.c, 9, q.c);
-    if (!rc) rc = launch_particle_gather(c, perm, p.n, p.mass, 1, const_cast<double*>(q.mass));
-    if (!rc) rc = launch_particle_gather(c, perm, p.n, p.vol0, 1, const_cast<double*>(q.vol0));
-    if (!rc) rc = launch_gather_i64(c, perm, p.n, p.mid, const_cast<long long*>(q.mid));
-    if (!rc) {
-      if (p.plastic) rc = launch_particle_gather(c, perm, p.n, p.plastic, 1, q.plastic);
-      else MPMRB_CUDA_OK(cudaMemsetAsync(q.plastic, 0, 8 * p.n, c.stream));
+    if (prec == MPMRB_PREC_F32) {
+      if (!rc) rc = launch_particle_gather_f32(c, perm, p.n, p.v, 3, q32.v);
+      if (!rc) rc = launch_particle_gather_f32(c, perm, p.n, p.f, 9, q32.f);
+      if (!rc) rc = launch_particle_gather_f32(c, perm, p.n, p.c, 9, q32.c);
+      if (!rc) rc = launch_particle_gather_f32(c, perm, p.n, p.mass, 1, const_cast<float*>(q32.mass));
+      if (!rc) rc = launch_particle_gather_f32(c, perm, p.n, p.vol0, 1, const_cast<float*>(q32.vol0));
+      if (!rc) {
+        if (p.plastic) rc = launch_particle_gather_f32(c, perm, p.n, p.plastic, 1, q32.plastic);
+        else MPMRB_CUDA_OK(cudaMemsetAsync(q32.plastic, 0, 4 * p.n, c.stream));
+      }
+    } else {
+      if (!rc) rc = launch_particle_gather(c, perm, p.n, p.v, 3, q.v);
+      if (!rc) rc = launch_particle_gather(c, perm, p.n, p.f, 9, q.f);
+      if (!rc) rc = launch_particle_gather(c, perm, p.n, p.c, 9, q.c);
+      if (!rc) rc = launch_particle_gather(c, perm, p.n, p.mass, 1, const_cast<double*>(q.mass));
+      if (!rc) rc = launch_particle_gather(c, perm, p.n, p.vol0, 1, const_cast<double*>(q.vol0));
+      if (!rc) {
+        if (p.plastic) rc = launch_particle_gather(c, perm, p.n, p.plastic, 1, q.plastic);
+        else MPMRB_CUDA_OK(cudaMemsetAsync(q.plastic, 0, 8 * p.n, c.stream));
+      }
     }
+    if (!rc) rc = launch_gather_i64(c, perm, p.n, p.mid, const_cast<long long*>(q.mid));
     if (rc) return rc;
     if (cloth.ne > 0) {
       if (b_invperm.grow(4 * p.n) || b_qrole.grow(p.n) || b_qtau.grow(8 * 9 * p.n) ||
@@ -709,10 +744,18 @@ int Sim::end_step(mpmrb_step_stats* out, double* impulses_host) {
     // internal order -> the user's arrays (reference order)
     const int* perm = b_perm.as<int>();
     int rc = launch_particle_scatter(c, perm, p.n, q.x, 3, p.x);
-    if (!rc) rc = launch_particle_scatter(c, perm, p.n, q.v, 3, p.v);
-    if (!rc) rc = launch_particle_scatter(c, perm, p.n, q.f, 9, p.f);
-    if (!rc) rc = launch_particle_scatter(c, perm, p.n, q.c, 9, p.c);
-    if (!rc && p.plastic) rc = launch_particle_scatter(c, perm, p.n, q.plastic, 1, p.plastic);
+    if (prec == MPMRB_PREC_F32) {
+      if (!rc) rc = launch_particle_scatter_f32(c, perm, p.n, q32.v, 3, p.v);
+      if (!rc) rc = launch_particle_scatter_f32(c, perm, p.n, q32.f, 9, p.f);
+      if (!rc) rc = launch_particle_scatter_f32(c, perm, p.n, q32.c, 9, p.c);
+      if (!rc && p.plastic)
+        rc = launch_particle_scatter_f32(c, perm, p.n, q32.plastic, 1, p.plastic);
+    } else {
+      if (!rc) rc = launch_particle_scatter(c, perm, p.n, q.v, 3, p.v);
+      if (!rc) rc = launch_particle_scatter(c, perm, p.n, q.f, 9, p.f);
+      if (!rc) rc = launch_particle_scatter(c, perm, p.n, q.c, 9, p.c);
+      if (!rc && p.plastic) rc = launch_particle_scatter(c, perm, p.n, q.plastic, 1, p.plastic);
+    }
     if (rc) return rc;
   }
   if (p.n > 0) {

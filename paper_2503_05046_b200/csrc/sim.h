@@ -13,6 +13,8 @@ struct Sim {
   Ctx* ctx = nullptr;
   ParticlesDev p{};  // user arrays (reference order)
   ParticlesDev q{};  // sim-internal copy sorted by (block, cell), used by the substeps
+  ParticlesF32 q32{};  // its float32 layout (fp32 performance mode; x is q.x)
+  int prec = MPMRB_PREC_F64;
   bool have_particles = false;
   bool have_params = false;
   int nmat = 0;
@@ -47,6 +49,7 @@ struct Sim {
   DevBuf b_su_c, b_su_n, b_su_ent, b_cellsum, b_slots;
   // sorted particle state: x, v (3n) f, c (9n) mass, vol0, plastic (n) doubles; mid (n) int64
   DevBuf b_qd, b_qmid, b_perm, b_skeys, b_svals, b_cpart_user;
+  DevBuf b_qf;  // float32 particle state (fp32 mode): v 3n, f 9n, c 9n, mass, vol0, plastic n, tau 6n
   DevBuf b_react;  // per-CTA reaction partials
   // codimensional cloth (cloth.cu): mesh in user order + per-step internal views
   ClothDev cloth{};

@@ -124,7 +124,7 @@ def build_particles(scene):
     return particles, mesh
 
 
-def build_state(scene, particles=None, cloth=None) -> SimState:
+def build_state(scene, particles=None, cloth=None, precision: str = "f64") -> SimState:
     c = scene["contact"]
     s = scene["solver"]
     sp = SolverParams(eps_r=s.get("eps_r", 5e-2), max_iters=s.get("max_iters", 500))
@@ -136,7 +136,7 @@ def build_state(scene, particles=None, cloth=None) -> SimState:
                                     gravity=tuple(scene["gravity"])),
                     contact_params=ContactParams(stiffness=c["stiffness"], tau_d=c["tau_d"],
                                                  eps_v=c["eps_v"], margin=c.get("margin")),
-                    solver_params=sp, cloth=cloth)
+                    solver_params=sp, cloth=cloth, precision=precision)
 
 
 # ------------------------------------------------------------------ configs
