@@ -266,6 +266,13 @@ int mpmrb_contact_model(mpmrb_ctx* ctx, const double* vc, const double* phi,
                         const double* gamma_lag, const double* mu, int64_t n, double stiffness,
                         double tau_d, double eps_v, double dt, double* energy, double* grad,
                         double* hess);
+/* solver.py:224-256 solve_search_direction: d = -H^-1 g for n SPD 3x3 blocks
+ * h (n,3,3) and g (n,3), device arrays; blocks that fail the Cholesky are
+ * regularised like the reference.  *n_regularized_host counts them (the
+ * reference's warning); MPMRB_E_NONFINITE if any block is still not SPD after
+ * the last attempt (the reference's FloatingPointError).  Synchronises. */
+int mpmrb_search_direction(mpmrb_ctx* ctx, const double* h, const double* g, int64_t n,
+                           double* d, int32_t* n_regularized_host);
 /* geometry.py:162-169 query_signed_distance for one geom in its LOCAL frame. */
 int mpmrb_sdf_query(mpmrb_ctx* ctx, const mpmrb_geom* geom_host, const double* points,
                     int64_t n, double* phi, double* normal, double* witness);

@@ -371,6 +371,22 @@ int mpmrb_contact_model(mpmrb_ctx* c, const double* vc, const double* phi, const
   return c->check_status("contact_model");
 }
 
+int mpmrb_search_direction(mpmrb_ctx* c, const double* h, const double* g, int64_t n, double* d,
+                           int32_t* n_reg) {
+  CHECK_CTX(c);
+  if (c->scratch[SS_DIR].grow(64)) return MPMRB_E_CUDA;
+  int* reg = c->scratch[SS_DIR].as<int>();
+  int rc = launch_search_direction(*c, h, g, n, d, reg);
+  if (rc) return rc;
+  int hreg[2] = {0, 0};
+  MPMRB_CUDA_OK(cudaMemcpyAsync(hreg, reg, sizeof(hreg), cudaMemcpyDeviceToHost, c->stream));
+  rc = c->check_status("solve_search_direction");
+  if (rc) return rc;
+  if (n_reg) *n_reg = hreg[0];
+  if (hreg[1]) return set_error(MPMRB_E_NONFINITE, "Hessian block not SPD after regularization");
+  return MPMRB_OK;
+}
+
 int mpmrb_sdf_query(mpmrb_ctx* c, const mpmrb_geom* geom_host, const double* pts, int64_t n,
                     double* phi, double* normal, double* witness) {
   CHECK_CTX(c);

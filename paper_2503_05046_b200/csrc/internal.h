@@ -50,7 +50,8 @@ enum ScratchSlot {
   SS_SOLVER0, SS_SOLVER1, SS_SOLVER2, SS_SOLVER3, SS_SOLVER4, SS_SOLVER5, SS_SOLVER6,
   SS_SOLVER7, SS_SOLVER8, SS_MATS, SS_GEOMS, SS_PROBLEM, SS_HOSTINFO,
   // ordered (deterministic) scatter / P2G
-  SS_ORD_K, SS_ORD_I, SS_ORD_S, SS_ORD_N, SS_ORD_V, SS_ORD_O
+  SS_ORD_K, SS_ORD_I, SS_ORD_S, SS_ORD_N, SS_ORD_V, SS_ORD_O,
+  SS_DIR  // search-direction counters (mpmrb_search_direction)
 };
 
 inline unsigned grid_for(long long n, int threads) {

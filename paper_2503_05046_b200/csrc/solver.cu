@@ -1155,6 +1155,51 @@ __global__ void k_su_lists(const int* __restrict__ nd_dev, const int* __restrict
   }
 }
 
+// solver.py:224-256 solve_search_direction: d = -H^-1 g per 3x3 SPD block,
+// Cholesky in registers; a block that fails is regularised by +1e-12
+// max(tr H, 1) 10^attempt on the diagonal (cumulative, <= 3 times) exactly as
+// the reference's batch loop does for its bad blocks.  reg[0] counts the
+// regularised blocks (the reference's warning), reg[1] the blocks still not SPD
+// after the last attempt (its FloatingPointError).
+__global__ void k_search_direction(const double* __restrict__ hb, const double* __restrict__ g,
+                                   long long n, double* __restrict__ d, int* __restrict__ reg) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double* H = hb + 9 * i;
+    double h[6] = {H[0], H[4], H[8], H[3], H[6], H[7]};  // 00 11 22 10 20 21 (lower)
+    double l11 = 0, l21 = 0, l31 = 0, l22 = 0, l32 = 0, l33 = 0;
+    bool good = false;
+    for (int attempt = 0; attempt < 4; ++attempt) {
+      l11 = sqrt(h[0]);
+      l21 = h[3] / l11;
+      l31 = h[4] / l11;
+      l22 = sqrt(h[1] - l21 * l21);
+      l32 = (h[5] - l31 * l21) / l22;
+      l33 = sqrt(h[2] - l31 * l31 - l32 * l32);
+      good = isfinite(l11) && isfinite(l22) && isfinite(l33) && l11 > 0.0 && l22 > 0.0 &&
+             l33 > 0.0;
+      if (good || attempt == 3) break;
+      if (attempt == 0) atomicAdd(&reg[0], 1);
+      const double tr = h[0] + h[1] + h[2];
+      const double bump = 1e-12 * fmax(tr, 1.0) * (attempt == 0 ? 1.0 : (attempt == 1 ? 10.0 : 100.0));
+      h[0] += bump;
+      h[1] += bump;
+      h[2] += bump;
+    }
+    if (!good) atomicAdd(&reg[1], 1);
+    const double* gi = g + 3 * i;
+    const double y1 = -gi[0] / l11;
+    const double y2 = (-gi[1] - l21 * y1) / l22;
+    const double y3 = (-gi[2] - l31 * y1 - l32 * y2) / l33;
+    const double x3 = y3 / l33;
+    const double x2 = (y2 - l32 * x3) / l22;
+    const double x1 = (y1 - l21 * x2 - l31 * x3) / l11;
+    d[3 * i] = x1;
+    d[3 * i + 1] = x2;
+    d[3 * i + 2] = x3;
+  }
+}
+
 unsigned su_grid(long long cap) {
   long long b = (cap + kSetupThreads - 1) / kSetupThreads;
   if (b < 1) b = 1;
@@ -1201,6 +1246,16 @@ int launch_solver_setup(Ctx& c, const int* nd_dev, const int* nc_dev, long long 
   if (rc) return rc;
   k_su_lists<<<su_grid(nd_cap + 1), kSetupThreads, 0, c.stream>>>(
       nd_dev, su.flag, su.flag_off, su.off_exp, su.cn, su.cn_rec, su.fn);
+  c.launches++;
+  MPMRB_CUDA_OK(cudaGetLastError());
+  return MPMRB_OK;
+}
+
+int launch_search_direction(Ctx& c, const double* h, const double* g, long long n, double* d,
+                            int* reg) {
+  MPMRB_CUDA_OK(cudaMemsetAsync(reg, 0, 2 * sizeof(int), c.stream));
+  if (n == 0) return MPMRB_OK;
+  k_search_direction<<<su_grid(n), kSetupThreads, 0, c.stream>>>(h, g, n, d, reg);
   c.launches++;
   MPMRB_CUDA_OK(cudaGetLastError());
   return MPMRB_OK;

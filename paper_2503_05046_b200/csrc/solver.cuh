@@ -116,5 +116,8 @@ int launch_solver_setup(Ctx& c, const int* nd_dev, const int* nc_dev, long long 
                         long long nc_cap, const int* cnodes, const SolverSetup& su,
                         DevBuf& tiles);
 int launch_qn_solve(Ctx& c, const SolverArgs& a, int grid_ctas);
+// solver.py:224-256 (reg[2] device: regularised blocks, blocks still not SPD)
+int launch_search_direction(Ctx& c, const double* h, const double* g, long long n, double* d,
+                            int* reg);
 
 }  // namespace mpmrb

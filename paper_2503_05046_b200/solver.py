@@ -109,12 +109,95 @@ class ContactProblem:
             return _lib.zeros((0, 3))
         return _contact_velocities_raw(self.nodes, self.w, self.frames, self.bias, v)
 
-    def impulses(self, v) -> torch.Tensor:
+    def impulses(self, v, vc=None) -> torch.Tensor:
         from .contact_model import contact_impulses
         if self.n_contacts == 0:
             return _lib.zeros((0, 3))
-        return contact_impulses(self.contact_velocities(v), self.phi, self.gamma_lag, self.mu,
+        vc = self.contact_velocities(v) if vc is None else _lib.as_dev(vc)
+        return contact_impulses(vc, self.phi, self.gamma_lag, self.mu, self.contact_params,
+                                self.dt)
+
+    # ---- the reference's host-side building blocks of the solve
+    # (solver.py:111-194), on the device: contact velocities, the contact model
+    # and the ordered scatter are this package's kernels.  The fused solve
+    # (k_qn_solve) evaluates the same quantities inside one kernel; these are
+    # the API-level equivalents for callers of the reference's ContactProblem.
+
+    def energy(self, v, vc=None) -> float:
+        """solver.py:111-119: 1/2 |v - v*|_M^2 + sum of contact energies."""
+        from .contact_model import contact_energy
+        v = _lib.as_dev(v)
+        dv = v - self.v_star
+        e = 0.5 * float(torch.sum(self.m[:, None] * dv * dv))
+        if self.n_contacts:
+            vc = self.contact_velocities(v) if vc is None else _lib.as_dev(vc)
+            e += float(torch.sum(contact_energy(vc, self.phi, self.gamma_lag, self.mu,
+                                                self.contact_params, self.dt)))
+        return e
+
+    def _scatter_contact(self, vals) -> torch.Tensor:
+        from .transfer import scatter_reduce
+        return scatter_reduce(self.nodes, vals.contiguous(), int(self.m.shape[0]), self.plan,
+                              self.epoch, mode=self.mode, workers=self.workers,
+                              particle_ids=self.particle_ids)
+
+    def gradient(self, v, vc=None):
+        """solver.py:127-140: (total gradient, contact part J^T dl/dv_c)."""
+        from .contact_model import contact_gradient
+        v = _lib.as_dev(v)
+        g = self.m[:, None] * (v - self.v_star)
+        if self.n_contacts == 0:
+            return g, torch.zeros_like(g)
+        vc = self.contact_velocities(v) if vc is None else _lib.as_dev(vc)
+        g_c = contact_gradient(vc, self.phi, self.gamma_lag, self.mu, self.contact_params,
+                               self.dt)
+        g_world = torch.einsum("ci,cij->cj", g_c, self.frames)  # R^T g_c per contact
+        jt = self._scatter_contact(self.w[:, :, None] * g_world[:, None, :])
+        return g + jt, jt
+
+    def hessian_blocks(self, v, vc=None) -> torch.Tensor:
+        """solver.py:151-167: m_i I + sum_c w_ic^2 R^T G R, (nd, 3, 3)."""
+        from .contact_model import contact_hessian
+        h = torch.diag_embed(self.m[:, None].expand(-1, 3).contiguous())
+        if self.n_contacts == 0:
+            return h
+        v = _lib.as_dev(v)
+        vc = self.contact_velocities(v) if vc is None else _lib.as_dev(vc)
+        big_g = contact_hessian(vc, self.phi, self.gamma_lag, self.mu, self.contact_params,
+                                self.dt)
+        rgr = self.frames.transpose(1, 2) @ big_g @ self.frames
+        vals = (self.w * self.w)[:, :, None] * rgr.reshape(-1, 1, 9)
+        return h + self._scatter_contact(vals).reshape(-1, 3, 3)
+
+    def dense_hessian(self, v) -> torch.Tensor:
+        """solver.py:169-186: the full (3nd, 3nd) Hessian with cross-node
+        coupling (oracle use; O(nd^2) memory)."""
+        from .contact_model import contact_hessian
+        nd = int(self.m.shape[0])
+        h = torch.diag(self.m.repeat_interleave(3))
+        if self.n_contacts == 0:
+            return h
+        v = _lib.as_dev(v)
+        big_g = contact_hessian(self.contact_velocities(v), self.phi, self.gamma_lag, self.mu,
                                 self.contact_params, self.dt)
+        rgr = torch.einsum("cki,ckl,clj->cij", self.frames, big_g, self.frames)
+        ww = self.w[:, :, None] * self.w[:, None, :]                      # (nc, 27, 27)
+        blocks = ww[:, :, :, None, None] * rgr[:, None, None, :, :]       # (nc, 27, 27, 3, 3)
+        rows = (3 * self.nodes[:, :, None] + torch.arange(3, device=h.device)).reshape(-1, 81)
+        vals = blocks.permute(0, 1, 3, 2, 4).reshape(-1, 81, 81)
+        flat = h.view(-1)
+        idx = rows[:, :, None] * (3 * nd) + rows[:, None, :]
+        flat.index_put_((idx.reshape(-1),), vals.reshape(-1), accumulate=True)
+        return h
+
+    def residual_threshold(self, v, g, g_contact, params: "SolverParams"):
+        """solver.py:188-194: (||g||_M^-1, eps_a + eps_r max(||v||_M, ||J^T dl||_M^-1))."""
+        v, g, gc = _lib.as_dev(v), _lib.as_dev(g), _lib.as_dev(g_contact)
+        inv_m = 1.0 / self.m
+        residual = float(torch.sqrt(torch.sum(g * g * inv_m[:, None])))
+        p_norm = float(torch.sqrt(torch.sum(self.m[:, None] * v * v)))
+        j_norm = float(torch.sqrt(torch.sum(gc * gc * inv_m[:, None])))
+        return residual, params.eps_a + params.eps_r * max(p_norm, j_norm)
 
     def to_struct(self) -> _lib.Problem:
         p = _lib.Problem()
@@ -182,6 +265,79 @@ def line_search(deriv, max_iters: int = 50, tol: float = 1e-8) -> LineSearchResu
             cand = 2.0 * max(a, 1e-8)
         a = cand
     return LineSearchResult(alpha=lo if lo > 0.0 else a, evals=max_iters, derivative=d)
+
+
+def solve_search_direction(h_blocks, g) -> torch.Tensor:
+    """solver.py:224-256: d = -H^-1 g per SPD 3x3 block (device Cholesky,
+    csrc/solver.cu k_search_direction), regularising near-singular blocks like
+    the reference; FloatingPointError if one stays non-SPD."""
+    h = _lib.as_dev(h_blocks).reshape(-1, 3, 3).contiguous()
+    gg = _lib.as_dev(g).reshape(-1, 3).contiguous()
+    d = _lib.empty(tuple(gg.shape))
+    nreg = C.c_int32(0)
+    _lib.check(_lib.lib().mpmrb_search_direction(_lib.ctx(), _lib.ptr(h), _lib.ptr(gg),
+                                                 h.shape[0], _lib.ptr(d), C.byref(nreg)))
+    if nreg.value:
+        log.warning("regularizing %d near-singular Hessian blocks", nreg.value)
+    return d
+
+
+def _directional_derivatives(problem: ContactProblem, v, dv, vc0):
+    """solver.py:301-325: phi'(a), phi''(a) along dv (device contact model)."""
+    from .contact_model import contact_grad_hess
+    mdv = problem.m[:, None] * dv
+    a1 = float(torch.sum((v - problem.v_star) * mdv))
+    a2 = float(torch.sum(dv * mdv))
+    dvc = None
+    if problem.n_contacts:
+        dv_p = torch.einsum("ck,ckd->cd", problem.w, dv[problem.nodes])
+        dvc = torch.einsum("cij,cj->ci", problem.frames, dv_p)
+
+    def deriv(alpha: float):
+        d, dd = a1 + a2 * alpha, a2
+        if dvc is not None:
+            g_c, big_g = contact_grad_hess(vc0 + alpha * dvc, problem.phi, problem.gamma_lag,
+                                           problem.mu, problem.contact_params, problem.dt)
+            d += float(torch.sum(g_c * dvc))
+            dd += float(torch.sum(dvc * torch.einsum("cij,cj->ci", big_g, dvc)))
+        return d, dd
+
+    return deriv
+
+
+def dense_newton_oracle(problem: ContactProblem, params: SolverParams, v0=None):
+    """solver.py:385-389: full-Hessian Newton with the reference's test-last
+    loop and exact line search (solver.py:328-365), driven from the host over
+    device arrays -- a test oracle, O((3nd)^3) per iteration."""
+    v = (problem.v_init if v0 is None else _lib.as_dev(v0)).clone()
+    report = SolveReport(n_contacts=problem.n_contacts, n_dofs=problem.n_dofs)
+    vc = problem.contact_velocities(v) if problem.n_contacts else None
+    g, g_c = problem.gradient(v, vc)
+    residual, threshold = problem.residual_threshold(v, g, g_c, params)
+    report.objective_trace.append(problem.energy(v, vc))
+    report.residual_trace.append(residual)
+    report.threshold_trace.append(threshold)
+    for it in range(params.max_iters):
+        if residual < (threshold if it > 0 else params.eps_a):
+            report.converged = True
+            break
+        dv = torch.linalg.solve(problem.dense_hessian(v), -g.reshape(-1)).reshape(-1, 3)
+        ls = line_search(_directional_derivatives(problem, v, dv, vc),
+                         max_iters=params.ls_max_iters, tol=params.ls_tol)
+        v = v + ls.alpha * dv
+        report.iterations += 1
+        report.alpha_trace.append(ls.alpha)
+        vc = problem.contact_velocities(v) if problem.n_contacts else None
+        g, g_c = problem.gradient(v, vc)
+        residual, threshold = problem.residual_threshold(v, g, g_c, params)
+        report.objective_trace.append(problem.energy(v, vc))
+        report.residual_trace.append(residual)
+        report.threshold_trace.append(threshold)
+    else:
+        report.converged = residual < threshold
+    if not bool(torch.isfinite(v).all()):
+        raise FloatingPointError("contact solve produced non-finite velocities")
+    return v, problem.impulses(v, vc), report
 
 
 def quasi_newton_solve(problem: ContactProblem, params: SolverParams, v0=None):

@@ -149,3 +149,18 @@ def scatter_reduce(node_ids, values, n_out: int, plan: SortPlan, epoch: int,
         stats.merges_performed = touched
         stats.nodes_touched = touched
     return out[:, 0] if squeeze else out
+
+
+def scatter_naive(node_ids, values, n_out: int) -> torch.Tensor:
+    """transfer.py:251-260's per-contribution baseline: on the GPU, one float64
+    atomic per contribution (summation order unspecified)."""
+    vals = _lib.as_dev(values)
+    ids = _lib.as_dev(node_ids, torch.int64)
+    squeeze = vals.dim() == 2
+    if squeeze:
+        vals = vals[..., None].contiguous()
+    rows, k, nch = vals.shape
+    out = torch.empty((n_out, nch), dtype=torch.float64, device=vals.device)
+    _lib.check(_lib.lib().mpmrb_scatter_reduce(_lib.ctx(), _lib.ptr(ids), _lib.ptr(vals), rows, k,
+                                               nch, n_out, _lib.ptr(out)))
+    return out[:, 0] if squeeze else out
