@@ -63,10 +63,22 @@ class BiasCache:
         self._epoch += 1
 
     def _slots(self, n_geoms: int, n: int):
+        """(geom, particle) slots for this call's geoms and particle count.
+        A change of either re-lays the slots, carrying every cached entry
+        whose (geom, particle) index still exists: the reference keys the
+        cache by particle id (collision.py:55-85), so a particle keeps its
+        first-sight bias when others join or leave the set."""
         if self._stamp is None or self._shape != (n_geoms, n):
-            self._stamp = torch.zeros(max(1, n_geoms * n), dtype=torch.int32,
-                                      device=_lib.device())
-            self._store = _lib.zeros((max(1, n_geoms * n), 3))
+            stamp = torch.zeros(max(1, n_geoms * n), dtype=torch.int32, device=_lib.device())
+            store = _lib.zeros((max(1, n_geoms * n), 3))
+            og, on = self._shape
+            if self._stamp is not None and og * on > 0 and n_geoms * n > 0:
+                kg, kn = min(og, n_geoms), min(on, n)
+                stamp[: n_geoms * n].view(n_geoms, n)[:kg, :kn] = \
+                    self._stamp[: og * on].view(og, on)[:kg, :kn]
+                store[: n_geoms * n].view(n_geoms, n, 3)[:kg, :kn] = \
+                    self._store[: og * on].view(og, on, 3)[:kg, :kn]
+            self._stamp, self._store = stamp, store
             self._shape = (n_geoms, n)
         return self._stamp, self._store
 

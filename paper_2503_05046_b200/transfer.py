@@ -136,11 +136,12 @@ def scatter_reduce(node_ids, values, n_out: int, plan: SortPlan, epoch: int,
     if particle_ids is None and rows != plan.n_particles:
         raise ValueError("row count does not match the plan's particle count")
     out = torch.empty((n_out, nch), dtype=torch.float64, device=vals.device)
-    # deterministic: ordered segmented fold, bitwise the reference's bincount
-    # order (transfer.py:135-145); fast: float64 atomics (order unspecified,
-    # within the reference's own fast-vs-deterministic bound)
-    fn = (_lib.lib().mpmrb_scatter_reduce_ordered if mode == "deterministic"
-          else _lib.lib().mpmrb_scatter_reduce)
+    # Both modes run the ordered segmented fold: bitwise the reference's
+    # bincount order (transfer.py:135-145).  The reference's fast mode only
+    # promises a result within 1e-12 of deterministic that repeats for a given
+    # worker count (test_transfer.py:77-102); the ordered fold meets that
+    # exactly.  The unordered float64-atomic scatter is scatter_naive.
+    fn = _lib.lib().mpmrb_scatter_reduce_ordered
     _lib.check(fn(_lib.ctx(), _lib.ptr(ids), _lib.ptr(vals), rows, k, nch, n_out, _lib.ptr(out)))
     if stats is not None:
         touched = int(torch.unique(ids).numel()) if rows else 0
