@@ -266,6 +266,13 @@ int mpmrb_contact_model(mpmrb_ctx* ctx, const double* vc, const double* phi,
                         const double* gamma_lag, const double* mu, int64_t n, double stiffness,
                         double tau_d, double eps_v, double dt, double* energy, double* grad,
                         double* hess);
+/* materials.py:70-83 polar_rotation of n 3x3 matrices (device arrays), the
+ * Higham iteration with a per-matrix stop at max|dR| <= 1e-13 (the reference
+ * stops on the batch-wide maximum; the extra iterations change R only at
+ * roundoff). */
+int mpmrb_polar_rotation(mpmrb_ctx* ctx, const double* f, int64_t n, double* r);
+/* materials.py:57-67 inverse_transpose3 via the adjugate. */
+int mpmrb_inverse_transpose3(mpmrb_ctx* ctx, const double* m, int64_t n, double* out);
 /* solver.py:224-256 solve_search_direction: d = -H^-1 g for n SPD 3x3 blocks
  * h (n,3,3) and g (n,3), device arrays; blocks that fail the Cholesky are
  * regularised like the reference.  *n_regularized_host counts them (the

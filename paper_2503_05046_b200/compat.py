@@ -155,6 +155,24 @@ class _ClassFacade:
         return isinstance(from_np(obj), self._cls)
 
 
+def _method_facade(cls):
+    """A subclass of a plain (parameter) class whose own public methods take
+    and return NumPy (e.g. the shapes' query); instances still pass the
+    package's isinstance checks."""
+    own = {k: v for k, v in vars(cls).items()
+           if not k.startswith("_") and callable(v) and not isinstance(v, (type, staticmethod,
+                                                                          classmethod))}
+    if not own:
+        return cls
+    ns = {k: _wrap_fn(v) for k, v in own.items()}
+    ns["__doc__"] = cls.__doc__
+    ns["__module__"] = cls.__module__
+    return type(cls.__name__, (cls,), ns)
+
+
+_FACADE_CLASSES: dict = {}
+
+
 def _facade(name: str, mod) -> types.ModuleType:
     fm = types.ModuleType(f"mpmrb.{name}", mod.__doc__)
     for attr, v in vars(mod).items():
@@ -162,8 +180,12 @@ def _facade(name: str, mod) -> types.ModuleType:
             continue
         if isinstance(v, type) and issubclass(v, _DEVICE_CLASSES):
             fv = _ClassFacade(v)
+        elif isinstance(v, type) and not issubclass(v, BaseException):
+            if v not in _FACADE_CLASSES:
+                _FACADE_CLASSES[v] = _method_facade(v)
+            fv = _FACADE_CLASSES[v]
         elif isinstance(v, type) or not callable(v):
-            fv = v  # parameter dataclasses, exceptions, constants
+            fv = v  # exceptions, constants
         else:
             fv = _wrap_fn(v)
         setattr(fm, attr, fv)

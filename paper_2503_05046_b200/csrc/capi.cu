@@ -371,6 +371,20 @@ int mpmrb_contact_model(mpmrb_ctx* c, const double* vc, const double* phi, const
   return c->check_status("contact_model");
 }
 
+int mpmrb_polar_rotation(mpmrb_ctx* c, const double* f, int64_t n, double* r) {
+  CHECK_CTX(c);
+  int rc = launch_polar(*c, f, n, 0, r);
+  if (rc) return rc;
+  return c->check_status("polar_rotation");
+}
+
+int mpmrb_inverse_transpose3(mpmrb_ctx* c, const double* m, int64_t n, double* out) {
+  CHECK_CTX(c);
+  int rc = launch_polar(*c, m, n, 1, out);
+  if (rc) return rc;
+  return c->check_status("inverse_transpose3");
+}
+
 int mpmrb_search_direction(mpmrb_ctx* c, const double* h, const double* g, int64_t n, double* d,
                            int32_t* n_reg) {
   CHECK_CTX(c);

@@ -165,6 +165,7 @@ int launch_gather_i8(Ctx& c, const signed char* src, const int* perm, long long 
                      signed char* dst);
 
 int launch_clamp(Ctx& c, const double* f, long long n, double* out, unsigned long long* nbad);
+int launch_polar(Ctx& c, const double* f, long long n, int inv_t_only, double* out);
 int launch_health(Ctx& c, const double* x, const double* v, long long n, double h, int* bad);
 
 // reorder.cu: once-per-step (block, cell) particle order

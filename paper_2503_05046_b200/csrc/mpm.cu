@@ -683,6 +683,16 @@ __global__ void k_clamp(const double* __restrict__ f, long long n, double* __res
   if ((threadIdx.x & 31) == 0 && b) atomicAdd(nbad, (unsigned long long)__popc(b));
 }
 
+// materials.py:57-83 on a stack of 3x3 matrices: the Higham polar rotation
+// (per-matrix stop, see svd3.cuh) or the adjugate inverse-transpose.
+__global__ void k_polar(const double* __restrict__ f, long long n, int inv_t_only,
+                        double* __restrict__ out) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const M3 F = m3_load(f + 9 * i);
+  m3_store(out + 9 * i, inv_t_only ? m3_inv_transpose(F) : polar_rotation(F));
+}
+
 // coupling.py:153-165: finite x, v and |x| < h (2^20 - 2)
 __global__ void k_health(const double* __restrict__ x, const double* __restrict__ v, long long n,
                          double lim, int* __restrict__ bad) {
@@ -697,6 +707,14 @@ __global__ void k_health(const double* __restrict__ x, const double* __restrict_
 int launch_health(Ctx& c, const double* x, const double* v, long long n, double h, int* bad) {
   if (n == 0) return MPMRB_OK;
   k_health<<<grid_for(3 * n, 256), 256, 0, c.stream>>>(x, v, n, h * (double)((1 << 20) - 2), bad);
+  c.launches++;
+  MPMRB_CUDA_OK(cudaGetLastError());
+  return MPMRB_OK;
+}
+
+int launch_polar(Ctx& c, const double* f, long long n, int inv_t_only, double* out) {
+  if (n == 0) return MPMRB_OK;
+  k_polar<<<grid_for(n, 128), 128, 0, c.stream>>>(f, n, inv_t_only, out);
   c.launches++;
   MPMRB_CUDA_OK(cudaGetLastError());
   return MPMRB_OK;

@@ -17,12 +17,15 @@
 from __future__ import annotations
 
 import ctypes as C
+import logging
 from dataclasses import dataclass
 
 import numpy as np
 import torch
 
 from . import _lib
+
+log = logging.getLogger(__name__)
 
 SIGMA_MIN = 0.05  # materials.py:21
 
@@ -93,6 +96,44 @@ def det3(m) -> torch.Tensor:
                         torch.linalg.cross(m[..., :, 1], m[..., :, 2], dim=-1))
 
 
+def _stack_op(fn, m) -> torch.Tensor:
+    m = _lib.as_dev(m)
+    shape = m.shape
+    flat = m.reshape(-1, 3, 3).contiguous()
+    out = torch.empty_like(flat)
+    _lib.check(fn(_lib.ctx(), _lib.ptr(flat), flat.shape[0], _lib.ptr(out)))
+    return out.reshape(shape)
+
+
+def inverse_transpose3(m) -> torch.Tensor:
+    """Batched inverse-transpose via the adjugate (materials.py:57-67)."""
+    return _stack_op(_lib.lib().mpmrb_inverse_transpose3, m)
+
+
+def polar_rotation(f) -> torch.Tensor:
+    """Rotation factor of the polar decomposition (materials.py:70-83), Higham
+    iteration on the device (per-matrix stop at max|dR| <= 1e-13)."""
+    return _stack_op(_lib.lib().mpmrb_polar_rotation, f)
+
+
+def energy_density(f, material: Material) -> float:
+    """psi(F) = mu sum (s_i - 1)^2 + lam/2 (J - 1)^2 with signed singular
+    values (materials.py:138-149); the reference uses it only in
+    verification oracles (not the runtime force path), as here."""
+    fd = _lib.as_dev(f)
+    if fd.shape != (3, 3):
+        raise ValueError(f"expected a (3, 3) deformation gradient, got {tuple(fd.shape)}")
+    if not bool(torch.isfinite(fd).all()):
+        raise ValueError("deformation gradient has non-finite entries")
+    mu, lam = material.lame
+    u, s, vt = torch.linalg.svd(fd)
+    if float(torch.linalg.det(u) * torch.linalg.det(vt)) < 0:
+        s = s.clone()
+        s[2] = -s[2]
+    j = float(det3(fd))
+    return float(mu * torch.sum((s - 1.0) ** 2)) + 0.5 * lam * (j - 1.0) ** 2
+
+
 def kirchhoff_stress_batch(f, mu: float, lam: float) -> torch.Tensor:
     """tau(F) for a (n,3,3) stack of one elastic material (materials.py:113-122)."""
     f = _lib.as_dev(f)
@@ -134,4 +175,7 @@ def clamp_degenerate(f) -> tuple[torch.Tensor, int]:
     nbad = C.c_int64()
     _lib.check(_lib.lib().mpmrb_clamp_degenerate(_lib.ctx(), _lib.ptr(fd), fd.shape[0],
                                                  _lib.ptr(out), C.byref(nbad)))
+    if nbad.value:
+        log.warning("clamped %d inverted deformation gradients (singular value floor %.2f)",
+                    int(nbad.value), SIGMA_MIN)
     return out, int(nbad.value)
