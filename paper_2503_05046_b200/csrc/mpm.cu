@@ -162,6 +162,35 @@ __device__ __forceinline__ void p2g_scatter_one(const GridDev& g, const Stencil1
 // ~18x fewer global atomics than the per-particle scatter (27 x 7 per
 // particle), which remains the fallback for warps whose particles are spread.
 constexpr int kP2GThreads = 128;
+// per-particle P2G record in shared memory (affine form, see k_p2g step 4):
+// m, pad | A (3), Bf (3) | G (9) | K (9) | 1-D weights wx, wy, wz (9) | pad
+constexpr int kPayM = 0, kPayA = 2, kPayB = 5, kPayG = 8, kPayK = 17, kPayW = 26;
+constexpr int kPayStride = 36;
+
+// the record's first kPayW entries (everything but the weights) with 16 B
+// shared-memory loads
+template <class T>
+__device__ __forceinline__ void load_payload(const T* rec, T (&q)[kPayW]) {
+  if constexpr (sizeof(T) == 8) {
+#pragma unroll
+    for (int k = 0; k < kPayW / 2; ++k) {
+      const double2 d2 = reinterpret_cast<const double2*>(rec)[k];
+      q[2 * k] = d2.x;
+      q[2 * k + 1] = d2.y;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < kPayW / 4; ++k) {
+      const float4 f4 = reinterpret_cast<const float4*>(rec)[k];
+      q[4 * k] = f4.x;
+      q[4 * k + 1] = f4.y;
+      q[4 * k + 2] = f4.z;
+      q[4 * k + 3] = f4.w;
+    }
+#pragma unroll
+    for (int k = (kPayW / 4) * 4; k < kPayW; ++k) q[k] = rec[k];
+  }
+}
 constexpr int kWarpTile = 128;  // nodes per warp tile (e.g. 4 x 4 x 8)
 
 // Per-particle P2G payload: m, m v, m C, S = -dt D^-1 V0 tau and the external
@@ -280,8 +309,8 @@ __global__ void __launch_bounds__(kP2GThreads, MPMRB_P2G_MINB) k_p2g(GridDev g, 
                                                      double* __restrict__ mom_force,
                                                      DevStatus* st) {
   __shared__ double s_tile[kP2GThreads / 32][7][kWarpTile];
-  __shared__ T s_pay[kP2GThreads / 32][37][16];  // 16 particles' payloads
-  __shared__ int s_cell[kP2GThreads / 32][3][16];  // their cells in the tile
+  __shared__ __align__(16) T s_pay[kP2GThreads / 32][16][kPayStride];  // 16 particles' payloads
+  __shared__ int4 s_cell[kP2GThreads / 32][16];  // their cells in the tile
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const long long w0 = ((long long)blockIdx.x * kP2GThreads) + wid * 32;
   if (w0 >= p.n) return;
@@ -342,12 +371,15 @@ __global__ void __launch_bounds__(kP2GThreads, MPMRB_P2G_MINB) k_p2g(GridDev g, 
   // to node (cell_p + offset_k).  One particle's 27 slots are 27 distinct
   // nodes, so the tile updates need neither atomics nor a reduction, and each
   // node's sum runs in particle order (deterministic).  The payloads travel
-  // through shared memory in two halves of 16 particles.
+  // through shared memory in two halves of 16 particles, one contiguous
+  // record per particle (vector loads), in affine form: with the slot offset
+  // o and dpos = (o - fx) h,
+  //   m v + mC dpos = A + G o,   S dpos + dt f = Bf + K o,
+  // G = h mC, K = h S, A = m v - G fx, Bf = dt f - K fx  (mpm.py:89-93).
   const int ox = lane / 9, oy = (lane / 3) % 3, oz = lane % 3;
+  const T oxT = T(ox), oyT = T(oy), ozT = T(oz);
   const bool slot_lane = lane < 27;
-  T (*pay)[16] = s_pay[wid];
   const int n_live = (int)min((long long)32, p.n - w0);
-  const T hT = (T)h;
   T acc[7];
   int q_run = -1;  // node of the particle run being summed in acc
 #pragma unroll 1
@@ -356,22 +388,27 @@ __global__ void __launch_bounds__(kP2GThreads, MPMRB_P2G_MINB) k_p2g(GridDev g, 
     if (p0 >= n_live) break;
     __syncwarp();
     if ((lane >> 4) == half) {
-      const int r = lane & 15;
-      pay[0][r] = m;
+      T* rec = s_pay[wid][lane & 15];
+      const T hT = (T)h;
+      T G[9], K[9];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) {
+        G[k] = hT * mC.a[k];
+        K[k] = hT * S.a[k];
+      }
+      rec[kPayM] = m;
 #pragma unroll
       for (int d = 0; d < 3; ++d) {
-        pay[1 + d][r] = mv[d];
-        pay[4 + d][r] = fi[d];
-        pay[7 + d][r] = s.fx[d];
+        rec[kPayA + d] = mv[d] - (G[3 * d] * s.fx[0] + G[3 * d + 1] * s.fx[1] + G[3 * d + 2] * s.fx[2]);
+        rec[kPayB + d] = fi[d] - (K[3 * d] * s.fx[0] + K[3 * d + 1] * s.fx[1] + K[3 * d + 2] * s.fx[2]);
       }
 #pragma unroll
       for (int k = 0; k < 9; ++k) {
-        pay[10 + k][r] = mC.a[k];
-        pay[19 + k][r] = S.a[k];
-        pay[28 + k][r] = s.w[k / 3][k % 3];
+        rec[kPayG + k] = G[k];
+        rec[kPayK + k] = K[k];
+        rec[kPayW + k] = s.w[k / 3][k % 3];
       }
-#pragma unroll
-      for (int a = 0; a < 3; ++a) s_cell[wid][a][r] = cb[a];
+      s_cell[wid][lane & 15] = make_int4(cb[0], cb[1], cb[2], 0);
     }
     __syncwarp();
     if (slot_lane) {
@@ -382,23 +419,22 @@ __global__ void __launch_bounds__(kP2GThreads, MPMRB_P2G_MINB) k_p2g(GridDev g, 
       const int pend = min(16, n_live - p0);
 #pragma unroll 1
       for (int r = 0; r < pend; ++r) {
-        const T pm = pay[0][r];
-        const T dx = (T(ox) - pay[7][r]) * hT, dy = (T(oy) - pay[8][r]) * hT,
-                dz = (T(oz) - pay[9][r]) * hT;
-        const T w = (pay[28 + ox][r] * pay[31 + oy][r]) * pay[34 + oz][r];
+        const T* rec = s_pay[wid][r];
+        T q[kPayW];
+        load_payload<T>(rec, q);
+        const T w = (rec[kPayW + ox] * rec[kPayW + 3 + oy]) * rec[kPayW + 6 + oz];
         T v[7];
-        v[0] = w * pm;
+        v[0] = w * q[kPayM];
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
-          const T aa = pay[1 + d][r] +
-                       (pay[10 + 3 * d][r] * dx + pay[11 + 3 * d][r] * dy + pay[12 + 3 * d][r] * dz);
-          const T bb = pay[19 + 3 * d][r] * dx + pay[20 + 3 * d][r] * dy + pay[21 + 3 * d][r] * dz;
-          v[1 + d] = w * aa;
-          v[4 + d] = w * (bb + pay[4 + d][r]);
+          const T* g = q + kPayG + 3 * d;
+          const T* k = q + kPayK + 3 * d;
+          v[1 + d] = w * (q[kPayA + d] + (g[0] * oxT + g[1] * oyT + g[2] * ozT));
+          v[4 + d] = w * (q[kPayB + d] + (k[0] * oxT + k[1] * oyT + k[2] * ozT));
         }
-        const int q = ((s_cell[wid][0][r] + ox) * ny + (s_cell[wid][1][r] + oy)) * nz +
-                      (s_cell[wid][2][r] + oz);
-        if (q != q_run) {
+        const int4 cr = s_cell[wid][r];
+        const int qn = ((cr.x + ox) * ny + (cr.y + oy)) * nz + (cr.z + oz);
+        if (qn != q_run) {
           // the run changes on every slot lane at once (the cell changed)
           __syncwarp(0x07ffffffu);
           if (q_run >= 0)
@@ -406,7 +442,7 @@ __global__ void __launch_bounds__(kP2GThreads, MPMRB_P2G_MINB) k_p2g(GridDev g, 
             for (int ch = 0; ch < 7; ++ch) tile[ch][q_run] += (double)acc[ch];
 #pragma unroll
           for (int ch = 0; ch < 7; ++ch) acc[ch] = v[ch];
-          q_run = q;
+          q_run = qn;
         } else {
 #pragma unroll
           for (int ch = 0; ch < 7; ++ch) acc[ch] += v[ch];
