@@ -6,6 +6,8 @@
 // once as a CUDA graph and replayed N times per coupling step with no host
 // synchronisation.  The host (coupling.py's scheduler) only syncs once per
 // step, in mpmrb_sim_end_step.
+#include <nvtx3/nvToolsExt.h>
+
 #include <cstring>
 #include <vector>
 
@@ -20,6 +22,11 @@ namespace mpmrb {
 namespace {
 
 constexpr int kMaxBodies = 32;
+
+struct NvtxRange {  // host-side range for nsys / ncu --nvtx
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 __global__ void k_emit_active(long long n_cap, const unsigned char* __restrict__ active,
                               const int* __restrict__ woff, const double* __restrict__ mass,
@@ -508,8 +515,17 @@ int Sim::capture_or_launch() {
   return MPMRB_OK;
 }
 
+// Stage boundaries: CUDA events for bench.py's live per-stage timing (direct
+// launches), and NVTX ranges named after the pipeline stages (nsys / ncu
+// --nvtx; while a graph is captured they bracket the capture).
 void Sim::mark(int k) {
+  static const char* kStage[kProfEvents - 1] = {"mpmrb grid build", "mpmrb P2G",
+                                                "mpmrb grid update", "mpmrb contacts",
+                                                "mpmrb contact solve", "mpmrb reactions",
+                                                "mpmrb G2P"};
   if (prof_on) cudaEventRecord(prof_ev[k], ctx->stream);
+  if (k > 0) nvtxRangePop();
+  if (k < kProfEvents - 1) nvtxRangePushA(kStage[k]);
 }
 
 // One substep with direct launches and events between the pipeline stages
@@ -538,6 +554,7 @@ int Sim::profile_substep(float* stage_ms, int* sizes) {
 }
 
 int Sim::begin_step(long long epoch, int n_substeps) {
+  NvtxRange r("mpmrb begin_step");
   Ctx& c = *ctx;
   if (!have_particles) return set_error(MPMRB_E_INVALID, "sim: particles not set");
   if (!have_params) return set_error(MPMRB_E_INVALID, "sim: params not set");
@@ -723,12 +740,14 @@ int Sim::substep() {
       return capture_or_launch();
     }
   }
+  NvtxRange r("mpmrb substep (graph)");
   MPMRB_CUDA_OK(cudaGraphLaunch(graph_exec, c.stream));
   c.launches += kernels_per_substep;
   return MPMRB_OK;
 }
 
 int Sim::end_step(mpmrb_step_stats* out, double* impulses_host) {
+  NvtxRange r("mpmrb end_step");
   Ctx& c = *ctx;
   std::vector<SubstepStat> st(steps_substeps > 0 ? steps_substeps : 1);
   unsigned long long misc[4] = {0, 0, 0, 0};
