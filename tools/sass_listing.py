@@ -28,7 +28,13 @@ def short(mangled: str) -> str:
     m = re.search(r"(k_[a-z0-9_]+?)(?:I|E|$)", mangled.split("_cu_")[-1] if "_cu_" in mangled
                   else mangled)
     name = m.group(1) if m else mangled
-    return re.sub(r"^\d+", "", name)
+    name = re.sub(r"^\d+", "", name)
+    tail = mangled.split(name, 1)[-1] if name in mangled else ""
+    if tail.startswith("IdE"):
+        name += "<double>"
+    elif tail.startswith("IfE"):
+        name += "<float>"
+    return name
 
 
 def main(out_dir: str = "profiles/sass") -> None:
