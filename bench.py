@@ -199,6 +199,37 @@ def oracle_window(scene: dict, budget_s: float, max_substeps: int | None = None)
     return dict(n=n, substeps=k, seconds=t, value=n * k / t, iters=iters, contacts=ncs)
 
 
+def oracle_loaded_substep(scene: dict, snap: dict) -> dict:
+    """Time the oracle port on ONE contact-loaded substep of the window: the
+    substep the GPU arm profiles (substep 0 of window step K/2), started from
+    the GPU state at that point (particles, plastic strain, body poses and
+    velocities, time), one thread.  A representative sample of the window's
+    work, next to the window prefix (substeps 0, 1, ...; 1 solver iteration)."""
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    sys.path.insert(0, str(ROOT / "tests"))
+    from oracle import grid as og
+    from oracle import step as ostep
+    from scenes import oracle_state
+    s = oracle_state(scene, snap["x"], snap["v"], snap["f"], snap["c"], snap["mass"],
+                     snap["volume0"], snap["material_id"])
+    s.plastic = snap["plastic"].copy()
+    for b, (pos, quat, vel, om) in zip(s.bodies, snap["bodies"]):
+        b.position, b.quat, b.v, b.omega = pos.copy(), quat.copy(), vel.copy(), om.copy()
+    s.time, s.step_index = snap["time"], snap["step_index"]
+    N = scene["substeps"]
+    t0 = time.perf_counter()
+    ostep.check_health(s)  # rigid-step start (coupling.py:168-182), then one substep
+    og.sort_plan(s.x, s.h, s.step_index)
+    s.cache.clear()
+    s.acc_lin[:] = 0.0
+    s.acc_ang[:] = 0.0
+    info = ostep.substep(s, scene["dt"] / N)
+    t = time.perf_counter() - t0
+    n = snap["x"].shape[0]
+    return dict(value=n / t, seconds=t, iterations=int(info["report"].iterations),
+                contacts=int(info["contacts"].n), n=n)
+
+
 def _window_sample_text(r: dict, N: int) -> str:
     return (f"substeps 0..{r['substeps'] - 1} of the timed window's scene from t=0 "
             f"(contiguous prefix of the GPU window; {r['n']} particles, "
@@ -381,13 +412,23 @@ def run_ours(args):
     restore()
     stream = state._stream
 
+    loaded_snap = {}
+
     def profiled_step(ncu: bool = False) -> dict:
         """Live per-stage timing of one substep in the middle of the window:
         restore, advance half the window, profile the next step's first
-        substep (direct launches, CUDA events on the sim's stream)."""
+        substep (direct launches, CUDA events on the sim's stream).  The state
+        at that substep's start is kept for the CPU oracle's loaded sample."""
         restore()
         for _ in range(args.steps // 2):
             mp.advance_step(state)
+        if not ncu:
+            loaded_snap.clear()
+            loaded_snap.update(state.particles.numpy())
+            loaded_snap["bodies"] = [(np.asarray(b.position, float), np.asarray(b.quat, float),
+                                      np.asarray(b.v, float), np.asarray(b.omega, float))
+                                     for b in state.bodies]
+            loaded_snap["time"], loaded_snap["step_index"] = state.time, state.step_index
         prof = {"ncu": ncu}
         mp.advance_step(state, profile=prof)
         return prof
@@ -538,6 +579,16 @@ def run_ours(args):
                    sample=_window_sample_text(r, N),
                    gpu_same_prefix=("the GPU arm's first rigid step of the same window: "
                                     f"{first_ms:.2f} ms device time"))
+        if loaded_snap and args.workload not in ("cloth", "tshirt"):
+            ld = oracle_loaded_substep(scene, loaded_snap)
+            gpu_ms = substep_ms
+            cpu["loaded_substep"] = dict(
+                value=ld["value"], unit=UNIT, seconds=ld["seconds"],
+                solver_iterations=ld["iterations"], contacts=ld["contacts"],
+                gpu_ms_same_substep=gpu_ms, gpu_solver_iterations=prof["iterations"],
+                ratio_gpu_over_cpu=(ld["seconds"] * 1e3) / gpu_ms,
+                sample=(f"substep 0 of window step {args.steps // 2} from the GPU state at its "
+                        "start (the substep roofline.stages_ms profiles), one thread"))
 
     if rank == 0:
         line = dict(

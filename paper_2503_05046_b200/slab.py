@@ -35,8 +35,11 @@ statistics): a node of a block shared with a neighbour belongs to the rank
 whose slab contains the node's coordinate; a node of an unshared block belongs
 to the only rank that has it.
 
-The communication layer works on CPU tensors under gloo (tests, and several
-ranks sharing one GPU) and on device tensors under NCCL.
+The P2G halos and the particle migration are point-to-point exchanges with the
+two adjacent ranks only (``Comm.neighbours``, batch_isend_irecv); the contact
+problem is gathered to rank 0 (``Comm.gather0``).  The communication layer
+works on CPU tensors under gloo (tests, and several ranks sharing one GPU) and
+on device tensors under NCCL.
 """
 
 from __future__ import annotations
@@ -102,11 +105,14 @@ def node_coords(block_coords: torch.Tensor, node_ids: torch.Tensor) -> torch.Ten
     return block_coords[b] * BLOCK_EDGE + off
 
 
-def halo_band(block_axis: torch.Tensor, bounds: np.ndarray, rank: int, h: float) -> torch.Tensor:
-    """Blocks within HALO_BLOCKS of this rank's interior slab bounds."""
+def halo_band(block_axis: torch.Tensor, bounds: np.ndarray, rank: int, h: float,
+              side: str = "both") -> torch.Tensor:
+    """Blocks within HALO_BLOCKS of this rank's interior slab bounds: its left
+    bound (shared with rank - 1), its right bound (rank + 1), or both."""
     band = torch.zeros_like(block_axis, dtype=torch.bool)
     width = BLOCK_EDGE * h
-    for k in (rank, rank + 1):
+    ks = {"left": (rank,), "right": (rank + 1,), "both": (rank, rank + 1)}[side]
+    for k in ks:
         if 0 < k < len(bounds) - 1:
             bX = int(round(bounds[k] / width))
             band |= (block_axis >= bX - HALO_BLOCKS) & (block_axis < bX + HALO_BLOCKS)
@@ -162,6 +168,62 @@ class Comm:
         pad[: src.shape[0]] = src
         outs = [torch.empty_like(pad) for _ in range(self.world)]
         dist.all_gather(outs, pad, group=self.group)
+        return [o[:k].to(t.device) for o, k in zip(outs, ns)]
+
+    def neighbours(self, to_left: torch.Tensor | None, to_right: torch.Tensor | None):
+        """Exchange with the adjacent ranks only: send ``to_left`` to rank - 1
+        and ``to_right`` to rank + 1 (same trailing shape and dtype, any row
+        count); returns (from_left, from_right), None at the ends of the
+        chain.  Point-to-point (batch_isend_irecv): two neighbours per rank
+        whatever the world size, instead of an all-gather to every rank."""
+        if self.world == 1:
+            return None, None
+        have = [(self.rank - 1, to_left), (self.rank + 1, to_right)]
+        have = [(q, t) for q, t in have if 0 <= q < self.world]
+        proto = next(t for _, t in have if t is not None)
+        tail, dtype = tuple(proto.shape[1:]), proto.dtype
+        # 1. row counts
+        sends, recvs, ops = {}, {}, []
+        for q, t in have:
+            sends[q] = torch.tensor([t.shape[0]], dtype=torch.int64, device=self.dev)
+            recvs[q] = torch.zeros(1, dtype=torch.int64, device=self.dev)
+            ops.append(dist.P2POp(dist.isend, sends[q], q, group=self.group))
+            ops.append(dist.P2POp(dist.irecv, recvs[q], q, group=self.group))
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+        # 2. payloads
+        ops, bufs = [], {}
+        for q, t in have:
+            k = int(recvs[q].item())
+            bufs[q] = torch.empty((k,) + tail, dtype=dtype, device=self.dev)
+            if t.shape[0]:
+                ops.append(dist.P2POp(dist.isend, t.to(self.dev).contiguous(), q, group=self.group))
+            if k:
+                ops.append(dist.P2POp(dist.irecv, bufs[q], q, group=self.group))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        dev = proto.device
+        left = bufs[self.rank - 1].to(dev) if (self.rank - 1) in bufs else None
+        right = bufs[self.rank + 1].to(dev) if (self.rank + 1) in bufs else None
+        return left, right
+
+    def gather0(self, t: torch.Tensor) -> list[torch.Tensor] | None:
+        """Every rank's tensor on rank 0 (None elsewhere); any row count."""
+        if self.world == 1:
+            return [t]
+        src = t.to(self.dev).contiguous()
+        n = torch.tensor([src.shape[0]], dtype=torch.int64, device=self.dev)
+        ns = [torch.zeros_like(n) for _ in range(self.world)]
+        dist.all_gather(ns, n, group=self.group)
+        ns = [int(k.item()) for k in ns]
+        cap = max(max(ns), 1)
+        pad = torch.zeros((cap,) + tuple(src.shape[1:]), dtype=src.dtype, device=self.dev)
+        pad[: src.shape[0]] = src
+        outs = [torch.empty_like(pad) for _ in range(self.world)] if self.rank == 0 else None
+        dist.gather(pad, outs, dst=0, group=self.group)
+        if self.rank != 0:
+            return None
         return [o[:k].to(t.device) for o, k in zip(outs, ns)]
 
     def sum(self, t: torch.Tensor) -> torch.Tensor:
@@ -228,14 +290,21 @@ class SlabState:
         dest = slab_of(p.x[:, self.axis], self.bounds)
         if c.world > 1:
             moving = dest != c.rank
-            n_moving = int(c.sum(torch.tensor([int(moving.sum())], dtype=torch.int64)).item())
-            if n_moving == 0:
+            skip = int((dest - c.rank).abs().max()) > 1 if dest.numel() else False
+            tot = c.sum(torch.tensor([int(moving.sum()), int(skip)], dtype=torch.int64))
+            if int(tot[1]):  # every rank raises (no rank is left in a collective)
+                raise RuntimeError("slab decomposition: a particle skipped a slab within one "
+                                   "step (reduce dt or widen the slabs)")
+            if int(tot[0]) == 0:
                 return
-            out = torch.nonzero(moving, as_tuple=False).reshape(-1)
             keep = torch.nonzero(~moving, as_tuple=False).reshape(-1)
-            pay = _pack_particles(p, self.gid, out, dest[out])
-            got = torch.cat(c.allgather(pay))
-            got = got[got[:, 0].to(torch.int64) == c.rank] if got.numel() else got
+            # grouped point-to-point: left movers to rank - 1, right movers to rank + 1
+            lo_idx = torch.nonzero(dest < c.rank, as_tuple=False).reshape(-1)
+            hi_idx = torch.nonzero(dest > c.rank, as_tuple=False).reshape(-1)
+            from_l, from_r = c.neighbours(_pack_particles(p, self.gid, lo_idx, dest[lo_idx]),
+                                          _pack_particles(p, self.gid, hi_idx, dest[hi_idx]))
+            got = torch.cat([t for t in (from_l, from_r) if t is not None] or
+                            [_pack_particles(p, self.gid, lo_idx[:0], dest[:0])])
             arrays = {k: getattr(p, k)[keep] for k in PARTICLE_FIELDS}
             gid = self.gid[keep]
             if got.shape[0]:
@@ -287,20 +356,27 @@ def _halo_reduce(ss: SlabState, grid: SparseGrid) -> torch.Tensor:
     if c.world == 1 or grid.n_blocks == 0:
         return shared
     bc = grid.block_coords
-    band = torch.nonzero(halo_band(bc[:, ss.axis], ss.bounds, c.rank, ss.state.h),
-                         as_tuple=False).reshape(-1)
     ch = torch.cat([grid.mass.view(-1, BLOCK_NODES, 1), grid.mom_apic.view(-1, BLOCK_NODES, 3),
                     grid.mom_force.view(-1, BLOCK_NODES, 3)], dim=2)  # (nb, 64, 7)
-    keys = c.allgather(grid.block_keys[band])
-    vals = c.allgather(ch[band].reshape(-1, BLOCK_NODES * 7))
+
+    def band_payload(side):
+        idx = torch.nonzero(halo_band(bc[:, ss.axis], ss.bounds, c.rank, ss.state.h, side),
+                            as_tuple=False).reshape(-1)
+        # one row per block: packed key (as float64 bits) + 64 x 7 channels
+        key = grid.block_keys[idx].view(torch.float64)[:, None]
+        return torch.cat([key, ch[idx].reshape(-1, BLOCK_NODES * 7)], dim=1)
+
+    # each band goes to the one neighbour that can share it (point-to-point)
+    from_l, from_r = c.neighbours(band_payload("left"), band_payload("right"))
     add = torch.zeros_like(ch)
-    for q in range(c.world):
-        if q == c.rank or keys[q].numel() == 0:
+    for got in (from_l, from_r):
+        if got is None or got.numel() == 0:
             continue
-        pos = match_keys(grid.block_keys, keys[q])
+        got = got.to(ch.device)
+        pos = match_keys(grid.block_keys, got[:, 0].contiguous().view(torch.int64))
         hit = pos >= 0
         if bool(hit.any()):
-            add[pos[hit]] += vals[q][hit].view(-1, BLOCK_NODES, 7)
+            add[pos[hit]] += got[hit, 1:].reshape(-1, BLOCK_NODES, 7)
             shared[pos[hit]] = True
     ch = ch + add
     grid.mass.copy_(ch[:, :, 0].reshape(-1))
@@ -346,11 +422,12 @@ def _distributed_solve(ss: SlabState, grid, stencil, contacts, dt_s, block_share
                       contacts.mu[:, None], contacts.gamma_lag[:, None], w], dim=1) \
         if contacts.n else _lib.zeros((0, 9 + 3 + 3 + 27))
     nrec = torch.cat([grid.mass[act][cn][:, None], grid.v_star[act][cn], grid.v_k[act][cn]], dim=1)
-    g_ck = c.allgather(skeys)
-    g_cr = c.allgather(crec)
+    # the contact records go to rank 0 only; every rank needs the counts
+    g_ck = c.gather0(skeys)
+    g_cr = c.gather0(crec)
     g_nk = all_cn
-    g_nr = c.allgather(nrec)
-    counts = [int(k.shape[0]) for k in g_ck]
+    g_nr = c.gather0(nrec)
+    counts = [int(k) for k in c.allgather(torch.tensor([[skeys.shape[0]]], dtype=torch.int64))]
     if c.rank == 0:
         ck = torch.cat([k.to(dev) for k in g_ck])
         cr = torch.cat([r.to(dev) for r in g_cr])

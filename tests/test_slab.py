@@ -186,3 +186,43 @@ def test_comm_world2_gloo(tmp_path):
         assert r["empty"][0].shape == (0, 4) and r["empty"][1].shape == (2, 4)
         assert r["s"].tolist() == [3.0, 2.0]
         assert r["b"].tolist() == [[0.0, 1.0, 2.0], [3.0, 4.0, 5.0]]
+
+
+def _neighbour_worker(rank, world, port, out):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    c = S.Comm()
+    # rank r sends r+1 rows of value 100 r + 1 to the left and 2 (r+1) rows of
+    # 100 r + 2 to the right; rank 1 sends nothing to the left (empty payload)
+    to_l = torch.full((0 if rank == 1 else rank + 1, 2), 100.0 * rank + 1)
+    to_r = torch.full((2 * (rank + 1), 2), 100.0 * rank + 2)
+    fl, fr = c.neighbours(to_l, to_r)
+    g = c.gather0(torch.full((rank, 3), float(rank), dtype=torch.float64))
+    torch.save(dict(fl=fl, fr=fr, g=g), os.path.join(out, f"n{rank}.pt"))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_neighbour_exchange_and_gather0_gloo(tmp_path, world):
+    """Comm.neighbours (the P2G halo and migration exchange) reaches exactly
+    the adjacent ranks, with variable and empty payloads; gather0 collects
+    every rank's rows on rank 0 only."""
+    mp.spawn(_neighbour_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world,
+             join=True)
+    for rank in range(world):
+        r = torch.load(tmp_path / f"n{rank}.pt")
+        if rank == 0:
+            assert r["fl"] is None
+            assert [t.shape[0] for t in r["g"]] == list(range(world))
+            assert all(bool((t == q).all()) for q, t in enumerate(r["g"]))
+        else:
+            left = rank - 1  # its right payload: 2 (left + 1) rows of 100 left + 2
+            assert r["fl"].shape == (2 * (left + 1), 2) and bool((r["fl"] == 100 * left + 2).all())
+            assert r["g"] is None
+        if rank == world - 1:
+            assert r["fr"] is None
+        else:
+            right = rank + 1  # its left payload (empty from rank 1)
+            n = 0 if right == 1 else right + 1
+            assert r["fr"].shape == (n, 2) and bool((r["fr"] == 100 * right + 1).all())
