@@ -84,10 +84,15 @@ __device__ __forceinline__ void jacobi_rotate_cols(M3T<T>& a, M3T<T>& v, int p, 
   T alpha = a(0, p) * a(0, p) + a(1, p) * a(1, p) + a(2, p) * a(2, p);
   T beta = a(0, q) * a(0, q) + a(1, q) * a(1, q) + a(2, q) * a(2, q);
   T gamma = a(0, p) * a(0, q) + a(1, p) * a(1, q) + a(2, p) * a(2, q);
-  if (gamma == T(0) || fabs(gamma) <= Tol<T>::jacobi * sqrt(alpha * beta)) return;
-  T zeta = (beta - alpha) / (T(2) * gamma);
-  T t = copysign(T(1), zeta) / (fabs(zeta) + sqrt(T(1) + zeta * zeta));
-  T c = T(1) / sqrt(T(1) + t * t);
+  // skip when |gamma| <= tol sqrt(alpha beta), compared squared (no sqrt)
+  if (gamma == T(0) || gamma * gamma <= (Tol<T>::jacobi * Tol<T>::jacobi) * (alpha * beta)) return;
+  // t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)) with zeta = (beta - alpha) /
+  // (2 gamma), rewritten with d = beta - alpha, e = 2 gamma as
+  // t = sign(d) e / (|d| + sqrt(d^2 + e^2)): one square root and one division
+  // (was two and three), then c = 1 / sqrt(1 + t^2) as one rsqrt
+  const T d = beta - alpha, e = T(2) * gamma;
+  T t = copysign(T(1), d) * e / (fabs(d) + sqrt(d * d + e * e));
+  T c = rsqrt(T(1) + t * t);
   T s = c * t;
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
@@ -143,17 +148,19 @@ __device__ __forceinline__ SVD3T<T> signed_svd(const M3T<T>& f) {
   const T tiny = Tol<T>::tiny;
   T c0[3], c1[3], c2[3];
   if (s[0] > tiny) {
-    for (int i = 0; i < 3; ++i) c0[i] = a(i, 0) / s[0];
+    const T inv = T(1) / s[0];
+    for (int i = 0; i < 3; ++i) c0[i] = a(i, 0) * inv;
   } else {
     c0[0] = T(1); c0[1] = T(0); c0[2] = T(0);
   }
   if (s[1] > tiny * fmax(T(1), s[0]) && s[1] > Tol<T>::rank * s[0]) {
-    for (int i = 0; i < 3; ++i) c1[i] = a(i, 1) / s[1];
+    const T inv = T(1) / s[1];
+    for (int i = 0; i < 3; ++i) c1[i] = a(i, 1) * inv;
     // re-orthogonalise against c0
     T d = c1[0] * c0[0] + c1[1] * c0[1] + c1[2] * c0[2];
     for (int i = 0; i < 3; ++i) c1[i] -= d * c0[i];
-    T nn = sqrt(c1[0] * c1[0] + c1[1] * c1[1] + c1[2] * c1[2]);
-    for (int i = 0; i < 3; ++i) c1[i] /= nn;
+    const T rn = rsqrt(c1[0] * c1[0] + c1[1] * c1[1] + c1[2] * c1[2]);
+    for (int i = 0; i < 3; ++i) c1[i] *= rn;
   } else {
     // any unit vector orthogonal to c0
     int k = (fabs(c0[0]) <= fabs(c0[1]) && fabs(c0[0]) <= fabs(c0[2])) ? 0
@@ -162,16 +169,17 @@ __device__ __forceinline__ SVD3T<T> signed_svd(const M3T<T>& f) {
     e[k] = T(1);
     T d = e[0] * c0[0] + e[1] * c0[1] + e[2] * c0[2];
     for (int i = 0; i < 3; ++i) c1[i] = e[i] - d * c0[i];
-    T nn = sqrt(c1[0] * c1[0] + c1[1] * c1[1] + c1[2] * c1[2]);
-    for (int i = 0; i < 3; ++i) c1[i] /= nn;
+    const T rn = rsqrt(c1[0] * c1[0] + c1[1] * c1[1] + c1[2] * c1[2]);
+    for (int i = 0; i < 3; ++i) c1[i] *= rn;
   }
   if (s[2] > Tol<T>::rank * fmax(s[0], tiny)) {
-    for (int i = 0; i < 3; ++i) c2[i] = a(i, 2) / s[2];
+    const T inv = T(1) / s[2];
+    for (int i = 0; i < 3; ++i) c2[i] = a(i, 2) * inv;
     T d0 = c2[0] * c0[0] + c2[1] * c0[1] + c2[2] * c0[2];
     T d1 = c2[0] * c1[0] + c2[1] * c1[1] + c2[2] * c1[2];
     for (int i = 0; i < 3; ++i) c2[i] -= d0 * c0[i] + d1 * c1[i];
-    T nn = sqrt(c2[0] * c2[0] + c2[1] * c2[1] + c2[2] * c2[2]);
-    for (int i = 0; i < 3; ++i) c2[i] /= nn;
+    const T rn = rsqrt(c2[0] * c2[0] + c2[1] * c2[1] + c2[2] * c2[2]);
+    for (int i = 0; i < 3; ++i) c2[i] *= rn;
   } else {
     cross3(c0, c1, c2);
   }
