@@ -198,6 +198,63 @@ __global__ void k_block_insert(const double* __restrict__ x, long long n, double
       }
     }
   }
+  // Fast path: the warp's candidate blocks fit a 2x2x2 box of blocks (the
+  // common case for particles sorted by (block, cell)).  Each lane marks the
+  // box blocks its stencil touches, the warp ORs the marks, and lanes 0-7
+  // insert the marked blocks: one round of <= 8 inserts instead of eight
+  // rounds of match + probe.
+  {
+    int wlo[3], whi[3];
+    bool box = true;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      wlo[a] = __reduce_min_sync(0xffffffffu, valid ? (int)lo[a] : INT_MAX);
+      whi[a] = __reduce_max_sync(0xffffffffu, valid ? (int)hi[a] : INT_MIN);
+      box &= whi[a] - wlo[a] <= 1;
+    }
+    if (box) {  // warp-uniform (also true when no lane is valid: nothing to insert)
+      unsigned marks = 0;
+      if (valid) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const int ix = (c >> 2) & 1, iy = (c >> 1) & 1, iz = c & 1;
+          if ((ix && hi[0] == lo[0]) || (iy && hi[1] == lo[1]) || (iz && hi[2] == lo[2]))
+            continue;
+          const int dx = (int)(ix ? hi[0] : lo[0]) - wlo[0];
+          const int dy = (int)(iy ? hi[1] : lo[1]) - wlo[1];
+          const int dz = (int)(iz ? hi[2] : lo[2]) - wlo[2];
+          marks |= 1u << ((dx << 2) | (dy << 1) | dz);
+        }
+      }
+      marks = __reduce_or_sync(0xffffffffu, marks);
+      if (lane < 8 && ((marks >> lane) & 1u)) {
+        int64_t key;
+        if (!pack_block(wlo[0] + ((lane >> 2) & 1), wlo[1] + ((lane >> 1) & 1),
+                        wlo[2] + (lane & 1), &key)) {
+          raise_status(st, MPMRB_E_ALLOCATION, 2, i - lane);  // grid.py:29-30
+        } else {
+          const unsigned long long k = (unsigned long long)key;
+          unsigned s = hash64(k) & mask;
+          for (unsigned probe = 0; probe <= mask; ++probe) {
+            const unsigned long long cur = hkeys[s];
+            if (cur == k) break;
+            if (cur == kEmptyKey) {
+              const unsigned long long old = atomicCAS(&hkeys[s], kEmptyKey, k);
+              if (old == kEmptyKey) {
+                const int idx = atomicAdd(nb, 1);
+                if (idx < block_cap) ukeys[idx] = (long long)k;
+                else raise_status(st, MPMRB_E_CAPACITY, 1, idx + 1);
+                break;
+              }
+              if (old == k) break;
+            }
+            s = (s + 1) & mask;
+          }
+        }
+      }
+      return;
+    }
+  }
 #pragma unroll 1
   for (int c = 0; c < 8; ++c) {
     int ix = (c >> 2) & 1, iy = (c >> 1) & 1, iz = c & 1;
