@@ -289,66 +289,36 @@ __global__ void k_block_insert(const double* __restrict__ x, long long n, double
   }
 }
 
-// Single-CTA bitonic sort of the unique keys (nb <= kSmallSort), then write the
-// sorted index into each key's hash slot (grid.py:97, 114-121).
-constexpr int kSortThreads = 1024;
-constexpr int kSmallSort = 16384;
-
-__global__ void __launch_bounds__(kSortThreads) k_block_sort(
-    const long long* __restrict__ ukeys, const int* __restrict__ nb_dev,
-    long long block_cap, long long* __restrict__ block_keys,
-    const unsigned long long* __restrict__ hkeys, int* __restrict__ hvals, unsigned mask) {
-  extern __shared__ long long sk[];
-  int nb = *nb_dev;
-  if (nb > block_cap) return;   // capacity error already raised by k_block_insert
-  if (nb > kSmallSort) return;  // handled by k_block_rank
-  int p2 = 1;
-  while (p2 < nb) p2 <<= 1;
-  for (int i = threadIdx.x; i < p2; i += kSortThreads) sk[i] = (i < nb) ? ukeys[i] : LLONG_MAX;
-  __syncthreads();
-  for (int size = 2; size <= p2; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int t = threadIdx.x; t < (p2 >> 1); t += kSortThreads) {
-        int lo = 2 * t - (t & (stride - 1));
-        int hi = lo + stride;
-        bool up = ((lo & size) == 0);
-        long long a = sk[lo], b = sk[hi];
-        if ((a > b) == up) {
-          sk[lo] = b;
-          sk[hi] = a;
-        }
-      }
-      __syncthreads();
-    }
-  }
-  for (int i = threadIdx.x; i < nb; i += kSortThreads) {
-    long long key = sk[i];
-    block_keys[i] = key;
-    unsigned s = hash64((unsigned long long)key) & mask;
-    while (hkeys[s] != (unsigned long long)key) s = (s + 1) & mask;
-    hvals[s] = i;
-  }
-}
-
-// Fallback for very large grids: rank = number of smaller keys (O(nb^2)).
-__global__ void k_block_rank(const long long* __restrict__ ukeys, const int* __restrict__ nb_dev,
-                             long long block_cap, long long* __restrict__ block_keys,
-                             const unsigned long long* __restrict__ hkeys,
-                             int* __restrict__ hvals, unsigned mask) {
-  int nb = *nb_dev;
-  if (nb <= kSmallSort || nb > block_cap) return;
-  __shared__ long long tile[256];
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  long long key = (i < nb) ? ukeys[i] : 0;
+// The sorted block order (grid.py:97, np.unique) by ranking: a key's sorted
+// index is the number of smaller keys (keys are unique).  kRankLanes lanes
+// share a key, each counting over a strided slice of the keys staged in shared
+// memory, so the O(nb^2) comparisons spread over nb * kRankLanes threads (a
+// single-CTA bitonic sort of ~2.7k keys took 42 us, latency-bound on its
+// 78 barrier stages).  Also writes each key's sorted index into its hash slot.
+constexpr int kRankLanes = 8;
+constexpr int kRankTile = 2048;
+__global__ void __launch_bounds__(256) k_block_rank_par(
+    const long long* __restrict__ ukeys, const int* __restrict__ nb_dev, long long block_cap,
+    long long* __restrict__ block_keys, const unsigned long long* __restrict__ hkeys,
+    int* __restrict__ hvals, unsigned mask) {
+  __shared__ long long tile[kRankTile];
+  const int nb = *nb_dev;
+  if (nb > block_cap) return;  // capacity error already raised by k_block_insert
+  if ((long long)blockIdx.x * (256 / kRankLanes) >= nb) return;  // CTA-uniform
+  const int t = blockIdx.x * 256 + threadIdx.x;
+  const int i = t / kRankLanes, sub = t % kRankLanes;
+  const long long key = i < nb ? ukeys[i] : LLONG_MAX;
   int rank = 0;
-  for (int base = 0; base < nb; base += 256) {
+  for (int base = 0; base < nb; base += kRankTile) {
     __syncthreads();
-    if (base + threadIdx.x < nb) tile[threadIdx.x] = ukeys[base + threadIdx.x];
+    const int lim = min(kRankTile, nb - base);
+    for (int q = threadIdx.x; q < lim; q += 256) tile[q] = ukeys[base + q];
     __syncthreads();
-    int lim = min(256, nb - base);
-    for (int j = 0; j < lim; ++j) rank += (tile[j] < key) ? 1 : 0;
+    for (int j = sub; j < lim; j += kRankLanes) rank += tile[j] < key ? 1 : 0;
   }
-  if (i < nb) {
+#pragma unroll
+  for (int o = 1; o < kRankLanes; o <<= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
+  if (sub == 0 && i < nb) {
     block_keys[rank] = key;
     unsigned s = hash64((unsigned long long)key) & mask;
     while (hkeys[s] != (unsigned long long)key) s = (s + 1) & mask;
@@ -466,12 +436,6 @@ int launch_staleness(Ctx& c, const uint16_t* plan_keys, const double* x, long lo
 int launch_grid_build(Ctx& c, const double* x, long long n, double h, long long* block_keys,
                       long long block_cap, unsigned long long* hkeys, int* hvals,
                       long long hash_cap, long long* ukeys, int* nb_dev) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    MPMRB_CUDA_OK(cudaFuncSetAttribute(k_block_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       kSmallSort * (int)sizeof(long long)));
-    attr_set = true;
-  }
   unsigned mask = (unsigned)(hash_cap - 1);
   k_hash_clear<<<grid_for(hash_cap, 256), 256, 0, c.stream>>>(hkeys, hash_cap, nb_dev);
   c.launches++;
@@ -480,18 +444,9 @@ int launch_grid_build(Ctx& c, const double* x, long long n, double h, long long*
                                                           block_cap, nb_dev, c.status);
     c.launches++;
   }
-  // smem sized for the capacity (rounded to a power of two, capped)
-  long long p2 = 1;
-  while (p2 < block_cap && p2 < kSmallSort) p2 <<= 1;
-  k_block_sort<<<1, kSortThreads, p2 * sizeof(long long), c.stream>>>(ukeys, nb_dev, block_cap,
-                                                                     block_keys, hkeys, hvals,
-                                                                     mask);
+  k_block_rank_par<<<grid_for(block_cap * kRankLanes, 256), 256, 0, c.stream>>>(
+      ukeys, nb_dev, block_cap, block_keys, hkeys, hvals, mask);
   c.launches++;
-  if (block_cap > kSmallSort) {
-    k_block_rank<<<grid_for(block_cap, 256), 256, 0, c.stream>>>(ukeys, nb_dev, block_cap,
-                                                                block_keys, hkeys, hvals, mask);
-    c.launches++;
-  }
   MPMRB_CUDA_OK(cudaGetLastError());
   return MPMRB_OK;
 }
