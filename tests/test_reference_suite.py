@@ -6,7 +6,7 @@ restatements of them.
 The reference tests are not part of this repository: tools/refsuite_run.sh
 copies /root/reference/pkg/tests/{conftest,oracles,test_transfer,test_mpm,
 test_collision,test_contact_model,test_solver,test_coupling,
-test_materials,test_geometry}.py into
+test_materials,test_geometry,test_rigid}.py into
 tests/refsuite/_staged/ (git-ignored) for one GPU run and removes them
 afterwards; the run's per-test outcome is committed under profiles/.  Without
 the staged files this test skips.

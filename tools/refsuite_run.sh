@@ -7,7 +7,7 @@ set -e
 cd "$(dirname "$0")/.."
 STAGED=tests/refsuite/_staged
 rm -rf "$STAGED"; mkdir -p "$STAGED"
-for f in conftest oracles test_transfer test_mpm test_collision test_contact_model test_solver test_coupling test_materials test_geometry; do
+for f in conftest oracles test_transfer test_mpm test_collision test_contact_model test_solver test_coupling test_materials test_geometry test_rigid; do
   cp /root/reference/pkg/tests/$f.py "$STAGED/"
 done
 set +e
