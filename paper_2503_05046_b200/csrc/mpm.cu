@@ -115,52 +115,18 @@ __global__ void k_stresses(const double* __restrict__ f, const long long* __rest
   m3_store(tau + 9 * i, t);
 }
 
-// Scatter of one particle's 27 x 7 contributions with global float64 atomics
-// (the fallback when a chunk's particles are spread too widely for a tile).
-template <class T>
-__device__ __forceinline__ void p2g_scatter_one(const GridDev& g, const Stencil1T<T>& s,
-                                                const StencilBlocks& sb, T m, const T* mv,
-                                                const M3T<T>& mC, const M3T<T>& S, const T* fi,
-                                                double* gmass, double* mom_apic,
-                                                double* mom_force) {
-  const T h = (T)g.h;
-#pragma unroll 1
-  for (int ox = 0; ox < 3; ++ox) {
-    const T dx = (T(ox) - s.fx[0]) * h;
-#pragma unroll 1
-    for (int oy = 0; oy < 3; ++oy) {
-      const T dy = (T(oy) - s.fx[1]) * h;
-      const T wxy = s.w[0][ox] * s.w[1][oy];
-#pragma unroll
-      for (int oz = 0; oz < 3; ++oz) {
-        const T dz = (T(oz) - s.fx[2]) * h;
-        const T w = wxy * s.w[2][oz];
-        const int node = stencil_node(s, sb, ox, oy, oz);
-        atomicAdd(&gmass[node], (double)(w * m));
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          T a = mv[d] + (mC(d, 0) * dx + mC(d, 1) * dy + mC(d, 2) * dz);
-          T b = S(d, 0) * dx + S(d, 1) * dy + S(d, 2) * dz + fi[d];
-          atomicAdd(&mom_apic[3 * node + d], (double)(w * a));
-          atomicAdd(&mom_force[3 * node + d], (double)(w * b));
-        }
-      }
-    }
-  }
-}
-
 // P2G (mpm.py:66-99 with the stress of materials.py:113-122), warp-level.
 // Each warp takes 32 consecutive particles (the fused path sorts particles by
 // (block, cell) once per step, so a warp covers a few neighbouring cells):
-//   1. warp bounding box of the base cells; the stencils must fit a private
-//      shared-memory node tile of <= kWarpTile nodes;
+//   1. the warp's lanes are cut into segments of consecutive particles whose
+//      stencils fit a private shared-memory node tile of <= kWarpTile nodes
+//      (one segment inside a block, two across a block boundary);
 //   2. slot-parallel accumulation (step 4 below): lane k < 27 owns stencil
-//      slot k and walks the warp's particles in order, summing runs of
+//      slot k and walks the segment's particles in order, summing runs of
 //      same-cell particles in registers and adding them to the tile (one
 //      particle's 27 slots are 27 distinct nodes: no atomics, no reduction);
-//   3. the tile is flushed with one float64 atomic per node and channel.
-// ~18x fewer global atomics than the per-particle scatter (27 x 7 per
-// particle), which remains the fallback for warps whose particles are spread.
+//   3. the tile is flushed with one float64 atomic per node and channel,
+//      ~18x fewer global atomics than a per-particle scatter (27 x 7).
 constexpr int kP2GThreads = 128;
 // per-particle P2G record in shared memory (affine form, see k_p2g step 4):
 // m, pad | A (3), Bf (3) | G (9) | K (9) | 1-D weights wx, wy, wz (9) | pad
@@ -317,181 +283,191 @@ __global__ void __launch_bounds__(kP2GThreads, MPMRB_P2G_MINB) k_p2g(GridDev g, 
   const double h = g.h;
   long long i = w0 + lane;
   const bool live = i < p.n;
-  // 1. base cells and the warp bounding box
+  const int n_live = (int)min((long long)32, p.n - w0);
+  // 1. base cells and this lane's payload (registers)
   int b[3] = {0, 0, 0};
-  if (live)
-#pragma unroll
-    for (int a = 0; a < 3; ++a) b[a] = (int)base_cell(p.x[3 * i + a], h);
-  int lo[3], hi[3];
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    lo[a] = __reduce_min_sync(0xffffffffu, live ? b[a] : INT_MAX);
-    hi[a] = __reduce_max_sync(0xffffffffu, live ? b[a] : INT_MIN);
-  }
-  const int cx = hi[0] - lo[0] + 1, cy = hi[1] - lo[1] + 1, cz = hi[2] - lo[2] + 1;
-  const int nx = cx + 2, ny = cy + 2, nz = cz + 2;
-  // tiled path: <= kWarpTile nodes and <= 2 blocks per axis (flush lookup)
-  const bool spans2 = (((lo[0] + nx - 1) >> 2) - (lo[0] >> 2) <= 1) &&
-                      (((lo[1] + ny - 1) >> 2) - (lo[1] >> 2) <= 1) &&
-                      (((lo[2] + nz - 1) >> 2) - (lo[2] >> 2) <= 1);
-  if ((long long)nx * ny * nz > kWarpTile || !spans2) {
-    // spread warp: per-particle scatter with global atomics
-    if (live) {
-      Stencil1T<T> s;
-      T m, mv[3], fi[3];
-      M3T<T> mC, S;
-      particle_payload<T>(p, i, h, dt, mats, nmat, s, m, mv, mC, S, fi, st);
-      StencilBlocks sb;
-      if (!resolve_blocks(s, g.hkeys, g.hvals, g.mask, sb)) {
-        raise_status(st, MPMRB_E_ALLOCATION, 20, i);
-        return;
-      }
-      p2g_scatter_one<T>(g, s, sb, m, mv, mC, S, fi, gmass, mom_apic, mom_force);
-    }
-    return;
-  }
-  // 2. zero the warp's node tile
-  double (*tile)[kWarpTile] = s_tile[wid];
-  const int nnode = nx * ny * nz;
-  for (int q = lane; q < nnode; q += 32)
-#pragma unroll
-    for (int ch = 0; ch < 7; ++ch) tile[ch][q] = 0.0;
-  // 3. payload of this lane's particle (registers)
   Stencil1T<T> s;
   T m = T(0), mv[3] = {T(0), T(0), T(0)}, fi[3] = {T(0), T(0), T(0)};
   M3T<T> mC, S;
-  int cb[3] = {0, 0, 0};
   if (live) {
     particle_payload<T>(p, i, h, dt, mats, nmat, s, m, mv, mC, S, fi, st);
 #pragma unroll
-    for (int a = 0; a < 3; ++a) cb[a] = (int)s.base[a] - lo[a];
+    for (int a = 0; a < 3; ++a) b[a] = (int)s.base[a];
   }
-  // 4. slot-parallel accumulation: lane k < 27 owns stencil slot k and walks
-  // the warp's particles in lane order, adding particle p's 7 contributions
-  // to node (cell_p + offset_k).  One particle's 27 slots are 27 distinct
-  // nodes, so the tile updates need neither atomics nor a reduction, and each
-  // node's sum runs in particle order (deterministic).  The payloads travel
-  // through shared memory in two halves of 16 particles, one contiguous
-  // record per particle (vector loads), in affine form: with the slot offset
-  // o and dpos = (o - fx) h,
-  //   m v + mC dpos = A + G o,   S dpos + dt f = Bf + K o,
-  // G = h mC, K = h S, A = m v - G fx, Bf = dt f - K fx  (mpm.py:89-93).
+  double (*tile)[kWarpTile] = s_tile[wid];
   const int ox = lane / 9, oy = (lane / 3) % 3, oz = lane % 3;
   const T oxT = T(ox), oyT = T(oy), ozT = T(oz);
   const bool slot_lane = lane < 27;
-  const int n_live = (int)min((long long)32, p.n - w0);
-  T acc[7];
-  int q_run = -1;  // node of the particle run being summed in acc
+  // 2. segments: the warp's particles are cut into runs of consecutive lanes
+  // [s0, s1) whose stencils fit one node tile (<= kWarpTile nodes, <= 2
+  // blocks per axis for the flush lookup).  A warp inside one block is one
+  // segment; a warp straddling two blocks (consecutive in key order, not
+  // necessarily adjacent in space) is two.  s1 is the first lane whose prefix
+  // bounding box no longer fits (prefix boxes only grow).
 #pragma unroll 1
-  for (int half = 0; half < 2; ++half) {
-    const int p0 = 16 * half;
-    if (p0 >= n_live) break;
-    __syncwarp();
-    if ((lane >> 4) == half) {
-      T* rec = s_pay[wid][lane & 15];
-      const T hT = (T)h;
-      T G[9], K[9];
+  for (int s0 = 0; s0 < n_live;) {
+    const bool act = live && lane >= s0;
+    int mn[3], mx[3];
 #pragma unroll
-      for (int k = 0; k < 9; ++k) {
-        G[k] = hT * mC.a[k];
-        K[k] = hT * S.a[k];
-      }
-      rec[kPayM] = m;
-#pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        rec[kPayA + d] = mv[d] - (G[3 * d] * s.fx[0] + G[3 * d + 1] * s.fx[1] + G[3 * d + 2] * s.fx[2]);
-        rec[kPayB + d] = fi[d] - (K[3 * d] * s.fx[0] + K[3 * d + 1] * s.fx[1] + K[3 * d + 2] * s.fx[2]);
-      }
-#pragma unroll
-      for (int k = 0; k < 9; ++k) {
-        rec[kPayG + k] = G[k];
-        rec[kPayK + k] = K[k];
-        rec[kPayW + k] = s.w[k / 3][k % 3];
-      }
-      s_cell[wid][lane & 15] = make_int4(cb[0], cb[1], cb[2], 0);
+    for (int a = 0; a < 3; ++a) {
+      mn[a] = act ? b[a] : INT_MAX;
+      mx[a] = act ? b[a] : INT_MIN;
     }
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const int tn = __shfl_up_sync(0xffffffffu, mn[a], o);
+        const int tx = __shfl_up_sync(0xffffffffu, mx[a], o);
+        if (lane >= o) {
+          mn[a] = min(mn[a], tn);
+          mx[a] = max(mx[a], tx);
+        }
+      }
+    }
+    bool fits = true;
+    if (act) {
+      const int px = mx[0] - mn[0] + 3, py = mx[1] - mn[1] + 3, pz = mx[2] - mn[2] + 3;
+      fits = px * py * pz <= kWarpTile && (((mn[0] + px - 1) >> 2) - (mn[0] >> 2) <= 1) &&
+             (((mn[1] + py - 1) >> 2) - (mn[1] >> 2) <= 1) &&
+             (((mn[2] + pz - 1) >> 2) - (mn[2] >> 2) <= 1);
+    }
+    const unsigned bad = __ballot_sync(0xffffffffu, act && !fits);
+    const int s1 = bad ? __ffs(bad) - 1 : n_live;  // > s0: one stencil always fits
+    int lo[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) lo[a] = __shfl_sync(0xffffffffu, mn[a], s1 - 1);
+    const int nx = __shfl_sync(0xffffffffu, mx[0], s1 - 1) - lo[0] + 3;
+    const int ny = __shfl_sync(0xffffffffu, mx[1], s1 - 1) - lo[1] + 3;
+    const int nz = __shfl_sync(0xffffffffu, mx[2], s1 - 1) - lo[2] + 3;
+    const int nnode = nx * ny * nz;
+    // 3. zero the segment's node tile
     __syncwarp();
-    if (slot_lane) {
-      // consecutive particles of one cell (sorted order) hit the same node:
-      // their contributions are summed in registers and added to the tile
-      // when the cell changes (warp-uniform, so one flush writes 27 distinct
-      // nodes), which also keeps the tile's read-modify-write chains short
-      const int pend = min(16, n_live - p0);
+    for (int q = lane; q < nnode; q += 32)
+#pragma unroll
+      for (int ch = 0; ch < 7; ++ch) tile[ch][q] = 0.0;
+    // 4. slot-parallel accumulation: lane k < 27 owns stencil slot k and walks
+    // the segment's particles in lane order, adding particle p's 7
+    // contributions to node (cell_p + offset_k).  One particle's 27 slots are
+    // 27 distinct nodes, so the tile updates need neither atomics nor a
+    // reduction, and each node's sum runs in particle order (deterministic).
+    // The payloads travel through shared memory in halves of 16 particles, one
+    // contiguous record per particle (vector loads), in affine form: with the
+    // slot offset o and dpos = (o - fx) h,
+    //   m v + mC dpos = A + G o,   S dpos + dt f = Bf + K o,
+    // G = h mC, K = h S, A = m v - G fx, Bf = dt f - K fx  (mpm.py:89-93).
+    T acc[7];
+    int q_run = -1;  // node of the particle run being summed in acc
 #pragma unroll 1
-      for (int r = 0; r < pend; ++r) {
-        const T* rec = s_pay[wid][r];
-        T q[kPayW];
-        load_payload<T>(rec, q);
-        const T w = (rec[kPayW + ox] * rec[kPayW + 3 + oy]) * rec[kPayW + 6 + oz];
-        T v[7];
-        v[0] = w * q[kPayM];
+    for (int half = s0 >> 4; half <= (s1 - 1) >> 4; ++half) {
+      __syncwarp();
+      if ((lane >> 4) == half && act) {
+        T* rec = s_pay[wid][lane & 15];
+        const T hT = (T)h;
+        T G[9], K[9];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) {
+          G[k] = hT * mC.a[k];
+          K[k] = hT * S.a[k];
+        }
+        rec[kPayM] = m;
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
-          const T* g = q + kPayG + 3 * d;
-          const T* k = q + kPayK + 3 * d;
-          v[1 + d] = w * (q[kPayA + d] + (g[0] * oxT + g[1] * oyT + g[2] * ozT));
-          v[4 + d] = w * (q[kPayB + d] + (k[0] * oxT + k[1] * oyT + k[2] * ozT));
+          rec[kPayA + d] = mv[d] - (G[3 * d] * s.fx[0] + G[3 * d + 1] * s.fx[1] + G[3 * d + 2] * s.fx[2]);
+          rec[kPayB + d] = fi[d] - (K[3 * d] * s.fx[0] + K[3 * d + 1] * s.fx[1] + K[3 * d + 2] * s.fx[2]);
         }
-        const int4 cr = s_cell[wid][r];
-        const int qn = ((cr.x + ox) * ny + (cr.y + oy)) * nz + (cr.z + oz);
-        if (qn != q_run) {
-          // the run changes on every slot lane at once (the cell changed)
-          __syncwarp(0x07ffffffu);
-          if (q_run >= 0)
 #pragma unroll
-            for (int ch = 0; ch < 7; ++ch) tile[ch][q_run] += (double)acc[ch];
+        for (int k = 0; k < 9; ++k) {
+          rec[kPayG + k] = G[k];
+          rec[kPayK + k] = K[k];
+          rec[kPayW + k] = s.w[k / 3][k % 3];
+        }
+        s_cell[wid][lane & 15] = make_int4(b[0] - lo[0], b[1] - lo[1], b[2] - lo[2], 0);
+      }
+      __syncwarp();
+      if (slot_lane) {
+        // consecutive particles of one cell (sorted order) hit the same node:
+        // their contributions are summed in registers and added to the tile
+        // when the cell changes (warp-uniform, so one flush writes 27 distinct
+        // nodes), which also keeps the tile's read-modify-write chains short
+        const int r1 = min(16, s1 - 16 * half);
+#pragma unroll 1
+        for (int r = max(0, s0 - 16 * half); r < r1; ++r) {
+          const T* rec = s_pay[wid][r];
+          T q[kPayW];
+          load_payload<T>(rec, q);
+          const T w = (rec[kPayW + ox] * rec[kPayW + 3 + oy]) * rec[kPayW + 6 + oz];
+          T v[7];
+          v[0] = w * q[kPayM];
 #pragma unroll
-          for (int ch = 0; ch < 7; ++ch) acc[ch] = v[ch];
-          q_run = qn;
-        } else {
+          for (int d = 0; d < 3; ++d) {
+            const T* g = q + kPayG + 3 * d;
+            const T* k = q + kPayK + 3 * d;
+            v[1 + d] = w * (q[kPayA + d] + (g[0] * oxT + g[1] * oyT + g[2] * ozT));
+            v[4 + d] = w * (q[kPayB + d] + (k[0] * oxT + k[1] * oyT + k[2] * ozT));
+          }
+          const int4 cr = s_cell[wid][r];
+          const int qn = ((cr.x + ox) * ny + (cr.y + oy)) * nz + (cr.z + oz);
+          if (qn != q_run) {
+            // the run changes on every slot lane at once (the cell changed)
+            __syncwarp(0x07ffffffu);
+            if (q_run >= 0)
 #pragma unroll
-          for (int ch = 0; ch < 7; ++ch) acc[ch] += v[ch];
+              for (int ch = 0; ch < 7; ++ch) tile[ch][q_run] += (double)acc[ch];
+#pragma unroll
+            for (int ch = 0; ch < 7; ++ch) acc[ch] = v[ch];
+            q_run = qn;
+          } else {
+#pragma unroll
+            for (int ch = 0; ch < 7; ++ch) acc[ch] += v[ch];
+          }
         }
       }
     }
-  }
-  if (slot_lane && q_run >= 0)
+    if (slot_lane && q_run >= 0)
 #pragma unroll
-    for (int ch = 0; ch < 7; ++ch) tile[ch][q_run] += (double)acc[ch];
-  __syncwarp();
-  // 5. flush: one atomic per (node, channel).  The tile spans at most 2
-  // blocks per axis (<= 8 blocks, nodes <= 10 per axis): lanes 0-7 resolve
-  // one block each through the hash table, the others read them by shuffle.
-  const int blo0 = lo[0] >> 2, blo1 = lo[1] >> 2, blo2 = lo[2] >> 2;
-  int myblk = -1;
-  if (lane < 8) {
-    int64_t bkey;
-    if (pack_block(blo0 + ((lane >> 2) & 1), blo1 + ((lane >> 1) & 1), blo2 + (lane & 1), &bkey))
-      myblk = hash_find(g.hkeys, g.hvals, g.mask, (uint64_t)bkey);
-  }
-  for (int q0 = 0; q0 < nnode; q0 += 32) {
-    const int q = q0 + lane;
-    const bool inb = q < nnode;
-    const int qz = inb ? q % nz : 0, qy = inb ? (q / nz) % ny : 0, qx = inb ? q / (nz * ny) : 0;
-    const int gx = lo[0] + qx, gy = lo[1] + qy, gz = lo[2] + qz;
-    const int bsel = (((gx >> 2) - blo0) << 2) | (((gy >> 2) - blo1) << 1) | ((gz >> 2) - blo2);
-    const int blk = __shfl_sync(0xffffffffu, myblk, bsel & 7);
-    if (!inb) continue;
-    double v[7];
-    bool any = false;
+      for (int ch = 0; ch < 7; ++ch) tile[ch][q_run] += (double)acc[ch];
+    __syncwarp();
+    // 5. flush: one atomic per (node, channel).  The tile spans at most 2
+    // blocks per axis (<= 8 blocks, nodes <= 10 per axis): lanes 0-7 resolve
+    // one block each through the hash table, the others read them by shuffle.
+    const int blo0 = lo[0] >> 2, blo1 = lo[1] >> 2, blo2 = lo[2] >> 2;
+    int myblk = -1;
+    if (lane < 8) {
+      int64_t bkey;
+      if (pack_block(blo0 + ((lane >> 2) & 1), blo1 + ((lane >> 1) & 1), blo2 + (lane & 1), &bkey))
+        myblk = hash_find(g.hkeys, g.hvals, g.mask, (uint64_t)bkey);
+    }
+    for (int q0 = 0; q0 < nnode; q0 += 32) {
+      const int q = q0 + lane;
+      const bool inb = q < nnode;
+      const int qz = inb ? q % nz : 0, qy = inb ? (q / nz) % ny : 0, qx = inb ? q / (nz * ny) : 0;
+      const int gx = lo[0] + qx, gy = lo[1] + qy, gz = lo[2] + qz;
+      const int bsel = (((gx >> 2) - blo0) << 2) | (((gy >> 2) - blo1) << 1) | ((gz >> 2) - blo2);
+      const int blk = __shfl_sync(0xffffffffu, myblk, bsel & 7);
+      if (!inb) continue;
+      double v[7];
+      bool any = false;
 #pragma unroll
-    for (int ch = 0; ch < 7; ++ch) {
-      v[ch] = tile[ch][q];
-      any |= v[ch] != 0.0;
-    }
-    if (!any) continue;
-    if (blk < 0) {
-      raise_status(st, MPMRB_E_ALLOCATION, 22, w0);
-      continue;
-    }
-    const long long node =
-        (long long)blk * kNodesPerBlock + (((gx & 3) << 4) | ((gy & 3) << 2) | (gz & 3));
-    atomicAdd(&gmass[node], v[0]);
+      for (int ch = 0; ch < 7; ++ch) {
+        v[ch] = tile[ch][q];
+        any |= v[ch] != 0.0;
+      }
+      if (!any) continue;
+      if (blk < 0) {
+        raise_status(st, MPMRB_E_ALLOCATION, 22, w0);
+        continue;
+      }
+      const long long node =
+          (long long)blk * kNodesPerBlock + (((gx & 3) << 4) | ((gy & 3) << 2) | (gz & 3));
+      atomicAdd(&gmass[node], v[0]);
 #pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      atomicAdd(&mom_apic[3 * node + d], v[1 + d]);
-      atomicAdd(&mom_force[3 * node + d], v[4 + d]);
+      for (int d = 0; d < 3; ++d) {
+        atomicAdd(&mom_apic[3 * node + d], v[1 + d]);
+        atomicAdd(&mom_force[3 * node + d], v[4 + d]);
+      }
     }
+    s0 = s1;
   }
 }
 
