@@ -115,6 +115,77 @@ __global__ void k_stresses(const double* __restrict__ f, const long long* __rest
   m3_store(tau + 9 * i, t);
 }
 
+constexpr int kWarpTile = 128;  // nodes per warp tile (e.g. 4 x 4 x 8)
+
+// A warp's particles, in lane order, are cut into segments of consecutive
+// lanes [s0, s1) whose stencils fit one node tile: <= kWarpTile nodes and <= 2
+// blocks per axis (so the tile's blocks resolve with <= 8 hash lookups).  A
+// warp inside one block is one segment; a warp straddling two blocks
+// (consecutive in key order, not necessarily adjacent in space) is two.  s1 is
+// the first lane whose prefix bounding box no longer fits: prefix boxes only
+// grow, and one stencil always fits, so s1 > s0.
+struct WarpSeg {
+  int s1, lo[3], nx, ny, nz;
+};
+__device__ __forceinline__ WarpSeg warp_segment(const int (&b)[3], bool live, int lane, int s0,
+                                                int n_live) {
+  const bool act = live && lane >= s0;
+  int mn[3], mx[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    mn[a] = act ? b[a] : INT_MAX;
+    mx[a] = act ? b[a] : INT_MIN;
+  }
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const int tn = __shfl_up_sync(0xffffffffu, mn[a], o);
+      const int tx = __shfl_up_sync(0xffffffffu, mx[a], o);
+      if (lane >= o) {
+        mn[a] = min(mn[a], tn);
+        mx[a] = max(mx[a], tx);
+      }
+    }
+  }
+  bool fits = true;
+  if (act) {
+    const int px = mx[0] - mn[0] + 3, py = mx[1] - mn[1] + 3, pz = mx[2] - mn[2] + 3;
+    fits = px * py * pz <= kWarpTile && (((mn[0] + px - 1) >> 2) - (mn[0] >> 2) <= 1) &&
+           (((mn[1] + py - 1) >> 2) - (mn[1] >> 2) <= 1) &&
+           (((mn[2] + pz - 1) >> 2) - (mn[2] >> 2) <= 1);
+  }
+  const unsigned bad = __ballot_sync(0xffffffffu, act && !fits);
+  WarpSeg sg;
+  sg.s1 = bad ? __ffs(bad) - 1 : n_live;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) sg.lo[a] = __shfl_sync(0xffffffffu, mn[a], sg.s1 - 1);
+  sg.nx = __shfl_sync(0xffffffffu, mx[0], sg.s1 - 1) - sg.lo[0] + 3;
+  sg.ny = __shfl_sync(0xffffffffu, mx[1], sg.s1 - 1) - sg.lo[1] + 3;
+  sg.nz = __shfl_sync(0xffffffffu, mx[2], sg.s1 - 1) - sg.lo[2] + 3;
+  return sg;
+}
+
+// The <= 8 blocks a tile with lower corner lo spans: lane l < 8 resolves block
+// lo/4 + (l>>2 & 1, l>>1 & 1, l & 1) through the hash table (-1 if absent);
+// the other lanes read them by shuffle (tile_block).
+__device__ __forceinline__ int tile_blocks(const GridDev& g, const int (&lo)[3], int lane) {
+  int myblk = -1;
+  if (lane < 8) {
+    int64_t bkey;
+    if (pack_block((lo[0] >> 2) + ((lane >> 2) & 1), (lo[1] >> 2) + ((lane >> 1) & 1),
+                   (lo[2] >> 2) + (lane & 1), &bkey))
+      myblk = hash_find(g.hkeys, g.hvals, g.mask, (uint64_t)bkey);
+  }
+  return myblk;
+}
+// block of grid cell (gx, gy, gz) in the tile (all lanes must call)
+__device__ __forceinline__ int tile_block(int myblk, const int (&lo)[3], int gx, int gy, int gz) {
+  const int bsel = (((gx >> 2) - (lo[0] >> 2)) << 2) | (((gy >> 2) - (lo[1] >> 2)) << 1) |
+                   ((gz >> 2) - (lo[2] >> 2));
+  return __shfl_sync(0xffffffffu, myblk, bsel & 7);
+}
+
 // P2G (mpm.py:66-99 with the stress of materials.py:113-122), warp-level.
 // Each warp takes 32 consecutive particles (the fused path sorts particles by
 // (block, cell) once per step, so a warp covers a few neighbouring cells):
@@ -157,8 +228,6 @@ __device__ __forceinline__ void load_payload(const T* rec, T (&q)[kPayW]) {
     for (int k = (kPayW / 4) * 4; k < kPayW; ++k) q[k] = rec[k];
   }
 }
-constexpr int kWarpTile = 128;  // nodes per warp tile (e.g. 4 x 4 x 8)
-
 // Per-particle P2G payload: m, m v, m C, S = -dt D^-1 V0 tau and the external
 // impulse dt f of cloth vertex forces.  Cloth roles (cloth.cu): vertex
 // particles carry no stress (their in-plane forces arrive in fext), element
@@ -298,48 +367,13 @@ __global__ void __launch_bounds__(kP2GThreads, MPMRB_P2G_MINB) k_p2g(GridDev g, 
   const int ox = lane / 9, oy = (lane / 3) % 3, oz = lane % 3;
   const T oxT = T(ox), oyT = T(oy), ozT = T(oz);
   const bool slot_lane = lane < 27;
-  // 2. segments: the warp's particles are cut into runs of consecutive lanes
-  // [s0, s1) whose stencils fit one node tile (<= kWarpTile nodes, <= 2
-  // blocks per axis for the flush lookup).  A warp inside one block is one
-  // segment; a warp straddling two blocks (consecutive in key order, not
-  // necessarily adjacent in space) is two.  s1 is the first lane whose prefix
-  // bounding box no longer fits (prefix boxes only grow).
+  // 2. segments of lanes whose stencils fit one node tile (warp_segment)
 #pragma unroll 1
   for (int s0 = 0; s0 < n_live;) {
     const bool act = live && lane >= s0;
-    int mn[3], mx[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      mn[a] = act ? b[a] : INT_MAX;
-      mx[a] = act ? b[a] : INT_MIN;
-    }
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        const int tn = __shfl_up_sync(0xffffffffu, mn[a], o);
-        const int tx = __shfl_up_sync(0xffffffffu, mx[a], o);
-        if (lane >= o) {
-          mn[a] = min(mn[a], tn);
-          mx[a] = max(mx[a], tx);
-        }
-      }
-    }
-    bool fits = true;
-    if (act) {
-      const int px = mx[0] - mn[0] + 3, py = mx[1] - mn[1] + 3, pz = mx[2] - mn[2] + 3;
-      fits = px * py * pz <= kWarpTile && (((mn[0] + px - 1) >> 2) - (mn[0] >> 2) <= 1) &&
-             (((mn[1] + py - 1) >> 2) - (mn[1] >> 2) <= 1) &&
-             (((mn[2] + pz - 1) >> 2) - (mn[2] >> 2) <= 1);
-    }
-    const unsigned bad = __ballot_sync(0xffffffffu, act && !fits);
-    const int s1 = bad ? __ffs(bad) - 1 : n_live;  // > s0: one stencil always fits
-    int lo[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) lo[a] = __shfl_sync(0xffffffffu, mn[a], s1 - 1);
-    const int nx = __shfl_sync(0xffffffffu, mx[0], s1 - 1) - lo[0] + 3;
-    const int ny = __shfl_sync(0xffffffffu, mx[1], s1 - 1) - lo[1] + 3;
-    const int nz = __shfl_sync(0xffffffffu, mx[2], s1 - 1) - lo[2] + 3;
+    const WarpSeg sg = warp_segment(b, live, lane, s0, n_live);
+    const int s1 = sg.s1, nx = sg.nx, ny = sg.ny, nz = sg.nz;
+    const int lo[3] = {sg.lo[0], sg.lo[1], sg.lo[2]};
     const int nnode = nx * ny * nz;
     // 3. zero the segment's node tile
     __syncwarp();
@@ -431,20 +465,13 @@ __global__ void __launch_bounds__(kP2GThreads, MPMRB_P2G_MINB) k_p2g(GridDev g, 
     // 5. flush: one atomic per (node, channel).  The tile spans at most 2
     // blocks per axis (<= 8 blocks, nodes <= 10 per axis): lanes 0-7 resolve
     // one block each through the hash table, the others read them by shuffle.
-    const int blo0 = lo[0] >> 2, blo1 = lo[1] >> 2, blo2 = lo[2] >> 2;
-    int myblk = -1;
-    if (lane < 8) {
-      int64_t bkey;
-      if (pack_block(blo0 + ((lane >> 2) & 1), blo1 + ((lane >> 1) & 1), blo2 + (lane & 1), &bkey))
-        myblk = hash_find(g.hkeys, g.hvals, g.mask, (uint64_t)bkey);
-    }
+    const int myblk = tile_blocks(g, lo, lane);
     for (int q0 = 0; q0 < nnode; q0 += 32) {
       const int q = q0 + lane;
       const bool inb = q < nnode;
       const int qz = inb ? q % nz : 0, qy = inb ? (q / nz) % ny : 0, qx = inb ? q / (nz * ny) : 0;
       const int gx = lo[0] + qx, gy = lo[1] + qy, gz = lo[2] + qz;
-      const int bsel = (((gx >> 2) - blo0) << 2) | (((gy >> 2) - blo1) << 1) | ((gz >> 2) - blo2);
-      const int blk = __shfl_sync(0xffffffffu, myblk, bsel & 7);
+      const int blk = tile_block(myblk, lo, gx, gy, gz);
       if (!inb) continue;
       double v[7];
       bool any = false;
@@ -523,43 +550,40 @@ __global__ void __launch_bounds__(128, MPMRB_G2P_MINB) k_g2p(GridDev g, Particle
   const bool live = i < p.n;
   bool was_clamped = false;
   const double h = g.h;
-  // Warp tile (as in k_p2g): the sorted particles of a warp gather from a
-  // shared-memory copy of the <= kWarpTile grid velocities their stencils
-  // cover, staged with one hash lookup per block; spread warps gather from
-  // global memory directly.
+  // Warp tile (as in k_p2g): each segment of the warp's sorted particles
+  // (warp_segment) gathers from a shared-memory copy of the <= kWarpTile grid
+  // velocities its stencils cover, staged with one hash lookup per block.
+  const int n_live = (int)max(0LL, min(32LL, p.n - (i - lane)));
   int b[3] = {0, 0, 0};
-  if (live)
+  double xp[3] = {0.0, 0.0, 0.0};
+  Stencil1T<T> s;
+  if (live) {
 #pragma unroll
-    for (int a = 0; a < 3; ++a) b[a] = (int)base_cell(p.x[3 * i + a], h);
-  int lo[3], hi[3];
+    for (int a = 0; a < 3; ++a) xp[a] = p.x[3 * i + a];
+    make_stencil1_t<T>(xp, h, s);
 #pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    lo[a] = __reduce_min_sync(0xffffffffu, live ? b[a] : INT_MAX);
-    hi[a] = __reduce_max_sync(0xffffffffu, live ? b[a] : INT_MIN);
+    for (int a = 0; a < 3; ++a) b[a] = (int)s.base[a];
   }
-  const int nx = hi[0] - lo[0] + 3, ny = hi[1] - lo[1] + 3, nz = hi[2] - lo[2] + 3;
-  const bool tiled = (long long)nx * ny * nz <= kWarpTile &&
-                     (((lo[0] + nx - 1) >> 2) - (lo[0] >> 2) <= 1) &&
-                     (((lo[1] + ny - 1) >> 2) - (lo[1] >> 2) <= 1) &&
-                     (((lo[2] + nz - 1) >> 2) - (lo[2] >> 2) <= 1);
   T (*tv)[kWarpTile] = s_v[wid];
-  if (tiled) {
-    const int blo0 = lo[0] >> 2, blo1 = lo[1] >> 2, blo2 = lo[2] >> 2;
-    int myblk = -1;
-    if (lane < 8) {
-      int64_t bkey;
-      if (pack_block(blo0 + ((lane >> 2) & 1), blo1 + ((lane >> 1) & 1), blo2 + (lane & 1),
-                     &bkey))
-        myblk = hash_find(g.hkeys, g.hvals, g.mask, (uint64_t)bkey);
-    }
+  const T hT = (T)h;
+  T vn[3] = {T(0), T(0), T(0)};
+  M3T<T> B;
+#pragma unroll
+  for (int k = 0; k < 9; ++k) B.a[k] = T(0);
+#pragma unroll 1
+  for (int s0 = 0; s0 < n_live;) {
+    const WarpSeg sg = warp_segment(b, live, lane, s0, n_live);
+    const int nx = sg.nx, ny = sg.ny, nz = sg.nz;
+    const int lo[3] = {sg.lo[0], sg.lo[1], sg.lo[2]};
+    const int myblk = tile_blocks(g, lo, lane);
     const int nnode = nx * ny * nz;
+    __syncwarp();  // the previous segment's gathers are done
     for (int q0 = 0; q0 < nnode; q0 += 32) {
       const int q = q0 + lane;
       const bool inb = q < nnode;
       const int qz = inb ? q % nz : 0, qy = inb ? (q / nz) % ny : 0, qx = inb ? q / (nz * ny) : 0;
       const int gx = lo[0] + qx, gy = lo[1] + qy, gz = lo[2] + qz;
-      const int bsel = (((gx >> 2) - blo0) << 2) | (((gy >> 2) - blo1) << 1) | ((gz >> 2) - blo2);
-      const int blk = __shfl_sync(0xffffffffu, myblk, bsel & 7);
+      const int blk = tile_block(myblk, lo, gx, gy, gz);
       if (!inb) continue;
       // nodes outside the allocated blocks are never in a live stencil
       const long long node =
@@ -568,24 +592,8 @@ __global__ void __launch_bounds__(128, MPMRB_G2P_MINB) k_g2p(GridDev g, Particle
       for (int d = 0; d < 3; ++d) tv[d][q] = blk < 0 ? T(0) : (T)v_next[3 * node + d];
     }
     __syncwarp();
-  }
-  if (live) {
-    double xp[3] = {p.x[3 * i], p.x[3 * i + 1], p.x[3 * i + 2]};
-    Stencil1T<T> s;
-    make_stencil1_t<T>(xp, h, s);
-    StencilBlocks sb;
-    bool ok = true;
-    if (!tiled) ok = resolve_blocks(s, g.hkeys, g.hvals, g.mask, sb);
-    if (!ok) {
-      raise_status(st, MPMRB_E_ALLOCATION, 30, i);
-    } else {
-      const T hT = (T)h;
-      T vn[3] = {T(0), T(0), T(0)};
-      M3T<T> B;
-#pragma unroll
-      for (int k = 0; k < 9; ++k) B.a[k] = T(0);
-      const int cb0 = (int)s.base[0] - lo[0], cb1 = (int)s.base[1] - lo[1],
-                cb2 = (int)s.base[2] - lo[2];
+    if (live && lane >= s0 && lane < sg.s1) {
+      const int cb0 = b[0] - lo[0], cb1 = b[1] - lo[1], cb2 = b[2] - lo[2];
 #pragma unroll 1
       for (int ox = 0; ox < 3; ++ox) {
         const T dx = (T(ox) - s.fx[0]) * hT;
@@ -597,20 +605,11 @@ __global__ void __launch_bounds__(128, MPMRB_G2P_MINB) k_g2p(GridDev g, Particle
           for (int oz = 0; oz < 3; ++oz) {
             const T dz = (T(oz) - s.fx[2]) * hT;
             const T w = wxy * s.w[2][oz];
-            T vv[3];
-            if (tiled) {
-              const int q = ((cb0 + ox) * ny + (cb1 + oy)) * nz + (cb2 + oz);
-#pragma unroll
-              for (int d = 0; d < 3; ++d) vv[d] = tv[d][q];
-            } else {
-              const int node = stencil_node(s, sb, ox, oy, oz);
-#pragma unroll
-              for (int d = 0; d < 3; ++d) vv[d] = (T)v_next[3 * node + d];
-            }
+            const int q = ((cb0 + ox) * ny + (cb1 + oy)) * nz + (cb2 + oz);
             T wv[3];
 #pragma unroll
             for (int d = 0; d < 3; ++d) {
-              wv[d] = w * vv[d];
+              wv[d] = w * tv[d][q];
               vn[d] += wv[d];
               B(d, 0) += wv[d] * dx;
               B(d, 1) += wv[d] * dy;
@@ -619,6 +618,11 @@ __global__ void __launch_bounds__(128, MPMRB_G2P_MINB) k_g2p(GridDev g, Particle
           }
         }
       }
+    }
+    s0 = sg.s1;
+  }
+  if (live) {
+    {
       const T dinv = (T)(4.0 / (h * h));
       M3T<T> C;
 #pragma unroll
