@@ -102,6 +102,10 @@ int mpmrb_create(int device, mpmrb_ctx** out) {
     return set_cuda_error(e, "cudaMalloc(status)", __FILE__, __LINE__);
   }
   cudaMemset(c->status, 0, sizeof(DevStatus));
+  if (cudaMalloc(&c->scan_state, 8 * (kOnePassMaxTiles + 2)) == cudaSuccess)
+    cudaMemset(c->scan_state, 0, 8 * (kOnePassMaxTiles + 2));
+  else
+    c->scan_state = nullptr;  // scans take the three-kernel path
   const char* prof = getenv("MPMRB_SOLVER_PROF");
   if (prof && atoi(prof) > 0) {
     if (cudaMalloc(&c->solver_prof, 8 * kSolverProfWords) == cudaSuccess)
@@ -143,6 +147,8 @@ int mpmrb_destroy(mpmrb_ctx* c) {
   cudaStreamSynchronize(c->stream);
   for (auto& b : c->scratch) b.release();
   if (c->status) cudaFree(c->status);
+  if (c->scan_state) cudaFree(c->scan_state);
+  if (c->solver_prof) cudaFree(c->solver_prof);
   delete c;
   return MPMRB_OK;
 }

@@ -117,13 +117,15 @@ __global__ void k_contact_count(const double* __restrict__ x, long long n,
 
 __global__ void k_contact_emit(const double* __restrict__ x, long long n,
                                const mpmrb_geom* __restrict__ geoms, int ngeom, double margin,
-                               const int* __restrict__ offs, const int* __restrict__ total,
+                               const int* __restrict__ cnt, const int* __restrict__ offs,
+                               const int* __restrict__ total,
                                long long cap, int* __restrict__ bias_stamp,
                                double* __restrict__ bias_store, const int* __restrict__ epoch_dev,
                                ContactArrays ca, DevStatus* st) {
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= n) return;
   if (i == 0 && *total > cap) raise_status(st, MPMRB_E_CAPACITY, 40, *total);
+  if (cnt[i] == 0) return;  // most particles touch no geometry: skip the second SDF pass
   int o = offs[i];
   double p[3] = {x[3 * i], x[3 * i + 1], x[3 * i + 2]};
   for (int g = 0; g < ngeom; ++g) {
@@ -213,8 +215,8 @@ int launch_detect(Ctx& c, const double* x, long long n, const mpmrb_geom* geoms_
   c.launches++;
   int rc = scan_exclusive_i32(c, cnt, offs, n, nullptr, total_dev, tiles);
   if (rc) return rc;
-  k_contact_emit<<<grid_for(n, 128), 128, 0, c.stream>>>(x, n, geoms_dev, ngeom, margin, offs,
-                                                         total_dev, cap, bias_stamp, bias_store,
+  k_contact_emit<<<grid_for(n, 128), 128, 0, c.stream>>>(x, n, geoms_dev, ngeom, margin, cnt,
+                                                         offs, total_dev, cap, bias_stamp, bias_store,
                                                          epoch_stamp_dev, ca, c.status);
   c.launches++;
   MPMRB_CUDA_OK(cudaGetLastError());

@@ -41,10 +41,16 @@ struct Ctx {
   DevBuf scratch[32];
   // phase timers of the solver kernel (enabled by MPMRB_SOLVER_PROF=1)
   unsigned long long* solver_prof = nullptr;
+  // single-pass scan state (scan.cu): [0] ticket | epoch, [1..] tile status;
+  // zeroed once at creation, never reset (epoch-tagged), so scans replay
+  // inside CUDA graphs
+  unsigned long long* scan_state = nullptr;
   int check_status(const char* where);  // sync + read + clear device status
 };
 
 // Scratch slot ids for API-level (non-fused) calls.
+constexpr int kOnePassMaxTiles = 8192;  // single-pass scans up to 64M elements
+
 enum ScratchSlot {
   SS_TILE = 0, SS_TILE2, SS_HIST, SS_KEYS, SS_TMP0, SS_TMP1, SS_TMP2, SS_TMP3, SS_COUNT,
   SS_SOLVER0, SS_SOLVER1, SS_SOLVER2, SS_SOLVER3, SS_SOLVER4, SS_SOLVER5, SS_SOLVER6,

@@ -1,5 +1,7 @@
-// Device-wide exclusive prefix sums (hand-written, three-phase: tile reduce,
-// single-CTA scan of tile sums, tile down-sweep).  Used for contact
+// Device-wide exclusive prefix sums, hand-written: int32 scans run single-pass
+// (decoupled look-back, k_scan_onepass); int64 scans and contexts without the
+// scan state run three-phase (tile reduce, single-CTA scan of tile sums, tile
+// down-sweep).  Used for contact
 // compaction (collision.py:88-132 ordering), active-node compaction
 // (solver.py:203-205) and the Morton counting sort (transfer.py:89).
 //
@@ -118,6 +120,112 @@ __global__ void __launch_bounds__(kScanThreads) k_tile_down(const T* __restrict_
   }
 }
 
+// Single-pass scan with decoupled look-back (int32): each CTA takes a tile by
+// ticket, publishes its aggregate, and warp 0 walks back over the preceding
+// tiles' status words until it meets an inclusive prefix.  A status word is
+// [epoch:30 | flag:2 | value:32]; the epoch is read before the ticket and
+// advanced by the CTA that takes the last ticket, so stale words of earlier
+// launches never match and nothing is reset between launches or graph replays.
+constexpr unsigned kStAgg = 1u, kStInc = 2u;
+__device__ __forceinline__ unsigned long long st_word(unsigned ep, unsigned flag, int v) {
+  return ((unsigned long long)(ep & 0x3fffffffu) << 34) | ((unsigned long long)flag << 32) |
+         (unsigned long long)(unsigned)v;
+}
+constexpr int kOpThreads = 256, kOpItems = 16;
+constexpr int kOpTile = kOpThreads * kOpItems;  // 4096
+__global__ void __launch_bounds__(kOpThreads) k_scan_onepass(const int* __restrict__ in,
+                                                             int* __restrict__ out,
+                                                             long long n_cap, const int* n_dev,
+                                                             int* total,
+                                                             unsigned long long* state) {
+  __shared__ int sm[kOpThreads / 32];
+  __shared__ int s_tile, s_prefix;
+  __shared__ unsigned s_epoch;
+  unsigned* ctrl = reinterpret_cast<unsigned*>(state);  // [0] ticket, [1] epoch
+  volatile unsigned long long* st = state + 1;
+  if (threadIdx.x == 0) {
+    const unsigned ep = *reinterpret_cast<volatile unsigned*>(ctrl + 1);
+    __threadfence();
+    const int t = (int)atomicAdd(ctrl, 1u);
+    if (t == (int)gridDim.x - 1) {  // every CTA holds its ticket and has read the epoch
+      __threadfence();
+      atomicExch(ctrl, 0u);
+      atomicAdd(ctrl + 1, 1u);
+    }
+    s_tile = t;
+    s_epoch = ep;
+  }
+  __syncthreads();
+  const int t = s_tile;
+  const unsigned ep = s_epoch & 0x3fffffffu;
+  const long long n = n_dev ? (long long)*n_dev : n_cap;
+  const long long base = (long long)t * kOpTile;
+  if (base >= n) {
+    if (t == 0 && threadIdx.x == 0 && total) *total = 0;
+    return;  // tiles are taken in order: no live tile waits on a dead one
+  }
+  // each warp owns a contiguous chunk of 32 x kOpItems elements, read and
+  // written in coalesced rounds of 32; round r's inclusive warp scan carries
+  // the running total of rounds < r
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const long long chunk = base + (long long)wid * (32 * kOpItems);
+  int v[kOpItems];
+#pragma unroll
+  for (int r = 0; r < kOpItems; ++r) {
+    const long long idx = chunk + r * 32 + lane;
+    v[r] = idx < n ? in[idx] : 0;
+  }
+  int run = 0;
+#pragma unroll
+  for (int r = 0; r < kOpItems; ++r) {
+    const int inc = warp_incl_scan(v[r]);
+    v[r] = run + inc - v[r];  // exclusive within the warp's chunk
+    run += __shfl_sync(0xffffffffu, inc, 31);
+  }
+  if (lane == 31) sm[wid] = run;
+  __syncthreads();
+  int tot = 0, woff = 0;
+#pragma unroll
+  for (int k = 0; k < kOpThreads / 32; ++k) {
+    const int x = sm[k];
+    woff += k < wid ? x : 0;
+    tot += x;
+  }
+  if (threadIdx.x == 0) st[t] = st_word(ep, t == 0 ? kStInc : kStAgg, tot);
+  if (t > 0 && wid == 0) {
+    int excl = 0;
+    for (int j = t - 1;; j -= 32) {
+      const int idx = j - lane;
+      unsigned long long w;
+      bool ready;
+      do {
+        w = idx >= 0 ? st[idx] : st_word(ep, kStInc, 0);
+        ready = (unsigned)(w >> 34) == ep && ((w >> 32) & 3u) != 0u;
+      } while (!__all_sync(0xffffffffu, ready));
+      const unsigned inc = __ballot_sync(0xffffffffu, ((w >> 32) & 3u) == kStInc);
+      const int first = inc ? __ffs(inc) - 1 : 32;  // nearest tile holding an inclusive prefix
+      int val = lane <= first ? (int)(unsigned)w : 0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+      excl += val;
+      if (inc) break;
+    }
+    if (lane == 0) {
+      st[t] = st_word(ep, kStInc, excl + tot);
+      s_prefix = excl;
+    }
+  }
+  __syncthreads();
+  const int off = (t > 0 ? s_prefix : 0) + woff;
+#pragma unroll
+  for (int r = 0; r < kOpItems; ++r) {
+    const long long idx = chunk + r * 32 + lane;
+    if (idx < n) out[idx] = off + v[r];
+  }
+  if (total && threadIdx.x == 0 && n - base <= kOpTile)  // the last live tile
+    *total = (t > 0 ? s_prefix : 0) + tot;
+}
+
 template <class T>
 int scan_impl(Ctx& c, const T* in, T* out, long long n_cap, const int* n_dev, T* total_dev,
               DevBuf& tiles) {
@@ -137,6 +245,14 @@ int scan_impl(Ctx& c, const T* in, T* out, long long n_cap, const int* n_dev, T*
 
 int scan_exclusive_i32(Ctx& c, const int* in, int* out, long long n_cap, const int* n_dev,
                        int* total_dev, DevBuf& tiles) {
+  const long long ntiles = n_cap > 0 ? (n_cap + kOpTile - 1) / kOpTile : 1;
+  if (c.scan_state && ntiles <= kOnePassMaxTiles) {
+    k_scan_onepass<<<(unsigned)ntiles, kOpThreads, 0, c.stream>>>(in, out, n_cap, n_dev,
+                                                                    total_dev, c.scan_state);
+    c.launches++;
+    MPMRB_CUDA_OK(cudaGetLastError());
+    return MPMRB_OK;
+  }
   return scan_impl<int>(c, in, out, n_cap, n_dev, total_dev, tiles);
 }
 
