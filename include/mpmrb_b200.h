@@ -271,6 +271,14 @@ int mpmrb_contact_model(mpmrb_ctx* ctx, const double* vc, const double* phi,
  * stops on the batch-wide maximum; the extra iterations change R only at
  * roundoff). */
 int mpmrb_polar_rotation(mpmrb_ctx* ctx, const double* f, int64_t n, double* r);
+/* Exclusive prefix sum of n int32 device values into out (device); *total
+ * (device, may be NULL) receives the sum.  The offsets behind the reference's
+ * compactions and counting sorts: np.flatnonzero in collision.py:105 (contact
+ * selection) and solver.py:202 (active nodes), the stable integer argsort of
+ * transfer.py:89.  Single pass (decoupled look-back) for n <= 2^25, in the
+ * context's stream; does not synchronise. */
+int mpmrb_scan_exclusive_i32(mpmrb_ctx* ctx, const int32_t* in, int64_t n, int32_t* out,
+                             int32_t* total);
 /* materials.py:57-67 inverse_transpose3 via the adjugate. */
 int mpmrb_inverse_transpose3(mpmrb_ctx* ctx, const double* m, int64_t n, double* out);
 /* solver.py:224-256 solve_search_direction: d = -H^-1 g for n SPD 3x3 blocks

@@ -159,6 +159,7 @@ _SIGS = {
     "mpmrb_sim_set_precision": ([_P, C.c_int32], C.c_int),
     "mpmrb_search_direction": ([_P, _P, _P, _I64, _P, C.POINTER(C.c_int32)], C.c_int),
     "mpmrb_polar_rotation": ([_P, _P, _I64, _P], C.c_int),
+    "mpmrb_scan_exclusive_i32": ([_P, _P, _I64, _P, _P], C.c_int),
     "mpmrb_inverse_transpose3": ([_P, _P, _I64, _P], C.c_int),
     "mpmrb_sim_begin_step": ([_P, _I64, C.c_int32], C.c_int),
     "mpmrb_sim_substep": ([_P], C.c_int),

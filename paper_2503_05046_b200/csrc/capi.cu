@@ -384,6 +384,14 @@ int mpmrb_polar_rotation(mpmrb_ctx* c, const double* f, int64_t n, double* r) {
   return c->check_status("polar_rotation");
 }
 
+int mpmrb_scan_exclusive_i32(mpmrb_ctx* c, const int32_t* in, int64_t n, int32_t* out,
+                             int32_t* total) {
+  CHECK_CTX(c);
+  if (n < 0 || (n > 0 && (!in || !out))) return set_error(MPMRB_E_INVALID, "scan: bad arguments");
+  if (n > (1LL << 31) - 1) return set_error(MPMRB_E_INVALID, "scan: n exceeds int32 range");
+  return scan_exclusive_i32(*c, in, out, n, nullptr, total, c->scratch[SS_TILE]);
+}
+
 int mpmrb_inverse_transpose3(mpmrb_ctx* c, const double* m, int64_t n, double* out) {
   CHECK_CTX(c);
   int rc = launch_polar(*c, m, n, 1, out);

@@ -49,7 +49,7 @@ struct Ctx {
 };
 
 // Scratch slot ids for API-level (non-fused) calls.
-constexpr int kOnePassMaxTiles = 8192;  // single-pass scans up to 64M elements
+constexpr int kOnePassMaxTiles = 8192;  // single-pass scans up to 2^25 elements (4096 per tile)
 
 enum ScratchSlot {
   SS_TILE = 0, SS_TILE2, SS_HIST, SS_KEYS, SS_TMP0, SS_TMP1, SS_TMP2, SS_TMP3, SS_COUNT,
