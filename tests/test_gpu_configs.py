@@ -240,7 +240,11 @@ def test_sand_loaded_substep_matches_oracle(mp, half, settle, name):
     is therefore also run on a permutation of the particles (same physics,
     another summation order), and the GPU's deviation from the oracle is
     held to the larger of 10x that deviation and a floor: world impulses 2e-2
-    of the largest, their total 1e-2, particle positions 1e-9 m."""
+    of the largest, their total 1e-2, particle positions 1e-7 m.  The x floor
+    is 1e-5 h, well inside what the stopping rule determines: a velocity
+    error of eps_r x 0.2 m/s over dt = 2e-4 s is 2e-6 m (one permutation of
+    the oracle has measured as little as 2e-9 m, and the fused path's
+    float64 atomics give the GPU a different roundoff seed every run)."""
     if os.environ.get("MPMRB_SKIP_LARGE"):
         pytest.skip("MPMRB_SKIP_LARGE set")
     d = _loaded_substep_parity(mp, half, settle, name)
@@ -248,6 +252,6 @@ def test_sand_loaded_substep_matches_oracle(mp, half, settle, name):
     assert d["mass"] <= 1e-12 and d["mom"] <= 1e-12
     assert d["gam"] <= max(2e-2, 10 * d["o_gam"])
     assert d["tot"] <= max(1e-2, 10 * d["o_tot"])
-    assert d["x"] <= max(1e-9, 10 * d["o_x"])
+    assert d["x"] <= max(1e-7, 10 * d["o_x"])
     assert d["fconv"] and d["fw"] <= max(1e-2, 10 * d["o_tot"])
-    assert d["fx"] <= max(1e-9, 10 * d["o_x"])
+    assert d["fx"] <= max(1e-7, 10 * d["o_x"])
