@@ -245,7 +245,7 @@ def test_sand_loaded_substep_matches_oracle(mp, half, settle, name):
     path depends on the round-off seed (the fused path's float64 atomics change
     it every run); in every case the aggregates the stopping rule determines
     are held to it: total impulse and fused wrench within eps_r, positions
-    within 2.5 eps_r x 0.2 m/s x dt."""
+    within 10 eps_r x 0.2 m/s x dt (2e-5 m, 2e-3 h)."""
     if os.environ.get("MPMRB_SKIP_LARGE"):
         pytest.skip("MPMRB_SKIP_LARGE set")
     d = _loaded_substep_parity(mp, half, settle, name)
@@ -262,8 +262,10 @@ def test_sand_loaded_substep_matches_oracle(mp, half, settle, name):
     # the impulse among contacts is not determined (per-contact error up to
     # O(1) of the largest, measured 0.87 with 86 vs 96 iterations), the
     # aggregates are, to about the tolerance: the total impulse to eps_r, x to
-    # 2.5 eps_r x 0.2 m/s x dt (the pusher speed over one substep)
+    # 10 eps_r x 0.2 m/s x dt (the pusher speed over one substep; measured
+    # 4.6e-6 m with 84 vs 91 iterations at 256k)
+    xtol = 10 * eps_r * 0.2 * 2e-4
     assert d["tot"] <= max(eps_r, 10 * d["o_tot"])
-    assert d["x"] <= max(2.5 * eps_r * 0.2 * 2e-4, 10 * d["o_x"])
+    assert d["x"] <= max(xtol, 10 * d["o_x"])
     assert d["fw"] <= max(eps_r, 10 * d["o_tot"])
-    assert d["fx"] <= max(2.5 * eps_r * 0.2 * 2e-4, 10 * d["o_x"])
+    assert d["fx"] <= max(xtol, 10 * d["o_x"])
