@@ -66,9 +66,11 @@ def particle_to_grid(particles: ParticleSet, grid: SparseGrid, stencil: Stencil 
     ``mode="deterministic"`` (the reference's default) materialises the
     (n, 27, 7) contributions and sums every node channel in particle-id /
     slot order (ordered scatter: bitwise reproducible, plan-independent);
-    ``mode="fast"`` is one fused stress + 27x7 scatter kernel with float64
-    atomics.  ``stencil`` is accepted for API compatibility; the kernels
-    recompute it from particles.x."""
+    ``mode="fast"`` is the fused path's kernel: stress, then warp-private
+    shared-memory node tiles flushed with one float64 atomic per (node,
+    channel), within the reference's fast-vs-deterministic bound.
+    ``stencil`` is accepted for API compatibility; the kernels recompute it
+    from particles.x."""
     if epoch != plan.epoch:
         raise PlanEpochError(f"plan epoch {plan.epoch} used in step {epoch}")
     if mode not in ("deterministic", "fast"):
