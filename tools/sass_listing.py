@@ -74,8 +74,9 @@ def main(out_dir: str = "profiles/sass") -> None:
             mix["total"] += 1
         reg, stack, shared = usage.get(mangled, (None, None, None))
         rows.append((name, mangled, reg, stack, shared, mix))
-        if any(name == h or name.startswith(h + "I") for h in HOT):
-            (out / f"{name}.sass").write_text(
+        if any(name == h or name.startswith(h + "I") or name.startswith(h + "<") for h in HOT):
+            fname = name.replace("<", "_").replace(">", "")
+            (out / f"{fname}.sass").write_text(
                 f"// {mangled}\n// sm_100a, from {LIB.name} (cuobjdump -sass, encodings stripped)\n"
                 + "\n".join(body) + "\n")
     lines = ["# SASS summary (sm_100a): registers, stack / shared bytes, instruction mix",
