@@ -126,6 +126,8 @@ __global__ void __launch_bounds__(kScanThreads) k_tile_down(const T* __restrict_
 // [epoch:30 | flag:2 | value:32]; the epoch is read before the ticket and
 // advanced by the CTA that takes the last ticket, so stale words of earlier
 // launches never match and nothing is reset between launches or graph replays.
+// (The epoch wraps after 2^30 launches on one context; a stale word could then
+// match only if no launch in between covered its tile.)
 constexpr unsigned kStAgg = 1u, kStInc = 2u;
 __device__ __forceinline__ unsigned long long st_word(unsigned ep, unsigned flag, int v) {
   return ((unsigned long long)(ep & 0x3fffffffu) << 34) | ((unsigned long long)flag << 32) |
