@@ -269,3 +269,44 @@ def test_sand_loaded_substep_matches_oracle(mp, half, settle, name):
     assert d["x"] <= max(xtol, 10 * d["o_x"])
     assert d["fw"] <= max(eps_r, 10 * d["o_tot"])
     assert d["fx"] <= max(xtol, 10 * d["o_x"])
+
+
+def test_tshirt_unconverged_solves_match_oracle(mp):
+    """configs[3] (the T-shirt fold) at 16^2 vertices, with its own contact
+    stiffness (1e5) and tolerance (eps_r = 5e-2), the sheet dropped onto the
+    table: the light cloth's contact solves stop at max_iters = 500 on the
+    GPU, and they do so on the oracle too, in the same substeps with the same
+    contact counts and iteration counts.  The unconverged solves of the
+    full-size bench scene (27 of 80 in its window) are therefore a property of
+    the reference algorithm on this scene, not of the port.  Positions agree
+    to 1e-5 m (1.3e-3 h; measured 4e-7 to 1.4e-6 m, the unconverged solves'
+    stopping points depend on the round-off seed); the wrench is not compared:
+    an unconverged solve leaves the split of the impulse undetermined (20-110%
+    apart here)."""
+    from oracle import step as ostep
+    from paper_2503_05046_b200 import scenes
+    sc = scenes.tshirt_fold_scene(n_side=16)
+    sc["cloth"][0]["center"] = [0.0, 0.0, 0.0012]
+    sc["cloth"][0]["velocity"] = [0.0, 0.0, -0.3]
+    st = scenes.build_state(sc)
+    p0 = st.particles.numpy()
+    ref = oracle_state(sc, p0["x"], p0["v"], p0["f"], p0["c"], p0["mass"], p0["volume0"],
+                       p0["material_id"])
+    rows = []
+    for i in range(3):
+        s = mp.advance_step(st)
+        r = ostep.step(ref)
+        dx = float(np.abs(np_(st.particles.x) - ref.x).max())
+        rows.append(dict(step=i, contacts=s.n_contacts_mean, iters_mean=s.iterations_mean,
+                         iters_max=s.iterations_max, converged=bool(s.all_converged),
+                         oracle_contacts=r["n_contacts_mean"],
+                         oracle_iters_mean=r["iterations_mean"],
+                         oracle_iters_max=r["iterations_max"],
+                         oracle_converged=bool(r["all_converged"]), dx=dx))
+        assert s.n_contacts_mean == r["n_contacts_mean"], i
+        assert s.iterations_max == r["iterations_max"], i
+        assert bool(s.all_converged) == bool(r["all_converged"]), i
+        assert abs(s.iterations_mean - r["iterations_mean"]) <= 0.02 * r["iterations_mean"], i
+        assert dx <= 1e-5, (i, dx)
+    assert any(not row["converged"] for row in rows)  # the case this test is about
+    _record("tshirt16_unconverged", steps=rows)
