@@ -681,7 +681,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_qn_solve(SolverArgs a) {
 
   // lanes per contact node in phase N: 4 (more entries in flight per node)
   // while the contact nodes fit in one pass of the grid, else 2 (twice the
-  // nodes in flight per warp; tools/gpu_ab.sh: 16.4 -> 10.7 us of N work per
+  // nodes in flight per warp; measured in round 1: 16.4 -> 10.7 us of N work per
   // iteration with 31k contact nodes, no change with 9k)
   const int NL = 4LL * n_cn > (long long)nctas * kThreads ? 2 : 4;
   int iterations = 0, ls_evals_total = 0, status = 0;
