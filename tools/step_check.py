@@ -5,7 +5,7 @@ stop there too?  This runs STEP steps on the GPU, then one more from that
 state on both, and prints both steps' solver summaries and the position
 difference.
 
-    python tools/unconverged_check.py [sand|sand1m|cloth] [STEP] > gpurun_out/unconverged_check.txt
+    python tools/step_check.py [sand|sand1m|cloth] [STEP] > gpurun_out/step_check.txt
 """
 import copy
 import importlib
