@@ -5,7 +5,9 @@ stop there too?  This runs STEP steps on the GPU, then one more from that
 state on both, and prints both steps' solver summaries and the position
 difference.
 
-    python tools/step_check.py [sand|sand1m|cloth] [STEP] > gpurun_out/step_check.txt
+    python tools/step_check.py WORKLOAD [STEP] [NSTEPS] > gpurun_out/step_check.txt
+
+NSTEPS > 1 continues both sides for NSTEPS steps (a trajectory comparison).
 """
 import copy
 import importlib
@@ -27,6 +29,7 @@ oracle_state = importlib.import_module("scenes").oracle_state  # tests/scenes.py
 def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "sand"
     nstep = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+    ncomp = int(sys.argv[3]) if len(sys.argv) > 3 else 1
     sc = bench.workload_scene(name)
     st = scenes.build_state(sc)
     for i in range(nstep):
@@ -43,20 +46,22 @@ def main():
         b.position, b.quat = gb.position.copy(), gb.quat.copy()
         b.v, b.omega = gb.v.copy(), gb.omega.copy()
     ref.time, ref.step_index = st.time, st.step_index
-    s1 = mp.advance_step(st)
-    print(f"step {nstep} gpu: contacts", s1.n_contacts_mean, "iters max", s1.iterations_max, "mean",
-          s1.iterations_mean, "converged", s1.all_converged,
-          "unconverged substeps", s1.substeps_unconverged, flush=True)
-    t0 = time.time()
-    r1 = ostep.step(ref)
-    print(f"step {nstep} oracle: contacts", r1["n_contacts_mean"], "iters max", r1["iterations_max"],
-          "mean", r1["iterations_mean"], "converged", r1["all_converged"],
-          f"({time.time() - t0:.0f} s)", flush=True)
-    if st.cloth is not None:
-        print("d3 max diff:", float(np.abs(st.cloth.d3.cpu().numpy() - ref.cloth.d3).max()))
-    print("wrench rel diff:", float(np.abs(s1.wrench - r1["wrench"]).max()
-                                    / max(np.abs(r1["wrench"]).max(), 1e-300)))
-    print(f"x max diff after step {nstep}:", float(np.abs(st.particles.numpy()["x"] - ref.x).max()))
+    for k in range(nstep, nstep + ncomp):
+        s1 = mp.advance_step(st)
+        print(f"step {k} gpu: contacts", s1.n_contacts_mean, "iters max", s1.iterations_max,
+              "mean", s1.iterations_mean, "converged", s1.all_converged,
+              "unconverged substeps", s1.substeps_unconverged, flush=True)
+        t0 = time.time()
+        r1 = ostep.step(ref)
+        print(f"step {k} oracle: contacts", r1["n_contacts_mean"], "iters max",
+              r1["iterations_max"], "mean", r1["iterations_mean"], "converged",
+              r1["all_converged"], f"({time.time() - t0:.0f} s)", flush=True)
+        if st.cloth is not None:
+            print("d3 max diff:", float(np.abs(st.cloth.d3.cpu().numpy() - ref.cloth.d3).max()))
+        print("wrench rel diff:", float(np.abs(s1.wrench - r1["wrench"]).max()
+                                        / max(np.abs(r1["wrench"]).max(), 1e-300)))
+        print(f"x max diff after step {k}:",
+              float(np.abs(st.particles.numpy()["x"] - ref.x).max()), flush=True)
 
 
 if __name__ == "__main__":
