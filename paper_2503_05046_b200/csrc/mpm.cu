@@ -179,6 +179,22 @@ __device__ __forceinline__ int tile_blocks(const GridDev& g, const int (&lo)[3],
   }
   return myblk;
 }
+// tile node q -> (qx, qy, qz) for a tile of nx x ny x nz nodes (z fastest),
+// dividing by multiply-shift: exact for q < 4096 and ny, nz <= 15 (a tile
+// spans at most 2 blocks, 10 nodes, per axis)
+struct TileDiv {
+  int ny, nz, my, mz;
+};
+__device__ __forceinline__ TileDiv tile_div(int ny, int nz) {
+  return TileDiv{ny, nz, (65536 + ny - 1) / ny, (65536 + nz - 1) / nz};
+}
+__device__ __forceinline__ void tile_coords(const TileDiv& d, int q, int& qx, int& qy, int& qz) {
+  const int a = (q * d.mz) >> 16;  // q / nz
+  qz = q - a * d.nz;
+  qx = (a * d.my) >> 16;  // a / ny
+  qy = a - qx * d.ny;
+}
+
 // block of grid cell (gx, gy, gz) in the tile (all lanes must call)
 __device__ __forceinline__ int tile_block(int myblk, const int (&lo)[3], int gx, int gy, int gz) {
   const int bsel = (((gx >> 2) - (lo[0] >> 2)) << 2) | (((gy >> 2) - (lo[1] >> 2)) << 1) |
@@ -345,7 +361,7 @@ __global__ void __launch_bounds__(kP2GThreads, MPMRB_P2G_MINB) k_p2g(GridDev g, 
                                                      DevStatus* st) {
   __shared__ double s_tile[kP2GThreads / 32][7][kWarpTile];
   __shared__ __align__(16) T s_pay[kP2GThreads / 32][16][kPayStride];  // 16 particles' payloads
-  __shared__ int4 s_cell[kP2GThreads / 32][16];  // their cells in the tile
+  __shared__ int s_cell[kP2GThreads / 32][16];  // their base cells' tile node index
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const long long w0 = ((long long)blockIdx.x * kP2GThreads) + wid * 32;
   if (w0 >= p.n) return;
@@ -375,6 +391,8 @@ __global__ void __launch_bounds__(kP2GThreads, MPMRB_P2G_MINB) k_p2g(GridDev g, 
     const int s1 = sg.s1, nx = sg.nx, ny = sg.ny, nz = sg.nz;
     const int lo[3] = {sg.lo[0], sg.lo[1], sg.lo[2]};
     const int nnode = nx * ny * nz;
+    const int slot_off = (ox * ny + oy) * nz + oz;  // this slot lane's node from the base cell's
+    const TileDiv td = tile_div(ny, nz);
     // 3. zero the segment's node tile
     __syncwarp();
     for (int q = lane; q < nnode; q += 32)
@@ -416,7 +434,7 @@ __global__ void __launch_bounds__(kP2GThreads, MPMRB_P2G_MINB) k_p2g(GridDev g, 
           rec[kPayK + k] = K[k];
           rec[kPayW + k] = s.w[k / 3][k % 3];
         }
-        s_cell[wid][lane & 15] = make_int4(b[0] - lo[0], b[1] - lo[1], b[2] - lo[2], 0);
+        s_cell[wid][lane & 15] = ((b[0] - lo[0]) * ny + (b[1] - lo[1])) * nz + (b[2] - lo[2]);
       }
       __syncwarp();
       if (slot_lane) {
@@ -440,8 +458,7 @@ __global__ void __launch_bounds__(kP2GThreads, MPMRB_P2G_MINB) k_p2g(GridDev g, 
             v[1 + d] = w * (q[kPayA + d] + (g[0] * oxT + g[1] * oyT + g[2] * ozT));
             v[4 + d] = w * (q[kPayB + d] + (k[0] * oxT + k[1] * oyT + k[2] * ozT));
           }
-          const int4 cr = s_cell[wid][r];
-          const int qn = ((cr.x + ox) * ny + (cr.y + oy)) * nz + (cr.z + oz);
+          const int qn = s_cell[wid][r] + slot_off;
           if (qn != q_run) {
             // the run changes on every slot lane at once (the cell changed)
             __syncwarp(0x07ffffffu);
@@ -469,7 +486,8 @@ __global__ void __launch_bounds__(kP2GThreads, MPMRB_P2G_MINB) k_p2g(GridDev g, 
     for (int q0 = 0; q0 < nnode; q0 += 32) {
       const int q = q0 + lane;
       const bool inb = q < nnode;
-      const int qz = inb ? q % nz : 0, qy = inb ? (q / nz) % ny : 0, qx = inb ? q / (nz * ny) : 0;
+      int qx = 0, qy = 0, qz = 0;
+      if (inb) tile_coords(td, q, qx, qy, qz);
       const int gx = lo[0] + qx, gy = lo[1] + qy, gz = lo[2] + qz;
       const int blk = tile_block(myblk, lo, gx, gy, gz);
       if (!inb) continue;
@@ -577,11 +595,13 @@ __global__ void __launch_bounds__(128, MPMRB_G2P_MINB) k_g2p(GridDev g, Particle
     const int lo[3] = {sg.lo[0], sg.lo[1], sg.lo[2]};
     const int myblk = tile_blocks(g, lo, lane);
     const int nnode = nx * ny * nz;
+    const TileDiv td = tile_div(ny, nz);
     __syncwarp();  // the previous segment's gathers are done
     for (int q0 = 0; q0 < nnode; q0 += 32) {
       const int q = q0 + lane;
       const bool inb = q < nnode;
-      const int qz = inb ? q % nz : 0, qy = inb ? (q / nz) % ny : 0, qx = inb ? q / (nz * ny) : 0;
+      int qx = 0, qy = 0, qz = 0;
+      if (inb) tile_coords(td, q, qx, qy, qz);
       const int gx = lo[0] + qx, gy = lo[1] + qy, gz = lo[2] + qz;
       const int blk = tile_block(myblk, lo, gx, gy, gz);
       if (!inb) continue;
@@ -593,7 +613,7 @@ __global__ void __launch_bounds__(128, MPMRB_G2P_MINB) k_g2p(GridDev g, Particle
     }
     __syncwarp();
     if (live && lane >= s0 && lane < sg.s1) {
-      const int cb0 = b[0] - lo[0], cb1 = b[1] - lo[1], cb2 = b[2] - lo[2];
+      const int cbq = ((b[0] - lo[0]) * ny + (b[1] - lo[1])) * nz + (b[2] - lo[2]);
 #pragma unroll 1
       for (int ox = 0; ox < 3; ++ox) {
         const T dx = (T(ox) - s.fx[0]) * hT;
@@ -601,11 +621,12 @@ __global__ void __launch_bounds__(128, MPMRB_G2P_MINB) k_g2p(GridDev g, Particle
         for (int oy = 0; oy < 3; ++oy) {
           const T dy = (T(oy) - s.fx[1]) * hT;
           const T wxy = s.w[0][ox] * s.w[1][oy];
+          const int qxy = cbq + (ox * ny + oy) * nz;
 #pragma unroll
           for (int oz = 0; oz < 3; ++oz) {
             const T dz = (T(oz) - s.fx[2]) * hT;
             const T w = wxy * s.w[2][oz];
-            const int q = ((cb0 + ox) * ny + (cb1 + oy)) * nz + (cb2 + oz);
+            const int q = qxy + oz;
             T wv[3];
 #pragma unroll
             for (int d = 0; d < 3; ++d) {
