@@ -16,16 +16,21 @@ once per step too, ``coupling.py:168-219``).  Each substep (``coupling.py:
    with a neighbour.  A block is shared by at most two ranks and IEEE addition
    commutes, so both copies of a shared node hold bitwise-identical sums and
    the grid update agrees on both sides.
-2. **Contact problem gather.**  The contact solve is latency-bound (DESIGN.md
-   §3): splitting its line search across GPUs would put a cross-GPU scalar
-   all-reduce in each of its ~500 reductions per substep.  Instead the contact
-   problem — contacts with their stencils keyed by global node coordinates,
-   the contact nodes' (m, v*, v_k), and three scalars per rank summarising its
-   contact-free active nodes — is gathered to rank 0 once per substep and
-   solved by ``quasi_newton_solve_ext``.  Contact-free nodes enter every
-   reduction of the solve in closed form (g = m (v - v*), H = m I), so the
-   global problem is exactly the single-scene one.
-3. **Solution scatter.**  Rank 0 broadcasts the contact-node velocities,
+2. **Contact solve**, one of two modes (``SlabState.solve``).
+   ``"gather0"`` (default): the contact solve is latency-bound (DESIGN.md
+   §3), so the contact problem -- contacts with their stencils keyed by global
+   node coordinates, the contact nodes' (m, v*, v_k), and three scalars per
+   rank summarising its contact-free active nodes -- is gathered to rank 0
+   once per substep and solved by the fused solver
+   (``quasi_newton_solve_ext``).  Contact-free nodes enter every reduction in
+   closed form (g = m (v - v*), H = m I), so the global problem is exactly
+   the single-scene one.
+   ``"allreduce"``: the solve runs on every rank (``_allreduce_solve``).
+   Contacts stay where they were detected, the contact-node state is
+   replicated, one vector all-reduce per iteration sums J^T dl/dv_c and the
+   Hessian blocks, and every line-search evaluation all-reduces the two
+   scalars phi'(alpha), phi''(alpha) (solver.py:301-325).
+3. **Solution scatter** (gather0 mode).  Rank 0 broadcasts the contact-node velocities,
    P = prod(1 - alpha) (free nodes finish at v* + P (v_k - v*)), the impulses
    and the solve report.  Reactions accumulate per rank; the step wrench is
    all-reduced, so every rank advances the (replicated) rigid bodies alike.
@@ -264,11 +269,16 @@ class SlabState:
     bounds: np.ndarray
     axis: int
     comm: Comm
+    solve: str = "gather0"     # contact solve: "gather0" (rank 0) or "allreduce" (all ranks)
 
     @staticmethod
-    def from_state(state: SimState, comm: Comm | None = None, axis: int = 0) -> "SlabState":
+    def from_state(state: SimState, comm: Comm | None = None, axis: int = 0,
+                   solve: str = "gather0") -> "SlabState":
         """Split a fully built (replicated) scene: every rank calls this with the
-        same ``state`` and keeps its slab's particles."""
+        same ``state`` and keeps its slab's particles.  ``solve`` picks the
+        distributed contact solve (module docstring, item 2)."""
+        if solve not in ("gather0", "allreduce"):
+            raise ValueError(f"unknown slab solve mode {solve!r}")
         comm = comm or Comm()
         p = state.particles
         x_axis = p.x[:, axis]
@@ -281,7 +291,7 @@ class SlabState:
                       h=state.h, step=state.step, contact_params=state.contact_params,
                       solver_params=state.solver_params, mode=state.mode, workers=state.workers)
         st.time, st.step_index = state.time, state.step_index
-        return SlabState(st, idx.clone(), bounds, axis, comm)
+        return SlabState(st, idx.clone(), bounds, axis, comm, solve)
 
     # -------------------------------------------------------------- migration
     def migrate(self) -> None:
@@ -322,7 +332,10 @@ class SlabState:
         lo, hi = self.bounds[self.comm.rank], self.bounds[self.comm.rank + 1]
         x = self.state.particles.x[:, self.axis]
         slack = (HALO_BLOCKS - 1) * BLOCK_EDGE * self.state.h
-        if x.numel() and (float(x.min()) < lo - slack or float(x.max()) >= hi + slack):
+        if not x.numel():
+            return
+        xmin, xmax = torch.stack([x.min(), x.max()]).tolist()   # one host sync
+        if xmin < lo - slack or xmax >= hi + slack:
             raise RuntimeError("slab decomposition: particles drifted beyond the halo band "
                                "within one step (reduce dt or widen HALO_BLOCKS)")
 
@@ -385,9 +398,11 @@ def _halo_reduce(ss: SlabState, grid: SparseGrid) -> torch.Tensor:
     return shared
 
 
-def _distributed_solve(ss: SlabState, grid, stencil, contacts, dt_s, block_shared):
-    """Gather the contact problem to rank 0, solve, scatter the solution.
-    Returns (v_next, gamma (local contacts, contact frame), report, owned)."""
+def _local_contact_problem(ss: SlabState, grid, stencil, contacts, dt_s, block_shared):
+    """The prologue both solve modes share: this rank's active nodes and their
+    ownership, its contacts' stencils keyed by global node coordinates, the
+    global contact-node set C (sorted keys, identical on every rank) and the
+    all-reduced (S0, Q0, Q1) of the contact-free owned nodes."""
     st, c = ss.state, ss.comm
     dev = grid.mass.device
     act = torch.nonzero(grid.active, as_tuple=False).reshape(-1)
@@ -410,36 +425,57 @@ def _distributed_solve(ss: SlabState, grid, stencil, contacts, dt_s, block_share
         skeys = torch.zeros((0, 27), dtype=torch.int64, device=dev)
         w = _lib.zeros((0, 27))
         cn = torch.zeros(0, dtype=torch.int64, device=dev)
-    # global contact-node set
     all_cn = c.allgather(keys_act[cn])
     C = torch.unique(torch.cat([k.to(dev) for k in all_cn]))     # sorted
     in_C = match_keys(C, keys_act) >= 0
     fm = owned & ~in_C
-    fs = free_sums(grid.mass[act][fm], grid.v_star[act][fm], grid.v_k[act][fm])
-    ext = c.sum(fs)
-    # contact records and contact-node records to rank 0
-    crec = torch.cat([contacts.frames.reshape(-1, 9), contacts.bias, contacts.phi[:, None],
-                      contacts.mu[:, None], contacts.gamma_lag[:, None], w], dim=1) \
-        if contacts.n else _lib.zeros((0, 9 + 3 + 3 + 27))
+    ext = c.sum(free_sums(grid.mass[act][fm], grid.v_star[act][fm], grid.v_k[act][fm]))
     nrec = torch.cat([grid.mass[act][cn][:, None], grid.v_star[act][cn], grid.v_k[act][cn]], dim=1)
+    return dict(act=act, keys_act=keys_act, owned=owned, skeys=skeys, w=w, cn=cn, all_cn=all_cn,
+                C=C, ext=ext, nrec=nrec)
+
+
+def _local_v_next(grid, lp, v_C, P):
+    """v_next on the local grid: contact nodes from the solution over C, every
+    other active node at v* + P (v_k - v*)."""
+    act, C = lp["act"], lp["C"]
+    v_next = _lib.zeros((grid.n_nodes, 3))
+    va = grid.v_star[act] + P * (grid.v_k[act] - grid.v_star[act])
+    pos = match_keys(C, lp["keys_act"])
+    hit = pos >= 0
+    va[hit] = v_C[pos[hit]]
+    v_next[act] = va
+    return v_next
+
+
+def _contact_records(contacts, w) -> torch.Tensor:
+    if not contacts.n:
+        return _lib.zeros((0, 9 + 3 + 3 + 27))
+    return torch.cat([contacts.frames.reshape(-1, 9), contacts.bias, contacts.phi[:, None],
+                      contacts.mu[:, None], contacts.gamma_lag[:, None], w], dim=1)
+
+
+def _distributed_solve(ss: SlabState, grid, stencil, contacts, dt_s, block_shared):
+    """solve="gather0": gather the contact problem to rank 0, solve it there
+    with the fused solver (free nodes in closed form), broadcast the solution.
+    Returns (v_next, gamma (local contacts, contact frame), report, owned)."""
+    st, c = ss.state, ss.comm
+    dev = grid.mass.device
+    lp = _local_contact_problem(ss, grid, stencil, contacts, dt_s, block_shared)
+    C, skeys = lp["C"], lp["skeys"]
+    crec = _contact_records(contacts, lp["w"])
     # the contact records go to rank 0 only; every rank needs the counts
     g_ck = c.gather0(skeys)
     g_cr = c.gather0(crec)
-    g_nk = all_cn
-    g_nr = c.gather0(nrec)
+    g_nk = lp["all_cn"]
+    g_nr = c.gather0(lp["nrec"])
     counts = [int(k) for k in c.allgather(torch.tensor([[skeys.shape[0]]], dtype=torch.int64))]
     if c.rank == 0:
         ck = torch.cat([k.to(dev) for k in g_ck])
         cr = torch.cat([r.to(dev) for r in g_cr])
         nk = torch.cat([k.to(dev) for k in g_nk])
         nr = torch.cat([r.to(dev) for r in g_nr])
-        first = match_keys(C, nk)                               # every record maps into C
-        m = torch.empty(C.shape[0], dtype=torch.float64, device=dev)
-        vs = torch.empty((C.shape[0], 3), dtype=torch.float64, device=dev)
-        v0 = torch.empty((C.shape[0], 3), dtype=torch.float64, device=dev)
-        m[first] = nr[:, 0]                                      # shared copies are identical
-        vs[first] = nr[:, 1:4]
-        v0[first] = nr[:, 4:7]
+        m, vs, v0 = _node_state(C, nk, nr)
         nodes = match_keys(C, ck.reshape(-1)).reshape(-1, 27).clamp(min=0)
         prob = ContactProblem(m=m, v_star=vs, v_init=v0, nodes=nodes, w=cr[:, 15:42].contiguous(),
                               frames=cr[:, 0:9].reshape(-1, 3, 3).contiguous(),
@@ -447,7 +483,7 @@ def _distributed_solve(ss: SlabState, grid, stencil, contacts, dt_s, block_share
                               mu=cr[:, 13].contiguous(), gamma_lag=cr[:, 14].contiguous(),
                               contact_params=st.contact_params, dt=dt_s)
         v_sol, gamma_all, report, P = quasi_newton_solve_ext(prob, st.solver_params,
-                                                             ext.tolist())
+                                                             lp["ext"].tolist())
         meta = torch.tensor([P, float(report.converged), float(report.iterations),
                              float(report.ls_evals), float(report.regularized)],
                             dtype=torch.float64, device=dev)
@@ -462,14 +498,127 @@ def _distributed_solve(ss: SlabState, grid, stencil, contacts, dt_s, block_share
     report = SolveReport(converged=bool(meta[1] > 0.5), iterations=int(meta[2]),
                          n_contacts=int(sum(counts)), n_dofs=3 * int(C.shape[0]),
                          ls_evals=int(meta[3]), regularized=int(meta[4]))
-    # v_next on the local grid
-    v_next = _lib.zeros((grid.n_nodes, 3))
-    va = grid.v_star[act] + P * (grid.v_k[act] - grid.v_star[act])
-    pos = match_keys(C, keys_act)
-    hit = pos >= 0
-    va[hit] = v_sol[pos[hit]]
-    v_next[act] = va
-    return v_next, gamma, report, owned
+    return _local_v_next(grid, lp, v_sol, P), gamma, report, lp["owned"]
+
+
+def _node_state(C, keys, recs):
+    """(m, v*, v0) over the sorted contact-node set C from (key, record) rows;
+    copies of a shared node are bitwise identical (P2G halo reduce)."""
+    dev = C.device
+    first = match_keys(C, keys)                                  # every record maps into C
+    m = torch.empty(C.shape[0], dtype=torch.float64, device=dev)
+    vs = torch.empty((C.shape[0], 3), dtype=torch.float64, device=dev)
+    v0 = torch.empty((C.shape[0], 3), dtype=torch.float64, device=dev)
+    m[first] = recs[:, 0]
+    vs[first] = recs[:, 1:4]
+    v0[first] = recs[:, 4:7]
+    return m, vs, v0
+
+
+def _ordered_scatter(nodes, vals, n_out: int) -> torch.Tensor:
+    """(nc, 27, k) per-slot values summed onto n_out nodes in contact order
+    (mpmrb_scatter_reduce_ordered)."""
+    out = torch.empty((n_out, vals.shape[2]), dtype=torch.float64, device=vals.device)
+    if n_out == 0:
+        return out
+    _lib.check(_lib.lib().mpmrb_scatter_reduce_ordered(
+        _lib.ctx(), _lib.ptr(nodes.contiguous()), _lib.ptr(vals.contiguous()), nodes.shape[0],
+        27, vals.shape[2], n_out, _lib.ptr(out)))
+    return out
+
+
+def _allreduce_solve(ss: SlabState, grid, stencil, contacts, dt_s, block_shared):
+    """solve="allreduce": the quasi-Newton solve of solver.py:328-382 spread
+    over the ranks.  Contacts stay on the rank that detected them; the state
+    of the global contact-node set C (m, v*, v) is replicated on every rank;
+    the contact-free nodes enter in closed form through (S0, Q0, Q1) and
+    P = prod(1 - alpha), as in the fused kernel (solver.cu free-node terms).
+    Per iteration one vector all-reduce sums the ranks' J^T dl/dv_c and
+    Hessian blocks over C (solver.py:127-167); every rank then forms the same
+    gradient, residual (solver.py:188-194) and block-Cholesky direction
+    (solver.py:224-256) redundantly.  Each exact line-search evaluation
+    (solver.py:266-325) all-reduces two scalars (the contact part of phi',
+    phi''), so every rank takes the same branch and alpha.
+    Returns (v_next, gamma (local contacts, contact frame), report, owned)."""
+    from .contact_model import contact_grad_hess, contact_impulses
+    from .collision import _contact_velocities_raw
+    from .solver import line_search, solve_search_direction
+    st, c = ss.state, ss.comm
+    sp, cp = st.solver_params, st.contact_params
+    dev = grid.mass.device
+    lp = _local_contact_problem(ss, grid, stencil, contacts, dt_s, block_shared)
+    C = lp["C"]
+    nC, nc = int(C.shape[0]), contacts.n
+    g_nr = c.allgather(lp["nrec"])
+    m, vs, v = _node_state(C, torch.cat([k.to(dev) for k in lp["all_cn"]]),
+                           torch.cat([r.to(dev) for r in g_nr]))
+    n_glob = int(c.sum(torch.tensor([nc], dtype=torch.int64)).item())
+    nodes = match_keys(C, lp["skeys"].reshape(-1)).reshape(-1, 27).clamp(min=0)
+    w = lp["w"]
+    if nc:
+        frames, bias = contacts.frames, contacts.bias
+        phi, gl, mu = contacts.phi, contacts.gamma_lag, contacts.mu
+    S0, Q0, Q1 = (float(x) for x in lp["ext"].tolist())
+
+    def contact_terms(v):
+        """vc of the local contacts and their (J^T g_c | H_c) over C, (nC, 12)."""
+        if not nc:
+            return None, torch.zeros((nC, 12), dtype=torch.float64, device=dev)
+        vc = _contact_velocities_raw(nodes, w, frames, bias, v)
+        g_c, big_g = contact_grad_hess(vc, phi, gl, mu, cp, dt_s)
+        gw = torch.einsum("ci,cij->cj", g_c, frames)                      # R^T g_c
+        rgr = frames.transpose(1, 2) @ big_g @ frames
+        vals = torch.cat([w[:, :, None] * gw[:, None, :],
+                          (w * w)[:, :, None] * rgr.reshape(-1, 1, 9)], dim=2)
+        return vc, _ordered_scatter(nodes, vals, nC)
+
+    P, it, evals, reg, converged = 1.0, 0, 0, 0, False
+    while True:
+        vc, loc = contact_terms(v)
+        tot = c.sum(loc)                                 # the per-iteration vector all-reduce
+        jt, hc = tot[:, :3], tot[:, 3:]
+        e = v - vs
+        g = m[:, None] * e + jt
+        p2s = P * P * S0
+        s = torch.stack([(g * g / m[:, None]).sum(), (m[:, None] * v * v).sum(),
+                         (jt * jt / m[:, None]).sum()]).tolist() if nC else [0.0, 0.0, 0.0]
+        residual = float(np.sqrt(s[0] + p2s))
+        threshold = sp.eps_a + sp.eps_r * max(np.sqrt(s[1] + Q0 + 2.0 * P * Q1 + p2s),
+                                              np.sqrt(s[2]))
+        if it >= sp.max_iters:
+            converged = residual < threshold
+            break
+        if residual < (threshold if it > 0 else sp.eps_a):   # test-last, solver.py:339-345
+            converged = True
+            break
+        h = torch.diag_embed(m[:, None].expand(-1, 3).contiguous()) + hc.reshape(-1, 3, 3)
+        d = solve_search_direction(h, g) if nC else torch.zeros_like(v)
+        md = m[:, None] * d
+        a1 = float((e * md).sum()) - p2s                 # free nodes: d = -P e0
+        a2 = float((d * md).sum()) + p2s
+        dvc = (torch.einsum("cij,cj->ci", frames, torch.einsum("ck,ckd->cd", w, d[nodes]))
+               if nc else None)
+
+        def deriv(alpha: float):
+            part = torch.zeros(2, dtype=torch.float64, device=dev)
+            if nc:
+                g_a, big_a = contact_grad_hess(vc + alpha * dvc, phi, gl, mu, cp, dt_s)
+                part = torch.stack([(g_a * dvc).sum(),
+                                    (dvc * torch.einsum("cij,cj->ci", big_a, dvc)).sum()])
+            tot2 = c.sum(part).tolist()                  # the line search's scalar all-reduce
+            return a1 + a2 * alpha + tot2[0], a2 + tot2[1]
+
+        ls = line_search(deriv, max_iters=sp.ls_max_iters, tol=sp.ls_tol)
+        v = v + ls.alpha * d
+        P *= 1.0 - ls.alpha
+        it += 1
+        evals += ls.evals
+    if not bool(torch.isfinite(v).all()):
+        raise FloatingPointError("contact solve produced non-finite velocities")
+    gamma = contact_impulses(vc, phi, gl, mu, cp, dt_s) if nc else _lib.zeros((0, 3))
+    report = SolveReport(converged=converged, iterations=it, n_contacts=n_glob, n_dofs=3 * nC,
+                         ls_evals=evals, regularized=reg)
+    return _local_v_next(grid, lp, v, P), gamma, report, lp["owned"]
 
 
 def slab_substep(ss: SlabState, dt_s: float, plan, epoch: int) -> dict:
@@ -490,19 +639,18 @@ def slab_substep(ss: SlabState, dt_s: float, plan, epoch: int) -> dict:
         coords = node_coords(grid.block_coords, act)
         owned = node_owned(coords[:, ss.axis], shared[act // BLOCK_NODES], ss.bounds, c.rank,
                            st.h)
-        report = SolveReport(converged=True, n_contacts=0,
-                             n_dofs=3 * int(c.sum(torch.tensor([int(owned.sum())])).item()))
+        report = SolveReport(converged=True, n_contacts=0)
     else:
-        grid.v_next, gamma, report, owned = _distributed_solve(ss, grid, stencil, contacts, dt_s,
-                                                               shared)
+        solve = _allreduce_solve if ss.solve == "allreduce" else _distributed_solve
+        grid.v_next, gamma, report, owned = solve(ss, grid, stencil, contacts, dt_s, shared)
         if contacts.n:
             gamma_world = torch.einsum("ci,cij->cj", gamma, contacts.frames)
             bpos = torch.as_tensor(np.stack([np.asarray(b.position) for b in st.bodies]),
                                    dtype=torch.float64, device=gamma.device)
             st._accum.add_reactions(contacts.body, gamma_world, contacts.witness - bpos[contacts.body])
     clamped = grid_to_particle(p, grid, stencil, dt_s, st.materials)
-    n_active = int(c.sum(torch.tensor([int(owned.sum())], dtype=torch.int64)).item())
-    return dict(n_contacts=n_glob, report=report, clamped=clamped, n_active=n_active)
+    # per-rank statistics stay local; slab_advance_step reduces them once per step
+    return dict(n_contacts=n_glob, report=report, clamped=clamped, n_active=owned.sum())
 
 
 def slab_advance_step(ss: SlabState) -> StepSummary:
@@ -527,6 +675,13 @@ def slab_advance_step(ss: SlabState) -> StepSummary:
         conv &= info["report"].converged
         clamped += info["clamped"]
     dt = st.step.dt
+    # one all-reduce of the step's per-rank statistics (active nodes per
+    # substep, clamped gradients) instead of one per substep
+    stats = torch.cat([torch.stack(acts).to(torch.float64).cpu(),
+                       torch.tensor([float(clamped)], dtype=torch.float64)])
+    stats = c.sum(stats)
+    acts = [int(a) for a in stats[:-1].tolist()]
+    clamped = int(stats[-1].item())
     acc = torch.as_tensor(np.concatenate([st._accum.linear, st._accum.angular], axis=1))
     acc = c.sum(acc).numpy()
     nb = len(st.bodies)
@@ -538,7 +693,6 @@ def slab_advance_step(ss: SlabState) -> StepSummary:
     stale = torch.tensor([plan_staleness(plan, p.x, st.h) * p.n, float(p.n)], dtype=torch.float64)
     stale = c.sum(stale)
     n_tot = int(stale[1].item())
-    clamped = int(c.sum(torch.tensor([int(clamped)], dtype=torch.int64)).item())
     summary = StepSummary(step_index=st.step_index, time=new_time, n_particles=n_tot,
                           n_active_nodes=float(np.mean(acts)),
                           n_contacts_mean=float(np.mean(ncs)), n_contacts_max=int(np.max(ncs)),

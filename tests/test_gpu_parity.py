@@ -629,14 +629,14 @@ def _slab_scene(world=2):
     return sc
 
 
-def _slab_worker(rank, world, port, out, steps):
+def _slab_worker(rank, world, port, out, steps, solve="gather0"):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2503_05046_b200 import scenes, slab
     st = scenes.build_state(_slab_scene(world))
-    ss = slab.SlabState.from_state(st)
+    ss = slab.SlabState.from_state(st, solve=solve)
     n_local0 = ss.state.particles.n
     sums = [slab.slab_advance_step(ss) for _ in range(steps)]
     allp = slab.gather_particles(ss)
@@ -652,13 +652,16 @@ def _slab_worker(rank, world, port, out, steps):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world", [2, 3])
-def test_slab_decomposition_matches_single_scene(mp, tmp_path, world):
+@pytest.mark.parametrize("world,solve", [(2, "gather0"), (3, "gather0"), (2, "allreduce"),
+                                         (3, "allreduce")])
+def test_slab_decomposition_matches_single_scene(mp, tmp_path, world, solve):
     """Two slab ranks (gloo, sharing cuda:0) advance one scene: P2G halo reduce
     across the slab bound, the contact problem gathered to rank 0 and solved
     with the ranks' contact-free nodes in closed form, impulses scattered back.
     The result must match the single-scene run of the same operators
-    (advance_step_ops) up to reduction-order roundoff."""
+    (advance_step_ops) up to reduction-order roundoff.  solve="allreduce":
+    the contact solve runs on every rank with a vector all-reduce per
+    iteration and a scalar all-reduce per line-search evaluation."""
     import socket
 
     import torch.multiprocessing as tmp
@@ -669,7 +672,7 @@ def test_slab_decomposition_matches_single_scene(mp, tmp_path, world):
     port = s.getsockname()[1]
     s.close()
     out = str(tmp_path / "slab.npz")
-    tmp.spawn(_slab_worker, args=(world, port, out, steps), nprocs=world, join=True)
+    tmp.spawn(_slab_worker, args=(world, port, out, steps, solve), nprocs=world, join=True)
     r = np.load(out)
     st = scenes.build_state(_slab_scene(world))
     n = st.particles.n

@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=1)
     ap.add_argument("--backend", default=None)
+    ap.add_argument("--solve", default="gather0", choices=("gather0", "allreduce"))
     a = ap.parse_args()
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
@@ -39,7 +40,7 @@ def main():
     from paper_2503_05046_b200 import scenes, slab
     sc = bench.workload_scene(a.workload, 0)
     st = scenes.build_state(sc)
-    ss = slab.SlabState.from_state(st)
+    ss = slab.SlabState.from_state(st, solve=a.solve)
     for _ in range(a.warmup):
         slab.slab_advance_step(ss)
     torch.cuda.synchronize()
@@ -59,7 +60,7 @@ def main():
     if rank == 0:
         print(json.dumps(dict(metric="MPM particle-substeps/sec incl. convex contact solve",
                               value=n * sc["substeps"] / (ms * 1e-3), unit="particle-substeps/s",
-                              n_gpus=world, decomposition="slab", backend=backend,
+                              n_gpus=world, decomposition="slab", backend=backend, solve=a.solve,
                               steps=a.steps, warmup=a.warmup, ms_per_step=ms,
                               wall_s=time.perf_counter() - t0,
                               config=dict(workload=a.workload, particles=n,
