@@ -400,6 +400,44 @@ int mpmrb_sim_last_grid(mpmrb_sim* sim, int64_t* n_blocks_host, const int64_t** 
 int mpmrb_sim_last_contacts(mpmrb_sim* sim, int64_t* n_host, const int32_t** particle,
                             const double** gamma_world);
 
+/* ---------------------------------------------------- slab decomposition hooks
+ * slab.py's fused mode runs each substep in parts so that the exchanges of a
+ * slab-decomposed scene sit between them: part 0 = grid build + P2G; (P2G
+ * halo reduce on the grid channels); part 1 = grid update, active compaction,
+ * contact detection and preparation; part 2 = the contact solve, or instead
+ * the distributed solve writing v_next and gamma through the views and
+ * mpmrb_sim_set_solve_result; part 3 = reactions, substep end, G2P.
+ * Parts 0..3 in order are mpmrb_sim_substep with direct launches. */
+typedef struct {
+  int64_t n_blocks, n_active, n_contacts;   /* device counters, read back */
+  int64_t nc_cap;                            /* row stride of cnodes / cw */
+  const int64_t* block_keys;  /* (n_blocks,) sorted packed block keys (grid.py:26-31) */
+  double* mass;               /* (n_blocks*64,) node = block rank * 64 + (lx*4+ly)*4+lz */
+  double* mom_apic;           /* (n_blocks*64, 3) */
+  double* mom_force;          /* (n_blocks*64, 3) */
+  const double* v_star;       /* (n_blocks*64, 3), valid after part 1 */
+  const double* v_k;          /* (n_blocks*64, 3) */
+  double* v_next;             /* (n_blocks*64, 3), read by part 3's G2P */
+  const int32_t* act;         /* (n_active,) node index of each active node, ascending */
+  const double* m_act;        /* (n_active,) m, v*, v_k of the active nodes */
+  const double* v_star_act;   /* (n_active, 3) */
+  const double* v_k_act;      /* (n_active, 3) */
+  const int32_t* cnodes;      /* (27, nc_cap) active index of each stencil slot, -1 dead */
+  const double* cw;           /* (27, nc_cap) stencil weight, 0 for dead slots */
+  const double* frames;       /* (n_contacts, 3, 3) contact frames */
+  const double* bias;         /* (n_contacts, 3) */
+  const double* phi;          /* (n_contacts,) */
+  const double* mu;           /* (n_contacts,) */
+  const double* gamma_lag;    /* (n_contacts,) */
+  double* gamma;              /* (n_contacts, 3) contact-frame impulses (part 3 reads) */
+} mpmrb_sim_views;
+int mpmrb_sim_substep_part(mpmrb_sim* sim, int32_t part);
+/* Synchronises the sim's stream and reads the counters back. */
+int mpmrb_sim_get_views(mpmrb_sim* sim, mpmrb_sim_views* out);
+/* The report of a solve done outside part 2 (iterations, convergence, line-
+ * search evaluations) for the step statistics. */
+int mpmrb_sim_set_solve_result(mpmrb_sim* sim, const mpmrb_solve_report* report);
+
 #ifdef __cplusplus
 }
 #endif

@@ -107,6 +107,16 @@ class StepStats(C.Structure):
 _P = C.c_void_p
 _I64 = C.c_int64
 _D = C.c_double
+class SimViews(C.Structure):
+    """mpmrb_sim_views (include/mpmrb_b200.h): the fused substep's internal
+    grid and contact arrays, for slab.py's fused mode."""
+    _fields_ = [("n_blocks", C.c_int64), ("n_active", C.c_int64), ("n_contacts", C.c_int64),
+                ("nc_cap", C.c_int64)] + [(k, C.c_void_p) for k in (
+                    "block_keys", "mass", "mom_apic", "mom_force", "v_star", "v_k", "v_next",
+                    "act", "m_act", "v_star_act", "v_k_act", "cnodes", "cw", "frames", "bias",
+                    "phi", "mu", "gamma_lag", "gamma")]
+
+
 _SIGS = {
     "mpmrb_abi_version": ([], C.c_int),
     "mpmrb_last_error": ([], C.c_char_p),
@@ -169,6 +179,9 @@ _SIGS = {
     "mpmrb_sim_last_grid":([_P, C.POINTER(_I64), C.POINTER(_P), C.POINTER(_P), C.POINTER(_P),
                              C.POINTER(_P)], C.c_int),
     "mpmrb_sim_last_contacts": ([_P, C.POINTER(_I64), C.POINTER(_P), C.POINTER(_P)], C.c_int),
+    "mpmrb_sim_substep_part": ([_P, C.c_int32], C.c_int),
+    "mpmrb_sim_get_views": ([_P, C.POINTER(SimViews)], C.c_int),
+    "mpmrb_sim_set_solve_result": ([_P, C.POINTER(SolveReportC)], C.c_int),
 }
 
 EXPORTED = tuple(_SIGS)

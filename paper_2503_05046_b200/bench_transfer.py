@@ -3,11 +3,14 @@
 
 Same payload as the reference: n particles uniform in a 64h cube (seed 0),
 the sparse grid and 27-node stencils, values ~ N(0, 1) of shape (n, 27, 7);
-then the 7-channel scatter timed per call.  Modes (same CSV columns as the
-reference):
-  deterministic / fast  — scatter_reduce through the library (float64
-                          atomics; both modes take the same GPU path),
-  naive                 — torch index_add_ (a plain library scatter),
+then the 7-channel scatter timed per call (CUDA events).  Modes (same CSV
+columns as the reference, cli.py:60-82):
+  deterministic / fast  — scatter_reduce: the ordered segmented fold, each
+                          (node, channel) summed in particle-id order, bitwise
+                          the reference's deterministic result
+                          (transfer.py:135-145); both modes take this path,
+  naive                 — scatter_naive: one float64 atomic per contribution
+                          (transfer.py:251-260's per-row baseline),
 and the relative difference against the deterministic result.
 
     python -m paper_2503_05046_b200.bench_transfer --particles 100000 [--mode all]
@@ -41,21 +44,18 @@ def main(argv=None) -> int:
     ap.add_argument("--mode", choices=["deterministic", "fast", "naive", "all"], default="all")
     ap.add_argument("--repeats", type=int, default=20)
     args = ap.parse_args(argv)
-    from .transfer import build_sort_plan, scatter_reduce
+    from .transfer import build_sort_plan, scatter_naive, scatter_reduce
     n = args.particles
     grid, stencil, values, pos, h = payload(n)
     plan = build_sort_plan(pos, h, epoch=0)
     modes = ["deterministic", "fast", "naive"] if args.mode == "all" else [args.mode]
     ref = scatter_reduce(stencil.nodes, values, grid.n_nodes, plan, 0, mode="deterministic")
     scale = float(ref.abs().max())
-    idx = stencil.nodes.reshape(-1)
-    flat = values.reshape(-1, 7)
     print("mode,particles,workers,ms_per_scatter,rel_diff_vs_deterministic")
     for mode in modes:
         def run():
             if mode == "naive":
-                out = torch.zeros((grid.n_nodes, 7), dtype=torch.float64, device="cuda")
-                return out.index_add_(0, idx, flat)
+                return scatter_naive(stencil.nodes, values, grid.n_nodes)
             return scatter_reduce(stencil.nodes, values, grid.n_nodes, plan, 0, mode=mode)
         out = run()
         torch.cuda.synchronize()

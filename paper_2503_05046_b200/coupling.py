@@ -166,6 +166,37 @@ def _stream_of(state: SimState) -> torch.cuda.Stream:
     return state._stream
 
 
+def _configure_sim(state: SimState, sim, dt_s: float) -> None:
+    """Hand the state's particles, materials, cloth, bodies and parameters to
+    the fused simulator (on the state's stream; advance_step and slab.py)."""
+    L = _lib.lib()
+    p = state.particles
+    nb = len(state.bodies)
+    pv = p.view()
+    _lib.check(L.mpmrb_sim_set_precision(
+        sim, _lib.PREC_F32 if state.precision == "f32" else _lib.PREC_F64))
+    _lib.check(L.mpmrb_sim_set_particles(sim, C.byref(pv)))
+    tab, nm = material_table(state.materials)
+    _lib.check(L.mpmrb_sim_set_materials(sim, tab, nm))
+    cl = state.cloth
+    if cl is not None and cl.n_elements > 0:
+        _lib.check(L.mpmrb_sim_set_cloth(sim, cl.n_elements, _lib.ptr(cl.tri),
+                                         _lib.ptr(cl.epart), _lib.ptr(cl.dm_inv),
+                                         _lib.ptr(cl.vol), _lib.ptr(cl.d3),
+                                         _lib.ptr(cl.role)))
+    else:
+        _lib.check(L.mpmrb_sim_set_cloth(sim, 0, None, None, None, None, None, None))
+    gs = geom_structs(state.bodies)
+    garr = (_lib.Geom * max(1, len(gs)))(*gs)
+    _lib.check(L.mpmrb_sim_set_geoms(sim, garr, len(gs), nb))
+    cp, sp = state.contact_params, state.solver_params
+    g = (C.c_double * 3)(*[float(a) for a in state.step.gravity])
+    spc = sp.to_struct()
+    _lib.check(L.mpmrb_sim_set_params(sim, float(state.h), float(dt_s), g,
+                                      float(cp.stiffness), float(cp.tau_d), float(cp.eps_v),
+                                      float(state.margin), C.byref(spc)))
+
+
 STAGES = ("grid_build", "p2g", "grid_update", "contacts", "solve", "reactions", "g2p")
 
 
@@ -189,29 +220,7 @@ def advance_step(state: SimState, profile: dict | None = None) -> StepSummary:
     imp = (C.c_double * (6 * max(nb, 1)))()
     with torch.cuda.stream(stream):
         _lib.bind_stream(state._ctx, stream)
-        pv = p.view()
-        _lib.check(L.mpmrb_sim_set_precision(
-            sim, _lib.PREC_F32 if state.precision == "f32" else _lib.PREC_F64))
-        _lib.check(L.mpmrb_sim_set_particles(sim, C.byref(pv)))
-        tab, nm = material_table(state.materials)
-        _lib.check(L.mpmrb_sim_set_materials(sim, tab, nm))
-        cl = state.cloth
-        if cl is not None and cl.n_elements > 0:
-            _lib.check(L.mpmrb_sim_set_cloth(sim, cl.n_elements, _lib.ptr(cl.tri),
-                                             _lib.ptr(cl.epart), _lib.ptr(cl.dm_inv),
-                                             _lib.ptr(cl.vol), _lib.ptr(cl.d3),
-                                             _lib.ptr(cl.role)))
-        else:
-            _lib.check(L.mpmrb_sim_set_cloth(sim, 0, None, None, None, None, None, None))
-        gs = geom_structs(state.bodies)
-        garr = (_lib.Geom * max(1, len(gs)))(*gs)
-        _lib.check(L.mpmrb_sim_set_geoms(sim, garr, len(gs), nb))
-        cp, sp = state.contact_params, state.solver_params
-        g = (C.c_double * 3)(*[float(a) for a in state.step.gravity])
-        spc = sp.to_struct()
-        _lib.check(L.mpmrb_sim_set_params(sim, float(state.h), float(dt_s), g,
-                                          float(cp.stiffness), float(cp.tau_d), float(cp.eps_v),
-                                          float(state.margin), C.byref(spc)))
+        _configure_sim(state, sim, dt_s)
         rc = L.mpmrb_sim_begin_step(sim, epoch, n)
         if rc == _lib.E_DIVERGED:
             raise SimulationDiverged(

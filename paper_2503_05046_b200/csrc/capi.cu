@@ -804,6 +804,49 @@ int mpmrb_sim_substep(mpmrb_sim* s) {
   return s->substep();
 }
 
+int mpmrb_sim_substep_part(mpmrb_sim* s, int32_t part) {
+  if (!s) return set_error(MPMRB_E_INVALID, "null sim");
+  return s->substep_part(part);
+}
+
+int mpmrb_sim_get_views(mpmrb_sim* s, mpmrb_sim_views* v) {
+  if (!s || !v) return set_error(MPMRB_E_INVALID, "null sim or views");
+  int hc[3] = {0, 0, 0};
+  MPMRB_CUDA_OK(cudaStreamSynchronize(s->ctx->stream));
+  MPMRB_CUDA_OK(cudaMemcpy(hc, s->b_counters.p, sizeof(hc), cudaMemcpyDeviceToHost));
+  const long long N = s->nb_cap * kNodesPerBlock;
+  const long long cap = s->nc_cap;
+  v->n_blocks = hc[0];
+  v->n_active = hc[1];
+  v->n_contacts = hc[2] < cap ? hc[2] : cap;
+  v->nc_cap = cap;
+  v->block_keys = (const int64_t*)s->b_bkeys.p;
+  v->mass = s->b_mass.as<double>();
+  v->mom_apic = s->b_mom.as<double>();
+  v->mom_force = s->b_mom.as<double>() + 3 * N;
+  v->v_star = s->b_vstar.as<double>();
+  v->v_k = s->b_vk.as<double>();
+  v->v_next = s->b_vnext.as<double>();
+  v->act = s->b_act.as<int>();
+  v->m_act = s->b_mc.as<double>();
+  v->v_star_act = s->b_vstarc.as<double>();
+  v->v_k_act = s->b_vkc.as<double>();
+  v->cnodes = s->b_cnodes.as<int>();
+  v->cw = s->b_cw.as<double>();
+  v->frames = s->b_cframes.as<double>();
+  v->bias = s->b_cbias.as<double>();
+  v->phi = s->b_cphi.as<double>();
+  v->mu = s->b_cmu.as<double>();
+  v->gamma_lag = s->b_cgl.as<double>();
+  v->gamma = s->b_gamma.as<double>();
+  return MPMRB_OK;
+}
+
+int mpmrb_sim_set_solve_result(mpmrb_sim* s, const mpmrb_solve_report* r) {
+  if (!s || !r) return set_error(MPMRB_E_INVALID, "null sim or report");
+  return s->set_solve_result(r->converged, r->iterations, r->ls_evals, r->regularized);
+}
+
 int mpmrb_sim_end_step(mpmrb_sim* s, mpmrb_step_stats* st, double* impulses) {
   if (!s) return set_error(MPMRB_E_INVALID, "null sim");
   int rc = s->end_step(st, impulses);

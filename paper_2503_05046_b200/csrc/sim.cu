@@ -230,6 +230,18 @@ __global__ void k_reset_solveout(SolveOut* so) {
   }
 }
 
+__global__ void k_set_solveout(SolveOut* so, int converged, int iterations, int ls_evals,
+                               int regularized) {
+  if (threadIdx.x == 0) {
+    so->converged = converged;
+    so->iterations = iterations;
+    so->ls_evals = ls_evals;
+    so->regularized = regularized;
+    so->status = 0;
+    so->status_flags = 0;
+  }
+}
+
 long long next_pow2(long long v) {
   long long p = 1;
   while (p < v) p <<= 1;
@@ -350,12 +362,27 @@ int Sim::reserve(long long n, long long nb_needed) {
   return MPMRB_OK;
 }
 
-int Sim::capture_or_launch() {
+int Sim::capture_or_launch(int part_lo, int part_hi) {
   Ctx& c = *ctx;
+  // parts (mpmrb_sim_substep_part): 0 grid + P2G, 1 grid update + contacts,
+  // 2 contact solve, 3 reactions + G2P
+  auto in = [&](int k) { return part_lo <= k && k <= part_hi; };
   long long N = nb_cap * kNodesPerBlock;
   int* counters = b_counters.as<int>();  // [0] nb, [1] n_act, [2] nc, [3] substep idx
   GridDev g{b_hkeys.as<unsigned long long>(), b_hvals.as<int>(), (unsigned)(hash_cap - 1), h};
   int rc;
+  double* mom_apic = b_mom.as<double>();
+  double* mom_force = mom_apic + 3 * N;
+  ContactArrays ca{};
+  ca.particle = b_cpart.as<int>();
+  ca.body = b_cbody.as<int>();
+  ca.phi = b_cphi.as<double>();
+  ca.normal = b_cnormal.as<double>();
+  ca.witness = b_cwit.as<double>();
+  ca.frames = b_cframes.as<double>();
+  ca.bias = b_cbias.as<double>();
+  ca.mu = b_cmu.as<double>();
+  if (in(0)) {
   mark(0);
   // 1. grid (grid.py:71-103)
   rc = launch_grid_build(c, q.x, n_particles, h, b_bkeys.as<long long>(), nb_cap,
@@ -366,8 +393,6 @@ int Sim::capture_or_launch() {
   // 2. P2G (mpm.py:66-99)
   MPMRB_CUDA_OK(cudaMemsetAsync(b_mass.p, 0, 8 * N, c.stream));
   MPMRB_CUDA_OK(cudaMemsetAsync(b_mom.p, 0, 8 * 6 * N, c.stream));
-  double* mom_apic = b_mom.as<double>();
-  double* mom_force = mom_apic + 3 * N;
   if (cloth.ne > 0) {  // cloth forces before the transfer (cloth.cu)
     rc = launch_cloth_forces(c, cloth, q, b_mats.as<mpmrb_material>(), nmat);
     if (rc) return rc;
@@ -378,6 +403,8 @@ int Sim::capture_or_launch() {
            : launch_p2g(c, g, q, b_mats.as<mpmrb_material>(), nmat, dt_s, b_mass.as<double>(),
                         mom_apic, mom_force);
   if (rc) return rc;
+  }
+  if (in(1)) {
   mark(2);
   // 3. grid update + ordered active compaction (mpm.py:102-115, solver.py:203-205)
   rc = launch_grid_update(c, N, counters + 0, b_mass.as<double>(), mom_apic, mom_force, gravity[0],
@@ -395,15 +422,6 @@ int Sim::capture_or_launch() {
   c.launches++;
   mark(3);
   // 4. contacts (collision.py:88-132)
-  ContactArrays ca{};
-  ca.particle = b_cpart.as<int>();
-  ca.body = b_cbody.as<int>();
-  ca.phi = b_cphi.as<double>();
-  ca.normal = b_cnormal.as<double>();
-  ca.witness = b_cwit.as<double>();
-  ca.frames = b_cframes.as<double>();
-  ca.bias = b_cbias.as<double>();
-  ca.mu = b_cmu.as<double>();
   rc = launch_detect(c, q.x, n_particles, b_geoms.as<mpmrb_geom>(), ngeom, margin,
                      b_cnt.as<int>(), b_offs.as<int>(), counters + 2, b_tiles, nc_cap,
                      b_bias_stamp.as<int>(), b_bias_store.as<double>(), b_dyn.as<int>(), ca);
@@ -413,6 +431,8 @@ int Sim::capture_or_launch() {
       b_remap.as<int>(), K, den, b_cnodes.as<int>(), b_cw.as<double>(), b_cgl.as<double>(),
       c.status);
   c.launches++;
+  }
+  if (in(2)) {
   mark(4);
   // 5. quasi-Newton solve on the device (solver.py:328-382)
   k_reset_solveout<<<1, 32, 0, c.stream>>>(b_solveout.as<SolveOut>());
@@ -489,6 +509,8 @@ int Sim::capture_or_launch() {
   a.v_next_full = b_vnext.as<double>();
   rc = launch_qn_solve(c, a, 0);
   if (rc) return rc;
+  }
+  if (in(3)) {
   mark(5);
   k_reactions<<<kReactCtas, kReactThreads, 0, c.stream>>>(
       counters, b_gamma.as<double>(), ca.frames, ca.witness, ca.body, b_geoms.as<mpmrb_geom>(),
@@ -511,6 +533,7 @@ int Sim::capture_or_launch() {
     if (rc) return rc;
   }
   mark(7);
+  }
   MPMRB_CUDA_OK(cudaGetLastError());
   return MPMRB_OK;
 }
@@ -743,6 +766,20 @@ int Sim::substep() {
   NvtxRange r("mpmrb substep (graph)");
   MPMRB_CUDA_OK(cudaGraphLaunch(graph_exec, c.stream));
   c.launches += kernels_per_substep;
+  return MPMRB_OK;
+}
+
+int Sim::substep_part(int part) {
+  if (part < 0 || part > 3) return set_error(MPMRB_E_INVALID, "substep part must be 0..3");
+  NvtxRange r("mpmrb substep part");
+  return capture_or_launch(part, part);
+}
+
+int Sim::set_solve_result(int converged, int iterations, int ls_evals, int regularized) {
+  k_set_solveout<<<1, 32, 0, ctx->stream>>>(b_solveout.as<SolveOut>(), converged, iterations,
+                                            ls_evals, regularized);
+  ctx->launches++;
+  MPMRB_CUDA_OK(cudaGetLastError());
   return MPMRB_OK;
 }
 

@@ -65,7 +65,9 @@ struct Sim {
   void mark(int k);
   int profile_substep(float* stage_ms, int* sizes);
   int reserve(long long n, long long nb_needed);
-  int capture_or_launch();
+  int capture_or_launch(int part_lo = 0, int part_hi = 3);
+  int substep_part(int part);
+  int set_solve_result(int converged, int iterations, int ls_evals, int regularized);
   int begin_step(long long epoch, int n_substeps);
   int substep();
   int end_step(mpmrb_step_stats* out, double* impulses_host);

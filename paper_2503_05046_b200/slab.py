@@ -25,7 +25,7 @@ once per step too, ``coupling.py:168-219``).  Each substep (``coupling.py:
    (``quasi_newton_solve_ext``).  Contact-free nodes enter every reduction in
    closed form (g = m (v - v*), H = m I), so the global problem is exactly
    the single-scene one.
-   ``"allreduce"``: the solve runs on every rank (``_allreduce_solve``).
+   ``"allreduce"``: the solve runs on every rank (``_solve_allreduce``).
    Contacts stay where they were detected, the contact-node state is
    replicated, one vector all-reduce per iteration sums J^T dl/dv_c and the
    Hessian blocks, and every line-search evaluation all-reduces the two
@@ -49,13 +49,16 @@ on device tensors under NCCL.
 
 from __future__ import annotations
 
+import ctypes as C
 from dataclasses import dataclass
+from types import SimpleNamespace
 
 import numpy as np
 import torch
 import torch.distributed as dist
 
 from . import _lib
+from . import coupling as _coupling
 from .collision import BiasCache, contact_velocities, detect_contacts
 from .contact_model import normal_impulse
 from .coupling import ImpulseAccumulator, SimState, StepSummary, _rigid_update
@@ -364,19 +367,29 @@ def _unpack_particles(t: torch.Tensor, device):
 def _halo_reduce(ss: SlabState, grid: SparseGrid) -> torch.Tensor:
     """Sum the node channels of blocks shared with neighbours; returns the
     per-block "shared" mask."""
+    return _halo_sum(ss, grid.block_keys, grid.mass, grid.mom_apic, grid.mom_force)
+
+
+def _halo_sum(ss: SlabState, block_keys, mass, mom_apic, mom_force) -> torch.Tensor:
+    """_halo_reduce on raw channel arrays ((nb*64,), (nb*64, 3), (nb*64, 3),
+    updated in place): the operator pipeline's grid or the fused simulator's."""
     c = ss.comm
-    shared = torch.zeros(grid.n_blocks, dtype=torch.bool, device=grid.block_keys.device)
-    if c.world == 1 or grid.n_blocks == 0:
+    nb = int(block_keys.shape[0])
+    shared = torch.zeros(nb, dtype=torch.bool, device=block_keys.device)
+    if c.world == 1 or nb == 0:
         return shared
-    bc = grid.block_coords
-    ch = torch.cat([grid.mass.view(-1, BLOCK_NODES, 1), grid.mom_apic.view(-1, BLOCK_NODES, 3),
-                    grid.mom_force.view(-1, BLOCK_NODES, 3)], dim=2)  # (nb, 64, 7)
+    k = block_keys
+    msk = (1 << 21) - 1
+    bc = torch.stack([(k >> 42) - COORD_BIAS, ((k >> 21) & msk) - COORD_BIAS,
+                      (k & msk) - COORD_BIAS], dim=1)
+    ch = torch.cat([mass.view(-1, BLOCK_NODES, 1), mom_apic.reshape(-1, BLOCK_NODES, 3),
+                    mom_force.reshape(-1, BLOCK_NODES, 3)], dim=2)  # (nb, 64, 7)
 
     def band_payload(side):
         idx = torch.nonzero(halo_band(bc[:, ss.axis], ss.bounds, c.rank, ss.state.h, side),
                             as_tuple=False).reshape(-1)
         # one row per block: packed key (as float64 bits) + 64 x 7 channels
-        key = grid.block_keys[idx].view(torch.float64)[:, None]
+        key = block_keys[idx].view(torch.float64)[:, None]
         return torch.cat([key, ch[idx].reshape(-1, BLOCK_NODES * 7)], dim=1)
 
     # each band goes to the one neighbour that can share it (point-to-point)
@@ -386,30 +399,49 @@ def _halo_reduce(ss: SlabState, grid: SparseGrid) -> torch.Tensor:
         if got is None or got.numel() == 0:
             continue
         got = got.to(ch.device)
-        pos = match_keys(grid.block_keys, got[:, 0].contiguous().view(torch.int64))
+        pos = match_keys(block_keys, got[:, 0].contiguous().view(torch.int64))
         hit = pos >= 0
         if bool(hit.any()):
             add[pos[hit]] += got[hit, 1:].reshape(-1, BLOCK_NODES, 7)
             shared[pos[hit]] = True
     ch = ch + add
-    grid.mass.copy_(ch[:, :, 0].reshape(-1))
-    grid.mom_apic.copy_(ch[:, :, 1:4].reshape(-1, 3))
-    grid.mom_force.copy_(ch[:, :, 4:7].reshape(-1, 3))
+    mass.copy_(ch[:, :, 0].reshape(-1))
+    mom_apic.copy_(ch[:, :, 1:4].reshape(-1, 3))
+    mom_force.copy_(ch[:, :, 4:7].reshape(-1, 3))
     return shared
 
 
-def _local_contact_problem(ss: SlabState, grid, stencil, contacts, dt_s, block_shared):
-    """The prologue both solve modes share: this rank's active nodes and their
-    ownership, its contacts' stencils keyed by global node coordinates, the
+def _contact_problem(ss: SlabState, act, coords, owned, loc, w, m_a, vs_a, vk_a) -> dict:
+    """The part of the distributed contact problem both solve modes share:
+    this rank's contacts' stencils keyed by global node coordinates (``loc``:
+    (nc, 27) active-node index or -1 for a dead slot, ``w`` zero there), the
     global contact-node set C (sorted keys, identical on every rank) and the
-    all-reduced (S0, Q0, Q1) of the contact-free owned nodes."""
-    st, c = ss.state, ss.comm
+    all-reduced (S0, Q0, Q1) of the contact-free owned nodes.  ``m_a``,
+    ``vs_a``, ``vk_a``: m, v*, v_k of the active nodes."""
+    c = ss.comm
+    keys_act = pack_coords(coords)
+    dead = loc < 0
+    skeys = torch.where(dead, torch.full_like(loc, -1), keys_act[loc.clamp(min=0)])
+    cn = torch.unique(loc[~dead])
+    all_cn = c.allgather(keys_act[cn])
+    C = torch.unique(torch.cat([k.to(act.device) for k in all_cn]))     # sorted
+    in_C = match_keys(C, keys_act) >= 0
+    fm = owned & ~in_C
+    ext = c.sum(free_sums(m_a[fm], vs_a[fm], vk_a[fm]))
+    nrec = torch.cat([m_a[cn][:, None], vs_a[cn], vk_a[cn]], dim=1)
+    return dict(act=act, keys_act=keys_act, owned=owned, skeys=skeys, w=w, cn=cn,
+                all_cn=all_cn, C=C, ext=ext, nrec=nrec)
+
+
+def _local_contact_problem(ss: SlabState, grid, stencil, contacts, dt_s, block_shared):
+    """_contact_problem from the operator pipeline's grid, stencil and contacts
+    (also sets the contacts' lagged normal impulse, contact_model.py:50-55)."""
+    st = ss.state
     dev = grid.mass.device
     act = torch.nonzero(grid.active, as_tuple=False).reshape(-1)
     coords = node_coords(grid.block_coords, act)
-    keys_act = pack_coords(coords)
-    owned = node_owned(coords[:, ss.axis], block_shared[act // BLOCK_NODES], ss.bounds, c.rank,
-                       st.h)
+    owned = node_owned(coords[:, ss.axis], block_shared[act // BLOCK_NODES], ss.bounds,
+                       ss.comm.rank, st.h)
     remap = torch.full((grid.n_nodes,), -1, dtype=torch.int64, device=dev)
     remap[act] = torch.arange(act.shape[0], device=dev)
     if contacts.n:
@@ -417,53 +449,47 @@ def _local_contact_problem(ss: SlabState, grid, stencil, contacts, dt_s, block_s
         contacts.gamma_lag = normal_impulse(vcs[:, 2], contacts.phi, st.contact_params, dt_s)
         loc = remap[stencil.nodes[contacts.particle]]          # (nc,27) active index or -1
         w = stencil.weights[contacts.particle].clone()
-        dead = loc < 0
-        w[dead] = 0.0
-        skeys = torch.where(dead, torch.full_like(loc, -1), keys_act[loc.clamp(min=0)])
-        cn = torch.unique(loc[~dead])
+        w[loc < 0] = 0.0
     else:
-        skeys = torch.zeros((0, 27), dtype=torch.int64, device=dev)
+        loc = torch.zeros((0, 27), dtype=torch.int64, device=dev)
         w = _lib.zeros((0, 27))
-        cn = torch.zeros(0, dtype=torch.int64, device=dev)
-    all_cn = c.allgather(keys_act[cn])
-    C = torch.unique(torch.cat([k.to(dev) for k in all_cn]))     # sorted
-    in_C = match_keys(C, keys_act) >= 0
-    fm = owned & ~in_C
-    ext = c.sum(free_sums(grid.mass[act][fm], grid.v_star[act][fm], grid.v_k[act][fm]))
-    nrec = torch.cat([grid.mass[act][cn][:, None], grid.v_star[act][cn], grid.v_k[act][cn]], dim=1)
-    return dict(act=act, keys_act=keys_act, owned=owned, skeys=skeys, w=w, cn=cn, all_cn=all_cn,
-                C=C, ext=ext, nrec=nrec)
+    return _contact_problem(ss, act, coords, owned, loc, w, grid.mass[act], grid.v_star[act],
+                            grid.v_k[act])
+
+
+def _active_v_next(vs_a, vk_a, lp, v_C, P):
+    """v_next of the active nodes: contact nodes from the solution over C,
+    every other one at v* + P (v_k - v*)."""
+    va = vs_a + P * (vk_a - vs_a)
+    pos = match_keys(lp["C"], lp["keys_act"])
+    hit = pos >= 0
+    va[hit] = v_C[pos[hit]]
+    return va
 
 
 def _local_v_next(grid, lp, v_C, P):
-    """v_next on the local grid: contact nodes from the solution over C, every
-    other active node at v* + P (v_k - v*)."""
-    act, C = lp["act"], lp["C"]
+    act = lp["act"]
     v_next = _lib.zeros((grid.n_nodes, 3))
-    va = grid.v_star[act] + P * (grid.v_k[act] - grid.v_star[act])
-    pos = match_keys(C, lp["keys_act"])
-    hit = pos >= 0
-    va[hit] = v_C[pos[hit]]
-    v_next[act] = va
+    v_next[act] = _active_v_next(grid.v_star[act], grid.v_k[act], lp, v_C, P)
     return v_next
 
 
-def _contact_records(contacts, w) -> torch.Tensor:
-    if not contacts.n:
+def _contact_records(cts, w) -> torch.Tensor:
+    if not cts.n:
         return _lib.zeros((0, 9 + 3 + 3 + 27))
-    return torch.cat([contacts.frames.reshape(-1, 9), contacts.bias, contacts.phi[:, None],
-                      contacts.mu[:, None], contacts.gamma_lag[:, None], w], dim=1)
+    return torch.cat([cts.frames.reshape(-1, 9), cts.bias, cts.phi[:, None],
+                      cts.mu[:, None], cts.gamma_lag[:, None], w], dim=1)
 
 
-def _distributed_solve(ss: SlabState, grid, stencil, contacts, dt_s, block_shared):
+def _solve_gather0(ss: SlabState, lp: dict, cts, dt_s):
     """solve="gather0": gather the contact problem to rank 0, solve it there
     with the fused solver (free nodes in closed form), broadcast the solution.
-    Returns (v_next, gamma (local contacts, contact frame), report, owned)."""
+    ``cts``: this rank's contacts (n, frames, bias, phi, mu, gamma_lag).
+    Returns (v over C, P, gamma (local contacts, contact frame), report)."""
     st, c = ss.state, ss.comm
-    dev = grid.mass.device
-    lp = _local_contact_problem(ss, grid, stencil, contacts, dt_s, block_shared)
+    dev = lp["act"].device
     C, skeys = lp["C"], lp["skeys"]
-    crec = _contact_records(contacts, lp["w"])
+    crec = _contact_records(cts, lp["w"])
     # the contact records go to rank 0 only; every rank needs the counts
     g_ck = c.gather0(skeys)
     g_cr = c.gather0(crec)
@@ -494,11 +520,11 @@ def _distributed_solve(ss: SlabState, grid, stencil, contacts, dt_s, block_share
     gamma_all = c.bcast(gamma_all).to(dev)
     P = float(meta[0])
     start = sum(counts[: c.rank])
-    gamma = gamma_all[start: start + contacts.n]
+    gamma = gamma_all[start: start + cts.n]
     report = SolveReport(converged=bool(meta[1] > 0.5), iterations=int(meta[2]),
                          n_contacts=int(sum(counts)), n_dofs=3 * int(C.shape[0]),
                          ls_evals=int(meta[3]), regularized=int(meta[4]))
-    return _local_v_next(grid, lp, v_sol, P), gamma, report, lp["owned"]
+    return v_sol, P, gamma, report
 
 
 def _node_state(C, keys, recs):
@@ -527,7 +553,7 @@ def _ordered_scatter(nodes, vals, n_out: int) -> torch.Tensor:
     return out
 
 
-def _allreduce_solve(ss: SlabState, grid, stencil, contacts, dt_s, block_shared):
+def _solve_allreduce(ss: SlabState, lp: dict, cts, dt_s):
     """solve="allreduce": the quasi-Newton solve of solver.py:328-382 spread
     over the ranks.  Contacts stay on the rank that detected them; the state
     of the global contact-node set C (m, v*, v) is replicated on every rank;
@@ -539,16 +565,15 @@ def _allreduce_solve(ss: SlabState, grid, stencil, contacts, dt_s, block_shared)
     (solver.py:224-256) redundantly.  Each exact line-search evaluation
     (solver.py:266-325) all-reduces two scalars (the contact part of phi',
     phi''), so every rank takes the same branch and alpha.
-    Returns (v_next, gamma (local contacts, contact frame), report, owned)."""
+    Returns (v over C, P, gamma (local contacts, contact frame), report)."""
     from .contact_model import contact_grad_hess, contact_impulses
     from .collision import _contact_velocities_raw
     from .solver import line_search, solve_search_direction
     st, c = ss.state, ss.comm
     sp, cp = st.solver_params, st.contact_params
-    dev = grid.mass.device
-    lp = _local_contact_problem(ss, grid, stencil, contacts, dt_s, block_shared)
+    dev = lp["act"].device
     C = lp["C"]
-    nC, nc = int(C.shape[0]), contacts.n
+    nC, nc = int(C.shape[0]), cts.n
     g_nr = c.allgather(lp["nrec"])
     m, vs, v = _node_state(C, torch.cat([k.to(dev) for k in lp["all_cn"]]),
                            torch.cat([r.to(dev) for r in g_nr]))
@@ -556,8 +581,8 @@ def _allreduce_solve(ss: SlabState, grid, stencil, contacts, dt_s, block_shared)
     nodes = match_keys(C, lp["skeys"].reshape(-1)).reshape(-1, 27).clamp(min=0)
     w = lp["w"]
     if nc:
-        frames, bias = contacts.frames, contacts.bias
-        phi, gl, mu = contacts.phi, contacts.gamma_lag, contacts.mu
+        frames, bias = cts.frames, cts.bias
+        phi, gl, mu = cts.phi, cts.gamma_lag, cts.mu
     S0, Q0, Q1 = (float(x) for x in lp["ext"].tolist())
 
     def contact_terms(v):
@@ -572,7 +597,7 @@ def _allreduce_solve(ss: SlabState, grid, stencil, contacts, dt_s, block_shared)
                           (w * w)[:, :, None] * rgr.reshape(-1, 1, 9)], dim=2)
         return vc, _ordered_scatter(nodes, vals, nC)
 
-    P, it, evals, reg, converged = 1.0, 0, 0, 0, False
+    P, it, evals, converged = 1.0, 0, 0, False
     while True:
         vc, loc = contact_terms(v)
         tot = c.sum(loc)                                 # the per-iteration vector all-reduce
@@ -617,8 +642,11 @@ def _allreduce_solve(ss: SlabState, grid, stencil, contacts, dt_s, block_shared)
         raise FloatingPointError("contact solve produced non-finite velocities")
     gamma = contact_impulses(vc, phi, gl, mu, cp, dt_s) if nc else _lib.zeros((0, 3))
     report = SolveReport(converged=converged, iterations=it, n_contacts=n_glob, n_dofs=3 * nC,
-                         ls_evals=evals, regularized=reg)
-    return _local_v_next(grid, lp, v, P), gamma, report, lp["owned"]
+                         ls_evals=evals)
+    return v, P, gamma, report
+
+
+_SOLVES = {"gather0": _solve_gather0, "allreduce": _solve_allreduce}
 
 
 def slab_substep(ss: SlabState, dt_s: float, plan, epoch: int) -> dict:
@@ -641,8 +669,9 @@ def slab_substep(ss: SlabState, dt_s: float, plan, epoch: int) -> dict:
                            st.h)
         report = SolveReport(converged=True, n_contacts=0)
     else:
-        solve = _allreduce_solve if ss.solve == "allreduce" else _distributed_solve
-        grid.v_next, gamma, report, owned = solve(ss, grid, stencil, contacts, dt_s, shared)
+        lp = _local_contact_problem(ss, grid, stencil, contacts, dt_s, shared)
+        v_C, P, gamma, report = _SOLVES[ss.solve](ss, lp, contacts, dt_s)
+        grid.v_next, owned = _local_v_next(grid, lp, v_C, P), lp["owned"]
         if contacts.n:
             gamma_world = torch.einsum("ci,cij->cj", gamma, contacts.frames)
             bpos = torch.as_tensor(np.stack([np.asarray(b.position) for b in st.bodies]),
@@ -700,6 +729,150 @@ def slab_advance_step(ss: SlabState) -> StepSummary:
                           all_converged=conv,
                           staleness=float(stale[0].item()) / max(n_tot, 1),
                           clamped_gradients=clamped, wrench=wrench[:nb])
+    st.time = new_time
+    st.step_index += 1
+    return summary
+
+
+# ------------------------------------------------------------------ fused mode
+
+_TYPESTR = {torch.float64: "<f8", torch.int64: "<i8", torch.int32: "<i4"}
+
+
+class _DevArray:
+    """A device pointer of the simulator as a zero-copy torch view."""
+
+    def __init__(self, ptr, shape, dtype):
+        self.__cuda_array_interface__ = dict(shape=tuple(shape), typestr=_TYPESTR[dtype],
+                                             data=(int(ptr or 0), False), version=2,
+                                             strides=None)
+
+
+def _dev(ptr, shape, dtype=torch.float64) -> torch.Tensor:
+    if int(np.prod(shape)) == 0:
+        return torch.empty(shape, dtype=dtype, device=_lib.device())
+    return torch.as_tensor(_DevArray(ptr, shape, dtype), device=_lib.device())
+
+
+def _views(sim) -> _lib.SimViews:
+    v = _lib.SimViews()
+    _lib.check(_lib.lib().mpmrb_sim_get_views(sim, C.byref(v)))
+    return v
+
+
+def _block_coords(keys: torch.Tensor) -> torch.Tensor:
+    msk = (1 << 21) - 1
+    return torch.stack([(keys >> 42) - COORD_BIAS, ((keys >> 21) & msk) - COORD_BIAS,
+                        (keys & msk) - COORD_BIAS], dim=1)
+
+
+def _fused_substep(ss: SlabState, sim, dt_s: float) -> dict:
+    """One substep of the fused simulator on this rank's slab (coupling.py:
+    115-150): part 0 (grid + P2G kernels), the P2G halo reduce on the
+    simulator's own node channels, part 1 (grid update, active compaction,
+    contacts), the distributed contact solve writing v_next and the impulses
+    into the simulator's arrays, part 3 (reactions, G2P kernels)."""
+    st, c = ss.state, ss.comm
+    L = _lib.lib()
+    _lib.check(L.mpmrb_sim_substep_part(sim, 0))
+    V = _views(sim)
+    nb = int(V.n_blocks)
+    N = nb * BLOCK_NODES
+    keys = _dev(V.block_keys, (nb,), torch.int64)
+    shared = _halo_sum(ss, keys, _dev(V.mass, (N,)), _dev(V.mom_apic, (N, 3)),
+                       _dev(V.mom_force, (N, 3)))
+    _lib.check(L.mpmrb_sim_substep_part(sim, 1))
+    V = _views(sim)
+    na, nc = int(V.n_active), int(V.n_contacts)
+    act = _dev(V.act, (na,), torch.int32).to(torch.int64)
+    coords = node_coords(_block_coords(keys), act)
+    owned = node_owned(coords[:, ss.axis], shared[act // BLOCK_NODES], ss.bounds, c.rank, st.h)
+    n_glob = int(c.sum(torch.tensor([nc], dtype=torch.int64)).item())
+    if n_glob == 0:
+        _lib.check(L.mpmrb_sim_substep_part(sim, 2))   # no contacts anywhere: v_next = v*
+        report = SolveReport(converged=True, n_contacts=0)
+    else:
+        m_a, vs_a, vk_a = _dev(V.m_act, (na,)), _dev(V.v_star_act, (na, 3)), _dev(V.v_k_act,
+                                                                                    (na, 3))
+        cap = int(V.nc_cap)
+        loc = _dev(V.cnodes, (27, cap), torch.int32)[:, :nc].t().to(torch.int64)
+        w = _dev(V.cw, (27, cap))[:, :nc].t().contiguous()
+        cts = SimpleNamespace(n=nc, frames=_dev(V.frames, (nc, 3, 3)), bias=_dev(V.bias, (nc, 3)),
+                              phi=_dev(V.phi, (nc,)), mu=_dev(V.mu, (nc,)),
+                              gamma_lag=_dev(V.gamma_lag, (nc,)))
+        lp = _contact_problem(ss, act, coords, owned, loc, w, m_a, vs_a, vk_a)
+        v_C, P, gamma, report = _SOLVES[ss.solve](ss, lp, cts, dt_s)
+        _dev(V.v_next, (N, 3))[act] = _active_v_next(vs_a, vk_a, lp, v_C, P)
+        if nc:
+            _dev(V.gamma, (nc, 3)).copy_(gamma)
+        rep = _lib.SolveReportC()
+        rep.converged, rep.iterations = int(report.converged), int(report.iterations)
+        rep.ls_evals, rep.regularized = int(report.ls_evals), int(report.regularized)
+        _lib.check(L.mpmrb_sim_set_solve_result(sim, C.byref(rep)))
+    _lib.check(L.mpmrb_sim_substep_part(sim, 3))
+    return dict(n_contacts=n_glob, report=report, n_active=owned.sum())
+
+
+def slab_advance_step_fused(ss: SlabState) -> StepSummary:
+    """slab_advance_step on the fused simulator's kernels (the substep's
+    device pipeline of coupling.advance_step: stress-fused tiled P2G, hash
+    grid, contact detection and preparation, G2P with the return map), with
+    the slab exchanges between its parts (``_fused_substep``).  Particles
+    migrate at the step start; the drift guard runs on the step's final
+    positions.  Every rank returns the same summary."""
+    st, c = ss.state, ss.comm
+    L = _lib.lib()
+    ss.migrate()
+    p = st.particles
+    sim = _coupling._ensure_sim(st)
+    stream = _coupling._stream_of(st)
+    stream.wait_stream(torch.cuda.current_stream())
+    n = st.step.substeps
+    dt = st.step.dt
+    dt_s = dt / n
+    nb = len(st.bodies)
+    stats = _lib.StepStats()
+    imp = (C.c_double * (6 * max(nb, 1)))()
+    ncs, its, acts, conv = [], [], [], True
+    with torch.cuda.stream(stream):
+        _lib.bind_stream(st._ctx, stream)
+        _coupling._configure_sim(st, sim, dt_s)
+        rc = L.mpmrb_sim_begin_step(sim, st.step_index, n)
+        if rc == _lib.E_DIVERGED:
+            raise _coupling.SimulationDiverged(
+                f"non-finite or out-of-range particle state after step {st.step_index}")
+        _lib.check(rc)
+        for _ in range(n):
+            info = _fused_substep(ss, sim, dt_s)
+            ncs.append(info["n_contacts"])
+            its.append(info["report"].iterations)
+            acts.append(info["n_active"])
+            conv &= info["report"].converged
+        rc = L.mpmrb_sim_end_step(sim, C.byref(stats), imp)
+    if rc == _lib.E_DIVERGED:
+        raise _coupling.SimulationDiverged(f"non-finite particle state after step {st.step_index}")
+    _lib.check(rc)
+    torch.cuda.current_stream().wait_stream(stream)
+    ss.drift_check()
+    acc = np.frombuffer(imp, dtype=np.float64)[: 6 * nb].reshape(nb, 6).copy()
+    acc = c.sum(torch.as_tensor(acc)).numpy()
+    st._accum.linear[:] = acc[:, 0:3]
+    st._accum.angular[:] = acc[:, 3:6]
+    loc = torch.cat([torch.stack(acts).to(torch.float64).cpu(),
+                     torch.tensor([float(stats.clamped), _coupling._last_staleness(st) * p.n,
+                                   float(p.n)], dtype=torch.float64)])
+    tot = c.sum(loc)
+    acts = [int(a) for a in tot[:n].tolist()]
+    clamped, stale, n_tot = int(tot[n]), float(tot[n + 1]), int(tot[n + 2])
+    new_time = st.time + dt
+    wrench = np.concatenate([st._accum.linear / dt, st._accum.angular / dt], axis=1)
+    _rigid_update(st, new_time)
+    summary = StepSummary(step_index=st.step_index, time=new_time, n_particles=n_tot,
+                          n_active_nodes=float(np.mean(acts)),
+                          n_contacts_mean=float(np.mean(ncs)), n_contacts_max=int(np.max(ncs)),
+                          iterations_mean=float(np.mean(its)), iterations_max=int(np.max(its)),
+                          all_converged=conv, staleness=stale / max(n_tot, 1),
+                          clamped_gradients=clamped, wrench=wrench)
     st.time = new_time
     st.step_index += 1
     return summary

@@ -613,6 +613,19 @@ def test_bench_transfer_harness(mp, capsys):
     assert all(float(r[4]) <= 1e-12 for r in rows)
 
 
+def test_bench_transfer_payload_deterministic_matches_oracle(mp):
+    """The harness's deterministic scatter on its own payload (cli.py:48-59)
+    is bitwise the oracle's particle-order fold (reference transfer.py:135-145)."""
+    from oracle.grid import scatter_in_order
+    from paper_2503_05046_b200 import bench_transfer
+    from paper_2503_05046_b200.transfer import build_sort_plan, scatter_reduce
+    grid, stencil, values, pos, h = bench_transfer.payload(3000)
+    plan = build_sort_plan(pos, h, epoch=0)
+    out = scatter_reduce(stencil.nodes, values, grid.n_nodes, plan, 0, mode="deterministic")
+    ref = scatter_in_order(np_(stencil.nodes), np_(values), grid.n_nodes)
+    assert np.array_equal(np_(out), ref)
+
+
 # ------------------------------------------------------------------ slab decomposition
 
 def _slab_scene(world=2):
@@ -629,16 +642,17 @@ def _slab_scene(world=2):
     return sc
 
 
-def _slab_worker(rank, world, port, out, steps, solve="gather0"):
+def _slab_worker(rank, world, port, out, steps, solve="gather0", fused=False):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2503_05046_b200 import scenes, slab
-    st = scenes.build_state(_slab_scene(world))
+    st = scenes.build_state(_slab_scene(max(world, 2)))
     ss = slab.SlabState.from_state(st, solve=solve)
     n_local0 = ss.state.particles.n
-    sums = [slab.slab_advance_step(ss) for _ in range(steps)]
+    step = slab.slab_advance_step_fused if fused else slab.slab_advance_step
+    sums = [step(ss) for _ in range(steps)]
     allp = slab.gather_particles(ss)
     if rank == 0:
         np.savez(out, **{k: v.cpu().numpy() for k, v in allp.items()},
@@ -684,6 +698,46 @@ def test_slab_decomposition_matches_single_scene(mp, tmp_path, world, solve):
         ws = np.abs(sref.wrench).max()
         assert np.abs(r["wrench"][i] - sref.wrench).max() <= 1e-6 * ws + 1e-9, i
     assert np.abs(ref[-1].wrench[1]).max() > 0  # the ball is in contact across the bound
+    p = st.particles
+    np.testing.assert_allclose(r["x"], np_(p.x), rtol=0, atol=1e-10)
+    np.testing.assert_allclose(r["v"], np_(p.v), rtol=0, atol=1e-7)
+    np.testing.assert_allclose(r["f"], np_(p.f), rtol=0, atol=1e-8)
+    np.testing.assert_allclose(r["plastic"], np_(p.plastic), rtol=0, atol=1e-8)
+    np.testing.assert_allclose(r["bodies"], np.array([b.position for b in st.bodies]), rtol=0,
+                               atol=1e-10)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,solve", [(1, "gather0"), (2, "gather0"), (3, "gather0"),
+                                         (2, "allreduce")])
+def test_slab_fused_matches_single_scene(mp, tmp_path, world, solve):
+    """slab_advance_step_fused: each rank runs the fused simulator's kernels
+    (mpmrb_sim_substep_part 0..3) with the P2G halo reduce on the simulator's
+    node channels and the distributed contact solve written into its v_next
+    and impulse arrays.  It must match the single-scene fused advance_step up
+    to reduction-order roundoff."""
+    import socket
+
+    import torch.multiprocessing as tmp
+    from paper_2503_05046_b200 import coupling, scenes
+    steps = 5
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    out = str(tmp_path / "slabf.npz")
+    tmp.spawn(_slab_worker, args=(world, port, out, steps, solve, True), nprocs=world, join=True)
+    r = np.load(out)
+    st = scenes.build_state(_slab_scene(max(world, 2)))
+    n = st.particles.n
+    assert int(r["n_part"]) == n
+    ref = [coupling.advance_step(st) for _ in range(steps)]
+    for i, sref in enumerate(ref):
+        assert r["ncont"][i] == sref.n_contacts_mean, i
+        assert abs(r["nact"][i] - sref.n_active_nodes) <= 1e-9 * sref.n_active_nodes, i
+        ws = np.abs(sref.wrench).max()
+        assert np.abs(r["wrench"][i] - sref.wrench).max() <= 1e-6 * ws + 1e-9, i
+    assert np.abs(ref[-1].wrench[1]).max() > 0
     p = st.particles
     np.testing.assert_allclose(r["x"], np_(p.x), rtol=0, atol=1e-10)
     np.testing.assert_allclose(r["v"], np_(p.v), rtol=0, atol=1e-7)

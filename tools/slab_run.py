@@ -5,8 +5,10 @@ JSON line (rank 0) with the device time per rigid step (max over ranks):
         tools/slab_run.py [--workload multi4m|sand|sand1m] [--steps K] [--warmup W]
 
 NCCL when every rank has its own GPU; --backend gloo lets several ranks share
-one GPU (functional runs only).  The slab path composes the fine-grained device
-operators (paper_2503_05046_b200/slab.py), not the fused substep graph."""
+one GPU (functional runs only).  By default each rank runs the fused
+simulator's kernels with the slab exchanges between the substep's parts
+(slab_advance_step_fused); --ops composes the fine-grained device operators
+instead (slab_advance_step); --solve picks the distributed contact solve."""
 
 import argparse
 import json
@@ -29,6 +31,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=1)
     ap.add_argument("--backend", default=None)
     ap.add_argument("--solve", default="gather0", choices=("gather0", "allreduce"))
+    ap.add_argument("--ops", action="store_true",
+                    help="operator-by-operator substep (slab_advance_step) instead of the fused "
+                         "simulator's kernels (slab_advance_step_fused)")
     a = ap.parse_args()
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
@@ -41,15 +46,16 @@ def main():
     sc = bench.workload_scene(a.workload, 0)
     st = scenes.build_state(sc)
     ss = slab.SlabState.from_state(st, solve=a.solve)
+    step = slab.slab_advance_step if a.ops else slab.slab_advance_step_fused
     for _ in range(a.warmup):
-        slab.slab_advance_step(ss)
+        step(ss)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    sums = [slab.slab_advance_step(ss) for _ in range(a.steps)]
+    sums = [step(ss) for _ in range(a.steps)]
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / a.steps
@@ -61,6 +67,7 @@ def main():
         print(json.dumps(dict(metric="MPM particle-substeps/sec incl. convex contact solve",
                               value=n * sc["substeps"] / (ms * 1e-3), unit="particle-substeps/s",
                               n_gpus=world, decomposition="slab", backend=backend, solve=a.solve,
+                              substep="ops" if a.ops else "fused",
                               steps=a.steps, warmup=a.warmup, ms_per_step=ms,
                               wall_s=time.perf_counter() - t0,
                               config=dict(workload=a.workload, particles=n,
