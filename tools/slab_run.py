@@ -31,6 +31,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=1)
     ap.add_argument("--backend", default=None)
     ap.add_argument("--solve", default="gather0", choices=("gather0", "allreduce"))
+    ap.add_argument("--single", action="store_true",
+                    help="world 1 only: the undecomposed fused coupling.advance_step on the "
+                         "same window, for comparison")
     ap.add_argument("--ops", action="store_true",
                     help="operator-by-operator substep (slab_advance_step) instead of the fused "
                          "simulator's kernels (slab_advance_step_fused)")
@@ -47,6 +50,10 @@ def main():
     st = scenes.build_state(sc)
     ss = slab.SlabState.from_state(st, solve=a.solve)
     step = slab.slab_advance_step if a.ops else slab.slab_advance_step_fused
+    if a.single:
+        from paper_2503_05046_b200 import coupling
+        assert world == 1, "--single is the one-process reference run"
+        step = lambda _ss: coupling.advance_step(st)  # noqa: E731
     for _ in range(a.warmup):
         step(ss)
     torch.cuda.synchronize()
@@ -67,7 +74,7 @@ def main():
         print(json.dumps(dict(metric="MPM particle-substeps/sec incl. convex contact solve",
                               value=n * sc["substeps"] / (ms * 1e-3), unit="particle-substeps/s",
                               n_gpus=world, decomposition="slab", backend=backend, solve=a.solve,
-                              substep="ops" if a.ops else "fused",
+                              substep="single" if a.single else ("ops" if a.ops else "fused"),
                               steps=a.steps, warmup=a.warmup, ms_per_step=ms,
                               wall_s=time.perf_counter() - t0,
                               config=dict(workload=a.workload, particles=n,
