@@ -192,12 +192,27 @@ def _facade(name: str, mod) -> types.ModuleType:
     return fm
 
 
+def _advance_step_by_mode(state, *args, **kwargs):
+    """The reference's advance_step honours ``state.mode`` (coupling.py:168-
+    219 with transfer.py:9-14): "deterministic", its default, sums every
+    scatter in particle-id order, so results are bitwise reproducible and
+    independent of the sort plan (test_coupling.py::
+    test_substep_equivalence_bitwise).  That is the operator pipeline with the
+    ordered P2G fold (coupling.advance_step_ops); "fast" is the fused substep
+    graph (coupling.advance_step), whose P2G tiles flush with float64 atomics."""
+    if getattr(state, "mode", "deterministic") == "deterministic" and not args and not kwargs:
+        return coupling.advance_step_ops(state)
+    return coupling.advance_step(state, *args, **kwargs)
+
+
 def install(alias: str = "mpmrb") -> types.ModuleType:
     """Register the façade as ``alias`` (and ``alias.<module>``) in sys.modules."""
     root = types.ModuleType(alias, __doc__)
     root.__path__ = []  # a package, so "from mpmrb.x import y" resolves
     for name, mod in MODULES.items():
         fm = _facade(name, mod)
+        if name == "coupling":
+            fm.advance_step = _wrap_fn(_advance_step_by_mode)
         fm.__name__ = f"{alias}.{name}"
         sys.modules[f"{alias}.{name}"] = fm
         setattr(root, name, fm)

@@ -11,9 +11,9 @@ tests/refsuite/_staged/ (git-ignored) for one GPU run and removes them
 afterwards; the run's per-test outcome is committed under profiles/.  Without
 the staged files this test skips.
 
-Expected differences (asserted below, with the reason) are the reference's
-bitwise-equality tests whose summation order the GPU does not reproduce
-(SURVEY.md §4 lists eight such tests; all but one pass bitwise here).
+Expected differences would be the reference's bitwise-equality tests whose
+summation order the GPU does not reproduce (SURVEY.md §4 lists eight); all
+eight pass bitwise here.
 """
 
 import json
@@ -30,16 +30,13 @@ ROOT = Path(__file__).resolve().parents[1]
 STAGED = ROOT / "tests" / "refsuite" / "_staged"
 
 # reference tests that assert bitwise equality of float sums in an order the
-# GPU path does not follow, with the reason
-EXPECTED_DIFF = {
-    # the fused substep re-sorts particles by (block, cell) once per step and
-    # its P2G flushes warp tiles with float64 atomics: one step of N substeps
-    # and N steps of one substep agree to roundoff, not bitwise
-    # (tests/test_gpu_parity.py::test_fused_substep_equivalence is the
-    # tolerance variant)
-    "test_coupling.py::test_substep_equivalence_bitwise":
-        "per-step particle re-sort + atomic P2G flush: equal to roundoff, not bitwise",
-}
+# GPU path does not follow, with the reason.  None remain: the
+# façade's advance_step in the reference's default mode="deterministic" runs
+# the operator pipeline with the particle-id-order P2G fold
+# (compat._advance_step_by_mode), so test_substep_equivalence_bitwise holds
+# bitwise; the fused substep (mode="fast") agrees with it to roundoff
+# (tests/test_gpu_parity.py::test_fused_substep_equivalence).
+EXPECTED_DIFF: dict = {}
 
 
 def test_reference_suite_against_gpu_package(tmp_path):
