@@ -420,17 +420,24 @@ def _contact_problem(ss: SlabState, act, coords, owned, loc, w, m_a, vs_a, vk_a)
     ``vs_a``, ``vk_a``: m, v*, v_k of the active nodes."""
     c = ss.comm
     keys_act = pack_coords(coords)
+    n_act = int(act.shape[0])
     dead = loc < 0
     skeys = torch.where(dead, torch.full_like(loc, -1), keys_act[loc.clamp(min=0)])
-    cn = torch.unique(loc[~dead])
+    # the contact nodes: flags with a trash slot for dead slots (one nonzero
+    # instead of a sort-based unique)
+    flag = torch.zeros(n_act + 1, dtype=torch.bool, device=act.device)
+    flag[torch.where(dead, torch.full_like(loc, n_act), loc).reshape(-1)] = True
+    cn = torch.nonzero(flag[:n_act], as_tuple=False).reshape(-1)
     all_cn = c.allgather(keys_act[cn])
-    C = torch.unique(torch.cat([k.to(act.device) for k in all_cn]))     # sorted
-    in_C = match_keys(C, keys_act) >= 0
-    fm = owned & ~in_C
-    ext = c.sum(free_sums(m_a[fm], vs_a[fm], vk_a[fm]))
+    C = torch.cat([k.to(act.device) for k in all_cn])
+    # sorted; shared nodes appear once per rank that has contacts on them
+    C = torch.unique(C) if c.world > 1 else torch.sort(C).values
+    posC = match_keys(C, keys_act)                     # active node -> C, or -1
+    fm = (owned & (posC < 0)).to(m_a.dtype)            # contact-free owned nodes
+    ext = c.sum(free_sums(m_a * fm, vs_a, vk_a))
     nrec = torch.cat([m_a[cn][:, None], vs_a[cn], vk_a[cn]], dim=1)
     return dict(act=act, keys_act=keys_act, owned=owned, skeys=skeys, w=w, cn=cn,
-                all_cn=all_cn, C=C, ext=ext, nrec=nrec)
+                all_cn=all_cn, C=C, posC=posC, ext=ext, nrec=nrec)
 
 
 def _local_contact_problem(ss: SlabState, grid, stencil, contacts, dt_s, block_shared):
@@ -461,10 +468,10 @@ def _active_v_next(vs_a, vk_a, lp, v_C, P):
     """v_next of the active nodes: contact nodes from the solution over C,
     every other one at v* + P (v_k - v*)."""
     va = vs_a + P * (vk_a - vs_a)
-    pos = match_keys(lp["C"], lp["keys_act"])
-    hit = pos >= 0
-    va[hit] = v_C[pos[hit]]
-    return va
+    pos = lp["posC"]
+    if v_C.shape[0] == 0:
+        return va
+    return torch.where((pos >= 0)[:, None], v_C[pos.clamp(min=0)], va)
 
 
 def _local_v_next(grid, lp, v_C, P):
