@@ -525,12 +525,13 @@ def _solve_gather0(ss: SlabState, lp: dict, cts, dt_s):
     meta = c.bcast(meta)
     v_sol = c.bcast(v_sol).to(dev)
     gamma_all = c.bcast(gamma_all).to(dev)
-    P = float(meta[0])
+    mt = meta.tolist()                                   # one read-back
+    P = float(mt[0])
     start = sum(counts[: c.rank])
     gamma = gamma_all[start: start + cts.n]
-    report = SolveReport(converged=bool(meta[1] > 0.5), iterations=int(meta[2]),
+    report = SolveReport(converged=mt[1] > 0.5, iterations=int(mt[2]),
                          n_contacts=int(sum(counts)), n_dofs=3 * int(C.shape[0]),
-                         ls_evals=int(meta[3]), regularized=int(meta[4]))
+                         ls_evals=int(mt[3]), regularized=int(mt[4]))
     return v_sol, P, gamma, report
 
 
@@ -782,14 +783,20 @@ def _fused_substep(ss: SlabState, sim, dt_s: float) -> dict:
     st, c = ss.state, ss.comm
     L = _lib.lib()
     _lib.check(L.mpmrb_sim_substep_part(sim, 0))
+    shared = None
+    if c.world > 1:   # the halo reduce needs the block count before part 1
+        V = _views(sim)
+        nb = int(V.n_blocks)
+        N = nb * BLOCK_NODES
+        shared = _halo_sum(ss, _dev(V.block_keys, (nb,), torch.int64), _dev(V.mass, (N,)),
+                           _dev(V.mom_apic, (N, 3)), _dev(V.mom_force, (N, 3)))
+    _lib.check(L.mpmrb_sim_substep_part(sim, 1))
     V = _views(sim)
     nb = int(V.n_blocks)
     N = nb * BLOCK_NODES
     keys = _dev(V.block_keys, (nb,), torch.int64)
-    shared = _halo_sum(ss, keys, _dev(V.mass, (N,)), _dev(V.mom_apic, (N, 3)),
-                       _dev(V.mom_force, (N, 3)))
-    _lib.check(L.mpmrb_sim_substep_part(sim, 1))
-    V = _views(sim)
+    if shared is None:
+        shared = torch.zeros(nb, dtype=torch.bool, device=keys.device)
     na, nc = int(V.n_active), int(V.n_contacts)
     act = _dev(V.act, (na,), torch.int32).to(torch.int64)
     coords = node_coords(_block_coords(keys), act)
