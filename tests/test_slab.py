@@ -1,6 +1,7 @@
 """Slab domain decomposition (paper_2503_05046_b200/slab.py), host logic on CPU:
 slab bounds, ownership, halo bands, key packing, the particle migration
-payload, and the gloo communication layer at world_size 2.  The device path
+payload, the distributed solve's problem assembly, and the gloo communication
+layer at world_size 2 and 3.  The device path
 (2 ranks sharing cuda:0 vs the single-scene run) is tests/test_gpu_parity.py::
 test_slab_decomposition_matches_single_scene."""
 
@@ -226,3 +227,46 @@ def test_neighbour_exchange_and_gather0_gloo(tmp_path, world):
             right = rank + 1  # its left payload (empty from rank 1)
             n = 0 if right == 1 else right + 1
             assert r["fr"].shape == (n, 2) and bool((r["fr"] == 100 * right + 1).all())
+
+
+def test_contact_problem_assembly_host_logic():
+    """_contact_problem (the distributed solve's shared prologue) at one rank
+    on CPU tensors: the contact-node set, the stencil keys, the free-node sums
+    over owned contact-free nodes and the node records agree with a direct
+    restatement; _active_v_next puts the solution on contact nodes and
+    v* + P (v_k - v*) everywhere else."""
+    from types import SimpleNamespace
+    rng = np.random.default_rng(3)
+    na, nc = 60, 7
+    coords = torch.as_tensor(rng.integers(-50, 50, size=(na, 3)))
+    act = torch.arange(na)
+    owned = torch.as_tensor(rng.random(na) < 0.8)
+    loc = torch.as_tensor(rng.integers(0, na, size=(nc, 27)))
+    loc[torch.as_tensor(rng.random((nc, 27)) < 0.2)] = -1
+    w = torch.as_tensor(rng.random((nc, 27)))
+    w[loc < 0] = 0.0
+    m = torch.as_tensor(rng.uniform(0.1, 1.0, na))
+    vs = torch.as_tensor(rng.normal(size=(na, 3)))
+    vk = torch.as_tensor(rng.normal(size=(na, 3)))
+    ss = SimpleNamespace(comm=S.Comm())
+    lp = S._contact_problem(ss, act, coords, owned, loc, w, m, vs, vk)
+    keys = S.pack_coords(coords)
+    cn_ref = np.unique(loc[loc >= 0].numpy())
+    assert lp["cn"].tolist() == cn_ref.tolist()
+    assert lp["C"].tolist() == sorted(keys[cn_ref].tolist())
+    sk = lp["skeys"].numpy()
+    assert (sk[loc.numpy() < 0] == -1).all()
+    assert (sk[loc.numpy() >= 0] == keys.numpy()[loc.numpy()[loc.numpy() >= 0]]).all()
+    free = owned.numpy() & ~np.isin(np.arange(na), cn_ref)
+    ref = S.free_sums(m[free], vs[free], vk[free])
+    assert torch.allclose(lp["ext"], ref, rtol=1e-13, atol=1e-13)
+    assert torch.equal(lp["nrec"][:, 0], m[cn_ref])
+    # v_next: solution on C, closed form elsewhere
+    v_C = torch.as_tensor(rng.normal(size=(lp["C"].shape[0], 3)))
+    P = 0.3
+    va = S._active_v_next(vs, vk, lp, v_C, P)
+    pos = {k: i for i, k in enumerate(lp["C"].tolist())}
+    for i in range(na):
+        k = int(keys[i])
+        exp = v_C[pos[k]] if k in pos else vs[i] + P * (vk[i] - vs[i])
+        assert torch.equal(va[i], exp)
