@@ -143,10 +143,13 @@ __global__ void k_cloth_forces(long long ne, const int* __restrict__ tri,
   }
 }
 
+// T: the element particles' APIC C (float64, or float32 in the fp32 mode);
+// d3, positions and the return map stay float64
+template <class T>
 __global__ void k_cloth_post(long long ne, const int* __restrict__ tri,
                              const int* __restrict__ epart, const double* __restrict__ dm_inv,
                              double* __restrict__ d3, const int* __restrict__ inv_perm,
-                             double* __restrict__ x, const double* __restrict__ c,
+                             double* __restrict__ x, const T* __restrict__ c,
                              const long long* __restrict__ mid,
                              const mpmrb_material* __restrict__ mats, int nmat, double dt) {
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < ne;
@@ -157,12 +160,13 @@ __global__ void k_cloth_post(long long ne, const int* __restrict__ tri,
     if (m_id < 0 || m_id >= nmat) continue;
     const mpmrb_material m = mats[m_id];
     // d3 <- (I + dt C_e) d3
-    const double* C = c + 9LL * pe;
+    const T* C = c + 9LL * pe;
     double dn[3];
 #pragma unroll
     for (int i = 0; i < 3; ++i)
-      dn[i] = d3[3 * e + i] + dt * (C[3 * i] * d3[3 * e] + C[3 * i + 1] * d3[3 * e + 1] +
-                                    C[3 * i + 2] * d3[3 * e + 2]);
+      dn[i] = d3[3 * e + i] + dt * ((double)C[3 * i] * d3[3 * e] +
+                                    (double)C[3 * i + 1] * d3[3 * e + 1] +
+                                    (double)C[3 * i + 2] * d3[3 * e + 2]);
     double f1[3], f2[3], f3[3];
     element_F(x + 3 * v0, x + 3 * v1, x + 3 * v2, dm_inv + 4 * e, dn, f1, f2, f3);
     const QR3 o = qr_gs(f1, f2, f3);
@@ -224,15 +228,26 @@ int launch_cloth_forces(Ctx& c, const ClothDev& cl, const ParticlesDev& p,
   return MPMRB_OK;
 }
 
-int launch_cloth_post(Ctx& c, const ClothDev& cl, const ParticlesDev& p,
+template <class T>
+static int cloth_post(Ctx& c, const ClothDev& cl, const ParticlesT<T>& p,
                       const mpmrb_material* mats_dev, int nmat, double dt) {
   if (cl.ne == 0) return MPMRB_OK;
-  k_cloth_post<<<cl_grid(cl.ne), 256, 0, c.stream>>>(cl.ne, cl.tri, cl.epart, cl.dm_inv, cl.d3,
-                                                     cl.inv_perm, p.x, p.c, p.mid, mats_dev,
-                                                     nmat, dt);
+  k_cloth_post<T><<<cl_grid(cl.ne), 256, 0, c.stream>>>(cl.ne, cl.tri, cl.epart, cl.dm_inv, cl.d3,
+                                                        cl.inv_perm, p.x, p.c, p.mid, mats_dev,
+                                                        nmat, dt);
   c.launches++;
   MPMRB_CUDA_OK(cudaGetLastError());
   return MPMRB_OK;
+}
+
+int launch_cloth_post(Ctx& c, const ClothDev& cl, const ParticlesDev& p,
+                      const mpmrb_material* mats_dev, int nmat, double dt) {
+  return cloth_post(c, cl, p, mats_dev, nmat, dt);
+}
+
+int launch_cloth_post(Ctx& c, const ClothDev& cl, const ParticlesF32& p,
+                      const mpmrb_material* mats_dev, int nmat, double dt) {
+  return cloth_post(c, cl, p, mats_dev, nmat, dt);
 }
 
 int launch_inverse_perm(Ctx& c, const int* perm, long long n, int* inv) {

@@ -111,7 +111,7 @@ struct ParticlesT {
   const long long* mid;
   T* plastic;
   long long n;
-  // codimensional cloth (NULL when absent; float64 mode only): role per
+  // codimensional cloth (NULL when absent; both precisions): role per
   // particle (MPMRB_CLOTH_*), element stresses written by the cloth kernel,
   // vertex forces
   const signed char* role = nullptr;
@@ -165,6 +165,8 @@ int launch_seed_box(Ctx& c, const long long* lo, const long long* hi, int per_ax
 int launch_cloth_forces(Ctx& c, const ClothDev& cl, const ParticlesDev& p,
                         const mpmrb_material* mats_dev, int nmat);
 int launch_cloth_post(Ctx& c, const ClothDev& cl, const ParticlesDev& p,
+                      const mpmrb_material* mats_dev, int nmat, double dt);
+int launch_cloth_post(Ctx& c, const ClothDev& cl, const ParticlesF32& p,
                       const mpmrb_material* mats_dev, int nmat, double dt);
 int launch_inverse_perm(Ctx& c, const int* perm, long long n, int* inv);
 int launch_gather_i8(Ctx& c, const signed char* src, const int* perm, long long n,

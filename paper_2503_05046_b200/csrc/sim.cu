@@ -529,7 +529,9 @@ int Sim::capture_or_launch(int part_lo, int part_hi) {
                         b_misc.as<unsigned long long>(), b_misc.as<int>() + 2);
   if (rc) return rc;
   if (cloth.ne > 0) {  // d3 advection, return map, element particles to centroids
-    rc = launch_cloth_post(c, cloth, q, b_mats.as<mpmrb_material>(), nmat, dt_s);
+    rc = (prec == MPMRB_PREC_F32)
+             ? launch_cloth_post(c, cloth, q32, b_mats.as<mpmrb_material>(), nmat, dt_s)
+             : launch_cloth_post(c, cloth, q, b_mats.as<mpmrb_material>(), nmat, dt_s);
     if (rc) return rc;
   }
   mark(7);
@@ -581,8 +583,6 @@ int Sim::begin_step(long long epoch, int n_substeps) {
   Ctx& c = *ctx;
   if (!have_particles) return set_error(MPMRB_E_INVALID, "sim: particles not set");
   if (!have_params) return set_error(MPMRB_E_INVALID, "sim: params not set");
-  if (prec == MPMRB_PREC_F32 && cloth.ne > 0)
-    return set_error(MPMRB_E_INVALID, "sim: the fp32 performance mode does not support cloth");
   // size the grid for the current positions (one host sync per step)
   if (b_counters.grow(64) || b_misc.grow(64) || b_solveout.grow(sizeof(SolveOut)) ||
       b_bar.grow(4096) || b_partials.grow(sizeof(double) * (2 * 8 * kMaxSolverCtas + 8)) ||
@@ -698,6 +698,14 @@ int Sim::begin_step(long long epoch, int n_substeps) {
       q.role = nullptr;
       q.tau = nullptr;
       q.fext = nullptr;
+      invalidate();
+    }
+    // the fp32 layout shares the cloth roles, element stresses and vertex
+    // forces (float64) with the float64 one
+    if (q32.role != q.role || q32.tau != q.tau || q32.fext != q.fext) {
+      q32.role = q.role;
+      q32.tau = q.tau;
+      q32.fext = q.fext;
       invalidate();
     }
   }
