@@ -132,32 +132,46 @@ def test_fp32_p2g_conserves_mass_and_momentum(mp):
 
 def test_fp32_cloth_drift_bound(mp):
     """Codimensional cloth in the fp32 mode: a 33 x 33 sheet (3,137 particles)
-    dropped 1 cm onto the rigid sphere of configs[2], 40 coupling steps (640
-    substeps) in both precisions from the same state.  The cloth forces,
+    dropped 1 cm onto the rigid sphere of configs[2], 200 coupling steps
+    (3,200 substeps: the landing and the settling).  The cloth forces,
     element stresses, vertex forces, d3 and positions stay float64; P2G / G2P
-    and the element particles' C run in float32.  Bounds: positions within
-    0.05 h, sphere impulse integrated over the window within 5%."""
+    and the element particles' C run in float32.  The solves run to
+    eps_r = 1e-4, so the solver's stopping point does not hide the drift.
+
+    The sheet's motion on the sphere amplifies roundoff: two float64 runs from
+    the same state (the P2G flush is float64 atomics) end 0.17-0.19 h apart,
+    the float32 run 0.10-0.16 h from a float64 one
+    (profiles/r02_fp32_cloth_probe.jsonl, tools/fp32_cloth_probe.py).  So the
+    drift is measured against that spread.  Bounds: positions within 0.5 h
+    and within 2x the float64 run-to-run spread + 0.1 h; sphere impulse
+    integrated over the window within 5%, as for the sand (measured
+    0.2-1.0%; float64 repeat 0-1.7%)."""
     from paper_2503_05046_b200 import scenes
     sc = scenes.cloth_sheet_scene(n_side=33)
     sc["cloth"][0]["center"][2] = 0.26
+    sc["solver"]["eps_r"] = 1e-4
     a = scenes.build_state(sc)
+    a2 = scenes.build_state(sc)
     b = scenes.build_state(sc, precision="f32")
     assert torch.equal(a.particles.x, b.particles.x)
-    wa = np.zeros(6)
-    wb = np.zeros(6)
-    for _ in range(40):
-        sa = mp.advance_step(a)
-        sb = mp.advance_step(b)
-        wa += sa.wrench[0]
-        wb += sb.wrench[0]
+    w = {k: np.zeros(3) for k in "abr"}
+    for _ in range(200):
+        for k, st in (("a", a), ("r", a2), ("b", b)):
+            s = mp.advance_step(st)
+            w[k] += s.wrench[0][:3]
     h = sc["h"]
-    dx = float(np.abs(np_(a.particles.x) - np_(b.particles.x)).max()) / h
-    dw = float(np.abs(wa[:3] - wb[:3]).max() / np.abs(wa[:3]).max())
-    d3 = float(np.abs(np_(a.cloth.d3) - np_(b.cloth.d3)).max())
-    _record("cloth_sheet_33", steps=40, max_dx_over_h=dx, impulse_relerr=dw, max_d3_diff=d3,
-            contacts_last=[sa.n_contacts_mean, sb.n_contacts_mean])
-    assert sa.n_contacts_mean > 0          # the sheet is on the sphere
-    assert dx <= 0.05, dx
+    xa = np_(a.particles.x)
+    dx = float(np.abs(xa - np_(b.particles.x)).max()) / h
+    dx_rep = float(np.abs(xa - np_(a2.particles.x)).max()) / h
+    dw = float(np.abs(w["a"] - w["b"]).max() / np.abs(w["a"]).max())
+    dw_rep = float(np.abs(w["a"] - w["r"]).max() / np.abs(w["a"]).max())
+    _record("cloth_sheet_33", steps=200, max_dx_over_h=dx, f64_repeat_dx_over_h=dx_rep,
+            impulse_relerr=dw, f64_repeat_impulse_relerr=dw_rep,
+            max_d3_diff=float(np.abs(np_(a.cloth.d3) - np_(b.cloth.d3)).max()),
+            contacts_last=s.n_contacts_mean)
+    assert s.n_contacts_mean > 0          # the sheet is on the sphere
+    assert dx <= 0.5, dx
+    assert dx <= 2.0 * dx_rep + 0.1, (dx, dx_rep)
     assert dw <= 0.05, dw
 
 
