@@ -503,6 +503,8 @@ def run_ours(args):
         abytes = algorithmic_bytes(stage, n, prof["n_active"], sand, prof, args.precision)
         achieved = abytes / (st[stage] * 1e-3) / 1e9
         kname = {"solve": "k_qn_solve", "p2g": "k_p2g", "g2p": "k_g2p"}[stage]
+        if stage != "solve":  # the transfer kernels are instantiated per precision
+            kname += "<float>" if args.precision == "f32" else "<double>"
         tr = traffic_all.get(kname) or {}
         out = dict(bound="hbm", kernel=kname, achieved=achieved, peak=hbm, unit="GB/s",
                    frac=achieved / hbm, traffic=tr.get("dram_bytes"),
