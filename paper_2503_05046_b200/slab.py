@@ -632,13 +632,22 @@ def _solve_allreduce(ss: SlabState, lp: dict, cts, dt_s):
         dvc = (torch.einsum("cij,cj->ci", frames, torch.einsum("ck,ckd->cd", w, d[nodes]))
                if nc else None)
 
+        def local_part(alpha: float) -> torch.Tensor:
+            if not nc:
+                return torch.zeros(2, dtype=torch.float64, device=dev)
+            g_a, big_a = contact_grad_hess(vc + alpha * dvc, phi, gl, mu, cp, dt_s)
+            return torch.stack([(g_a * dvc).sum(),
+                                (dvc * torch.einsum("cij,cj->ci", big_a, dvc)).sum()])
+
+        # the search always evaluates alpha = 0 and then alpha = 1
+        # (solver.py:269-276): both travel in one all-reduce
+        first = c.sum(torch.cat([local_part(0.0), local_part(1.0)])).tolist()
+        known = {0.0: first[0:2], 1.0: first[2:4]}
+
         def deriv(alpha: float):
-            part = torch.zeros(2, dtype=torch.float64, device=dev)
-            if nc:
-                g_a, big_a = contact_grad_hess(vc + alpha * dvc, phi, gl, mu, cp, dt_s)
-                part = torch.stack([(g_a * dvc).sum(),
-                                    (dvc * torch.einsum("cij,cj->ci", big_a, dvc)).sum()])
-            tot2 = c.sum(part).tolist()                  # the line search's scalar all-reduce
+            tot2 = known.pop(alpha, None)
+            if tot2 is None:
+                tot2 = c.sum(local_part(alpha)).tolist()  # the line search's scalar all-reduce
             return a1 + a2 * alpha + tot2[0], a2 + tot2[1]
 
         ls = line_search(deriv, max_iters=sp.ls_max_iters, tol=sp.ls_tol)
