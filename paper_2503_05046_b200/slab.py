@@ -282,6 +282,9 @@ class SlabState:
         distributed contact solve (module docstring, item 2)."""
         if solve not in ("gather0", "allreduce"):
             raise ValueError(f"unknown slab solve mode {solve!r}")
+        if state.cloth is not None and state.cloth.n_elements > 0:
+            # mesh elements index particles that migration renumbers per rank
+            raise ValueError("cloth is not supported under slab decomposition")
         comm = comm or Comm()
         p = state.particles
         x_axis = p.x[:, axis]

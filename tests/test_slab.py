@@ -270,3 +270,14 @@ def test_contact_problem_assembly_host_logic():
         k = int(keys[i])
         exp = v_C[pos[k]] if k in pos else vs[i] + P * (vk[i] - vs[i])
         assert torch.equal(va[i], exp)
+
+
+def test_slab_rejects_unknown_solve_and_cloth():
+    """from_state validates before touching any device state."""
+    from types import SimpleNamespace
+    st = SimpleNamespace(cloth=None)
+    with pytest.raises(ValueError):
+        S.SlabState.from_state(st, solve="bogus")
+    st = SimpleNamespace(cloth=SimpleNamespace(n_elements=3))
+    with pytest.raises(ValueError):
+        S.SlabState.from_state(st)
