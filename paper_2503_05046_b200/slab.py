@@ -797,11 +797,12 @@ def _fused_substep(ss: SlabState, sim, dt_s: float) -> dict:
     _lib.check(L.mpmrb_sim_substep_part(sim, 0))
     shared = None
     if c.world > 1:   # the halo reduce needs the block count before part 1
-        V = _views(sim)
-        nb = int(V.n_blocks)
-        N = nb * BLOCK_NODES
-        shared = _halo_sum(ss, _dev(V.block_keys, (nb,), torch.int64), _dev(V.mass, (N,)),
-                           _dev(V.mom_apic, (N, 3)), _dev(V.mom_force, (N, 3)))
+        with torch.cuda.nvtx.range("slab halo reduce"):
+            V = _views(sim)
+            nb = int(V.n_blocks)
+            N = nb * BLOCK_NODES
+            shared = _halo_sum(ss, _dev(V.block_keys, (nb,), torch.int64), _dev(V.mass, (N,)),
+                               _dev(V.mom_apic, (N, 3)), _dev(V.mom_force, (N, 3)))
     _lib.check(L.mpmrb_sim_substep_part(sim, 1))
     V = _views(sim)
     nb = int(V.n_blocks)
@@ -826,8 +827,9 @@ def _fused_substep(ss: SlabState, sim, dt_s: float) -> dict:
         cts = SimpleNamespace(n=nc, frames=_dev(V.frames, (nc, 3, 3)), bias=_dev(V.bias, (nc, 3)),
                               phi=_dev(V.phi, (nc,)), mu=_dev(V.mu, (nc,)),
                               gamma_lag=_dev(V.gamma_lag, (nc,)))
-        lp = _contact_problem(ss, act, coords, owned, loc, w, m_a, vs_a, vk_a)
-        v_C, P, gamma, report = _SOLVES[ss.solve](ss, lp, cts, dt_s)
+        with torch.cuda.nvtx.range(f"slab contact solve ({ss.solve})"):
+            lp = _contact_problem(ss, act, coords, owned, loc, w, m_a, vs_a, vk_a)
+            v_C, P, gamma, report = _SOLVES[ss.solve](ss, lp, cts, dt_s)
         _dev(V.v_next, (N, 3))[act] = _active_v_next(vs_a, vk_a, lp, v_C, P)
         if nc:
             _dev(V.gamma, (nc, 3)).copy_(gamma)
